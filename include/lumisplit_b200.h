@@ -1,0 +1,185 @@
+/*
+ * lumisplit_b200 -- C ABI of the B200-native alternating sparse-dense solver.
+ *
+ * Drop-in boundary for the hot path of the reference package `lumisplit`
+ * (/root/reference/pkg/src/lumisplit).  The reference is pure Python/NumPy
+ * and has no FFI of its own; each entry point below replaces one reference
+ * function (cited per declaration), and the Python host package
+ * `paper_1908_01961_b200` binds them with ctypes (INTEGRATION.md shows the
+ * binding a maintainer would add to the reference).
+ *
+ * Conventions
+ *   - Every array argument is caller-owned DEVICE memory unless the comment
+ *     says "host".  No allocation happens inside the per-iteration calls;
+ *     the context preallocates all workspace in ls_ctx_create.
+ *   - Layer state is ONE planar float32 buffer `X` of U = K+4 planes of H*W:
+ *     planes 0..2 are log-reflectance r (R, G, B), planes 3..K+3 are the
+ *     transport layers T_0 (direct) .. T_K.  The reference's (H, W, C)
+ *     arrays are the (C, H, W) planes viewed with a permutation; the PCG
+ *     vector [r.ravel(), T.ravel()] of solver.py:110-122 corresponds to the
+ *     same planes.  ls_pack_hwc / ls_unpack_hwc convert.
+ *   - Palettes are passed as host arrays of K*3 doubles (reference
+ *     BaseColorPalette.colors, palette.py:56-66); row 0 (white) is implicit.
+ *   - Status codes: LS_OK, LS_ERR_NONFINITE (-> NumericalFaultError),
+ *     LS_ERR_ARG (-> ValueError), LS_ERR_CUDA.  Nothing throws across the ABI.
+ *   - One context per stream; contexts share no mutable state, so separate
+ *     host threads may drive separate contexts (correction.py:185-196).
+ *   - Reductions run in a fixed order without float atomics: results are
+ *     bitwise repeatable for a given device.
+ */
+#ifndef LUMISPLIT_B200_H
+#define LUMISPLIT_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LS_API __attribute__((visibility("default")))
+#else
+#define LS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { LS_OK = 0, LS_ERR_NONFINITE = 1, LS_ERR_ARG = 2, LS_ERR_CUDA = 3 };
+enum { LS_NUM_TERMS = 8, LS_MAX_K = 12 };
+
+/* energy.py:28-56 (EnergyWeights); chroma_reg: 0 = "projection", 1 = "identity". */
+typedef struct {
+  double lambda_data, lambda_clustering, lambda_r_sparsity, p;
+  double lambda_r_consistency, lambda_monochrome, lambda_i_sparsity;
+  double lambda_smoothness, lambda_non_neg, lambda_ir, lambda_cr;
+  double eps_nonneg, eps_irls;
+  int chroma_reg;
+} ls_weights;
+
+/* solver.py:32-49 (the SolveConfig fields the device path consumes). */
+typedef struct {
+  int pcg_iterations;
+  int max_halvings;
+  double svd_truncation;
+  double max_delta_b;
+} ls_solve_cfg;
+
+/* One Gauss-Newton step record (solver.py:180-188).  Term order:
+ * data, clustering, r_sparsity, r_consistency, monochrome, i_sparsity,
+ * smoothness, non_neg (energy.py:197-448). */
+typedef struct {
+  double energy_before, energy_after, alpha;
+  int accepted;
+  int pcg_iterations;
+  double initial_residual, final_residual;
+  double terms_before[LS_NUM_TERMS];
+  double terms[LS_NUM_TERMS];
+} ls_gn_record;
+
+/* Dense base-color step record (solver.py:245-252). */
+typedef struct {
+  double energy_before, energy_after, alpha, delta_b_norm;
+  int accepted;
+  int solved_nonzero;
+} ls_dense_record;
+
+typedef struct ls_ctx ls_ctx;
+
+/* ---- context ----------------------------------------------------------- */
+LS_API const char* ls_version(void);
+LS_API const char* ls_last_error(void);
+LS_API int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w,
+                  const ls_solve_cfg* cfg, ls_ctx** out);
+LS_API int ls_ctx_destroy(ls_ctx* ctx);
+LS_API int ls_set_weights(ls_ctx* ctx, const ls_weights* w, const ls_solve_cfg* cfg);
+LS_API int ls_set_stream(ls_ctx* ctx, void* cuda_stream);
+
+/* ---- layout helpers ---------------------------------------------------- */
+/* (H, W, C) interleaved <-> C planes of H*W. */
+LS_API int ls_pack_hwc(ls_ctx* ctx, const float* hwc, int C, float* planes);
+LS_API int ls_unpack_hwc(ls_ctx* ctx, const float* planes, int C, float* hwc);
+
+/* ---- per-frame auxiliary context (solver.py:341-351, energy.py:455-475) -- */
+/* Frame image, (H, W, 3) float32 interleaved.  Computes the planar copy,
+ * chromaticity (imaging.py:160-171, fp64) and the chroma-edge gate
+ * (energy.py:121-136). */
+LS_API int ls_set_image(ls_ctx* ctx, const float* image_hwc);
+/* Draws the consistency partners on the device, bit-exact with
+ * sample_consistency (energy.py:154-187): numpy PCG64 stream given by its
+ * 128-bit (state, inc) -- the host passes np.random.PCG64(seed).state -- and
+ * 32-bit buffered Lemire bounded integers.  prev_chroma_planes (2 planes of
+ * fp64, as returned by ls_get_chroma for the previous frame) may be NULL
+ * (first frame: spatial pairs only); chroma_planes NULL means the installed
+ * image's chroma.  Builds the per-pixel adjacency. */
+LS_API int ls_sample_consistency(ls_ctx* ctx, const double* chroma_planes, const double* prev_chroma_planes,
+                          uint64_t state_hi, uint64_t state_lo,
+                          uint64_t inc_hi, uint64_t inc_lo, int64_t* n_pairs_out);
+/* Explicit partner rows (ConsistencySamples, energy.py:139-151); src/dst
+ * flat pixel indices (int64), temporal as uint8, weight may be NULL (all 1).
+ * Partners must lie in the 15x15 window (|dx|,|dy| <= 7) -> else LS_ERR_ARG. */
+LS_API int ls_set_pairs(ls_ctx* ctx, int64_t n, const int64_t* src, const int64_t* dst,
+                 const uint8_t* temporal, const double* weight);
+/* Copies the current partner rows out (host-visible sizes via n_pairs_out of
+ * ls_sample_consistency); arrays are device memory of length n. */
+LS_API int ls_get_pairs(ls_ctx* ctx, int64_t* src, int64_t* dst, uint8_t* temporal);
+/* Edge gate override (float32 H*W) -- for EnergyAux built by hand. */
+LS_API int ls_set_edge(ls_ctx* ctx, const float* edge);
+/* Previous frame log-reflectance (3 planes) or NULL. */
+LS_API int ls_set_prev_r(ls_ctx* ctx, const float* prev_r_planes);
+/* Clustered-reflectance anchor: cluster ids (int32 H*W, values 1..K) or a
+ * fixed log anchor (3 planes); exactly one non-NULL (energy.py:470-475). */
+LS_API int ls_set_anchor(ls_ctx* ctx, const int32_t* cluster_ids, const float* r_cluster_log_planes);
+LS_API int ls_get_edge(ls_ctx* ctx, float* edge_out);
+LS_API int ls_get_chroma(ls_ctx* ctx, double* chroma_planes_out);
+/* Context-free: chromaticity planes (fp64) of an (H, W, 3) image
+ * (imaging.py:160-171) and the chroma-edge gate of chroma planes
+ * (energy.py:121-136), on the given stream. */
+LS_API int ls_chromaticity(const float* image_hwc, int H, int W, double* chroma_planes_out,
+                           void* cuda_stream);
+LS_API int ls_edge_from_chroma(const double* chroma_planes, int H, int W, float* edge_out,
+                               void* cuda_stream);
+
+/* palette.py:195-224: nearest-chroma ids (int32 H*W, 1..K) of the current
+ * image with dark-pixel scanline inheritance. */
+LS_API int ls_segment(ls_ctx* ctx, const double* colors_host, int32_t* ids_out);
+/* solver.py:295-308 first-frame initialisation into X (U planes). */
+LS_API int ls_initialize(ls_ctx* ctx, const double* colors_host, const int32_t* ids, float* X);
+
+/* ---- energy operators (energy.py:194-511, solver.py:110-140) ------------ */
+/* Per-term energies at Y with IRLS weights and linearisation frozen at X
+ * (assemble_blocks at X, block_energies at Y).  Y may equal X. */
+LS_API int ls_energy_terms(ls_ctx* ctx, const double* colors_host, const float* X, const float* Y,
+                    double terms_out_host[LS_NUM_TERMS]);
+/* b = -J^T F and diag(J^T J) at X (solver.py:125-136); planar U*N float. */
+LS_API int ls_grad_diag(ls_ctx* ctx, const double* colors_host, const float* X, float* b, float* diag);
+/* Ap = J^T J p, operator frozen at X (solver.py:110-122). */
+LS_API int ls_apply_normal(ls_ctx* ctx, const double* colors_host, const float* X, const float* p,
+                    float* Ap);
+/* Jacobi PCG on the frozen normal equations (solver.py:79-107), x planar.
+ * info_host = {iterations, initial_residual, final_residual}. */
+LS_API int ls_pcg(ls_ctx* ctx, const double* colors_host, const float* X, int iterations, float* x,
+           double info_host[3]);
+
+/* ---- solver steps (solver.py:143-255) ---------------------------------- */
+/* One sparse Gauss-Newton step from X; the candidate state is written to
+ * X_out (accepted iff rec->accepted; otherwise X_out is unspecified).
+ * Returns LS_ERR_NONFINITE (rec->terms_before filled) for a non-finite
+ * starting energy (solver.py:153-157). */
+LS_API int ls_gn_step(ls_ctx* ctx, const double* colors_host, const float* X, float* X_out,
+               ls_gn_record* rec);
+/* Dense 3K x 3K refinement normal system at delta_b = 0 (energy.py:563-610);
+ * uses the cluster ids set by ls_set_anchor when use_ids != 0.  Host outputs. */
+LS_API int ls_dense_normal(ls_ctx* ctx, const double* colors_host, const float* X, int use_ids,
+                    double* A_host, double* rhs_host);
+/* Truncated-SVD minimum-norm solve (solver.py:195-204), one-sided Jacobi SVD
+ * in fp64 on the device.  n <= 3*LS_MAX_K, host arrays. */
+LS_API int ls_svd_solve(ls_ctx* ctx, int n, const double* A_host, const double* rhs_host,
+                 double truncation, double* x_host);
+/* solve_dense_block (solver.py:207-255): solve, trust cap, clipped line
+ * search on the frozen energy.  colors_inout_host (K*3) is updated iff
+ * accepted; applied_host (K*3) receives the applied update. */
+LS_API int ls_dense_step(ls_ctx* ctx, double* colors_inout_host, const float* X, double* applied_host,
+                  ls_dense_record* rec);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LUMISPLIT_B200_H */

@@ -1,0 +1,419 @@
+// Per-frame auxiliary kernels:
+//   image unpack + chromaticity (imaging.py:160-171), chroma-edge gate
+//   (energy.py:121-136), the consistency-partner sampler bit-exact with
+//   numpy's PCG64 + buffered Lemire draws (energy.py:154-187), the per-pixel
+//   adjacency (CSR) the solver kernels pull from, segmentation
+//   (palette.py:195-224) and first-frame initialisation (solver.py:295-308).
+//
+// Everything the reference computes in fp64 is computed here in fp64 with
+// explicitly rounded operations (no FMA contraction) where the result feeds
+// a comparison (chroma gate, nearest-palette argmin), so the integer outputs
+// (partners, cluster ids) are bit-identical to the reference.
+#include "ls_kernels.h"
+
+namespace ls {
+
+typedef unsigned __int128 u128;
+
+constexpr unsigned long long kPcgMultHi = 0x2360ED051FC65DA4ULL;
+constexpr unsigned long long kPcgMultLo = 0x4385DF649FCCF645ULL;
+
+__device__ __forceinline__ u128 mk128(unsigned long long hi, unsigned long long lo) {
+  return ((u128)hi << 64) | (u128)lo;
+}
+
+// XSL-RR 128/64 output function of numpy's PCG64
+__device__ __forceinline__ unsigned long long pcg_out(u128 s) {
+  const unsigned rot = (unsigned)(s >> 122);
+  const unsigned long long x = (unsigned long long)(s >> 64) ^ (unsigned long long)s;
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+// state after `delta` LCG steps (Brown's jump-ahead)
+__device__ __forceinline__ u128 pcg_advance(u128 state, u128 inc, unsigned long long delta) {
+  u128 cur_mult = mk128(kPcgMultHi, kPcgMultLo), cur_plus = inc;
+  u128 acc_mult = 1, acc_plus = 0;
+  while (delta > 0) {
+    if (delta & 1ULL) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return acc_mult * state + acc_plus;
+}
+
+// sequential reader of the u32 stream (low half of each 64-bit output first)
+struct U32Stream {
+  u128 state, inc;
+  unsigned long long cur;
+  int half;
+  __device__ void seek(u128 s0, u128 inc_, unsigned long long pos) {
+    inc = inc_;
+    state = pcg_advance(s0, inc, (pos >> 1) + 1);   // outputs come from the stepped state
+    cur = pcg_out(state);
+    half = (int)(pos & 1ULL);
+  }
+  __device__ unsigned next() {
+    unsigned v;
+    if (half) {
+      v = (unsigned)(cur >> 32);
+      state = state * mk128(kPcgMultHi, kPcgMultLo) + inc;
+      cur = pcg_out(state);
+      half = 0;
+    } else {
+      v = (unsigned)(cur & 0xffffffffULL);
+      half = 1;
+    }
+    return v;
+  }
+};
+
+__device__ __forceinline__ unsigned long long shifted_pos(const SampleParams& P, unsigned long long j) {
+  unsigned long long s = j;
+  for (int t = 0; t < P.nz; ++t)
+    if ((unsigned long long)P.z[t] < s) ++s;
+    else break;
+  return s;
+}
+
+__device__ __forceinline__ bool known_zero(const SampleParams& P, unsigned long long pos) {
+  for (int t = 0; t < P.nz; ++t)
+    if ((unsigned long long)P.z[t] == pos) return true;
+  return false;
+}
+
+// ---- layout helpers -------------------------------------------------------
+__global__ void k_pack(const float* __restrict__ hwc, int C, int N, float* __restrict__ planes) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)C * N;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / N), i = (int)(e % N);
+    planes[e] = hwc[(int64_t)i * C + c];
+  }
+}
+__global__ void k_unpack(const float* __restrict__ planes, int C, int N, float* __restrict__ hwc) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)C * N;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / C), c = (int)(e % C);
+    hwc[e] = planes[(int64_t)c * N + i];
+  }
+}
+
+// ---- chromaticity (imaging.py:160-171) -------------------------------------
+__global__ void k_image(const float* __restrict__ hwc, int N, float* __restrict__ img, double* __restrict__ chroma) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const float r = hwc[3 * i], g = hwc[3 * i + 1], b = hwc[3 * i + 2];
+    if (img) {
+      img[i] = r;
+      img[N + i] = g;
+      img[2 * N + i] = b;
+    }
+    const double s = __dadd_rn(__dadd_rn((double)r, (double)g), (double)b);
+    double c0, c1;
+    if (s < 0.02) {
+      c0 = c1 = 1.0 / 3.0;
+    } else {
+      c0 = __ddiv_rn((double)r, s);
+      c1 = __ddiv_rn((double)g, s);
+    }
+    chroma[i] = c0;
+    chroma[N + i] = c1;
+  }
+}
+
+__device__ __forceinline__ double norm2d(double a, double b) {
+  return __dsqrt_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)));
+}
+
+// ---- chroma-edge gate (energy.py:121-136) ----------------------------------
+__global__ void k_edge(const double* __restrict__ ch, int H, int W, float* __restrict__ edge) {
+  const int N = H * W;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const int x = i % W, y = i / W;
+    const double c0 = ch[i], c1 = ch[N + i];
+    double d = 0.0;
+    if (x < W - 1) d = fmax(d, norm2d(__dsub_rn(ch[i + 1], c0), __dsub_rn(ch[N + i + 1], c1)));
+    if (x > 0) d = fmax(d, norm2d(__dsub_rn(c0, ch[i - 1]), __dsub_rn(c1, ch[N + i - 1])));
+    if (y < H - 1) d = fmax(d, norm2d(__dsub_rn(ch[i + W], c0), __dsub_rn(ch[N + i + W], c1)));
+    if (y > 0) d = fmax(d, norm2d(__dsub_rn(c0, ch[i - W]), __dsub_rn(c1, ch[N + i - W])));
+    edge[i] = (float)(1.0 - exp(-50.0 * d));
+  }
+}
+
+// ---- consistency sampler (energy.py:154-187) --------------------------------
+// codes[4p+s] = -1 (dropped) or offset code | temporal<<8 for pixel p, slot s.
+__global__ void k_sample(SampleParams P, const double* __restrict__ ch, const double* __restrict__ pch, int H,
+                         int W, int16_t* __restrict__ codes, int32_t* __restrict__ out_cnt,
+                         int32_t* __restrict__ in_cnt, unsigned long long* new_zero) {
+  const int N = H * W;
+  const u128 s0 = mk128(P.st_hi, P.st_lo), inc = mk128(P.inc_hi, P.inc_lo);
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
+    const int x = p % W, y = p / W;
+    int dxv[4], dyv[4], tv[4] = {0, 0, 0, 0};
+    U32Stream st;
+    // dx then dy: rng.integers(-7, 8, size=(n, 4)) -> Lemire on range 15,
+    // reject iff (u * 15) mod 2^32 < (2^32 mod 15) = 1, i.e. u == 0
+    for (int sec = 0; sec < 2; ++sec) {
+      unsigned long long pos = shifted_pos(P, (unsigned long long)sec * 4ULL * N + 4ULL * p);
+      st.seek(s0, inc, pos);
+      int got = 0;
+      while (got < 4) {
+        const unsigned u = st.next();
+        if (u == 0u) {
+          if (!known_zero(P, pos)) atomicMin(new_zero, pos);
+          ++pos;
+          continue;
+        }
+        ++pos;
+        const int v = (int)(((unsigned long long)u * 15ULL) >> 32) - kHalf;
+        if (sec == 0) dxv[got] = v; else dyv[got] = v;
+        ++got;
+      }
+    }
+    if (P.has_prev) {   // rng.integers(0, 2): Lemire threshold 0, no rejection
+      st.seek(s0, inc, shifted_pos(P, 8ULL * N + 4ULL * p));
+      for (int k = 0; k < 4; ++k) tv[k] = (int)(((unsigned long long)st.next() * 2ULL) >> 32);
+    }
+    const double c0 = ch[p], c1 = ch[N + p];
+    int cnt = 0;
+    for (int k = 0; k < 4; ++k) {
+      const int px = clampi(x + dxv[k], 0, W - 1), py = clampi(y + dyv[k], 0, H - 1);
+      const int q = py * W + px;
+      const double* src = tv[k] ? pch : ch;
+      const double dist = norm2d(__dsub_rn(c0, src[q]), __dsub_rn(c1, src[N + q]));
+      const bool keep = (dist < 0.05) && (tv[k] || q != p);
+      int16_t code = -1;
+      if (keep) {
+        code = (int16_t)(((py - y + kHalf) * kWin + (px - x + kHalf)) | (tv[k] ? kEntTemporal : 0));
+        ++cnt;
+        if (!tv[k]) atomicAdd(in_cnt + q, 1);
+      }
+      codes[4 * p + k] = code;
+    }
+    out_cnt[p] = cnt;
+  }
+}
+
+__global__ void k_degree(int N, const int32_t* a, const int32_t* b, int32_t* deg) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) deg[i] = a[i] + b[i];
+}
+
+// out entries in slot order (keys 0..3), incoming entries keyed by 4 + 4*src + slot
+__global__ void k_fill_samples(const int16_t* __restrict__ codes, int H, int W, const int32_t* __restrict__ row_ptr,
+                               int32_t* fill, uint16_t* ent, uint32_t* key) {
+  const int N = H * W;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
+    const int x = p % W, y = p / W;
+    for (int k = 0; k < 4; ++k) {
+      const int16_t c = codes[4 * p + k];
+      if (c < 0) continue;
+      const int pos = atomicAdd(fill + p, 1);
+      ent[row_ptr[p] + pos] = (uint16_t)c;
+      key[row_ptr[p] + pos] = (uint32_t)k;
+      if (!(c & kEntTemporal)) {
+        const int code = c & 0xff;
+        const int dy = code / kWin - kHalf, dx = code % kWin - kHalf;
+        const int q = (y + dy) * W + (x + dx);
+        const int pq = atomicAdd(fill + q, 1);
+        ent[row_ptr[q] + pq] = (uint16_t)(((-dy + kHalf) * kWin + (-dx + kHalf)) | kEntIncoming);
+        key[row_ptr[q] + pq] = 4u + 4u * (uint32_t)p + (uint32_t)k;
+      }
+    }
+  }
+}
+
+__global__ void k_pairs_count(int64_t n, const int64_t* src, const int64_t* dst, const uint8_t* temporal, int H,
+                              int W, int32_t* out_cnt, int32_t* in_cnt, int* bad) {
+  const int N = H * W;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = src[e], d = dst[e];
+    if (s < 0 || s >= N || d < 0 || d >= N) { *bad = 1; continue; }
+    const int dy = (int)(d / W) - (int)(s / W), dx = (int)(d % W) - (int)(s % W);
+    if (dy < -kHalf || dy > kHalf || dx < -kHalf || dx > kHalf) { *bad = 1; continue; }
+    atomicAdd(out_cnt + s, 1);
+    if (!temporal[e]) atomicAdd(in_cnt + d, 1);
+  }
+}
+
+__global__ void k_fill_pairs(int64_t n, const int64_t* src, const int64_t* dst, const uint8_t* temporal,
+                             const double* weight, int W, const int32_t* row_ptr, int32_t* fill, uint16_t* ent,
+                             uint32_t* key, float* ent_w) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)src[e], d = (int)dst[e];
+    const int dy = d / W - s / W, dx = d % W - s % W;
+    const bool t = temporal[e] != 0;
+    const float wv = weight ? (float)weight[e] : 1.f;
+    int pos = atomicAdd(fill + s, 1);
+    ent[row_ptr[s] + pos] = (uint16_t)(((dy + kHalf) * kWin + (dx + kHalf)) | (t ? kEntTemporal : 0));
+    key[row_ptr[s] + pos] = (uint32_t)e;
+    if (ent_w) ent_w[row_ptr[s] + pos] = wv;
+    if (!t) {
+      pos = atomicAdd(fill + d, 1);
+      ent[row_ptr[d] + pos] = (uint16_t)(((-dy + kHalf) * kWin + (-dx + kHalf)) | kEntIncoming);
+      key[row_ptr[d] + pos] = (uint32_t)(n + e);
+      if (ent_w) ent_w[row_ptr[d] + pos] = wv;
+    }
+  }
+}
+
+// deterministic order inside each adjacency row (insertion sort by key)
+__global__ void k_sort_rows(int N, const int32_t* __restrict__ row_ptr, uint16_t* ent, uint32_t* key, float* ent_w) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
+    const int a = row_ptr[p], b = row_ptr[p + 1];
+    for (int i = a + 1; i < b; ++i) {
+      const uint32_t k = key[i];
+      const uint16_t e = ent[i];
+      const float w = ent_w ? ent_w[i] : 0.f;
+      int j = i - 1;
+      while (j >= a && key[j] > k) {
+        key[j + 1] = key[j];
+        ent[j + 1] = ent[j];
+        if (ent_w) ent_w[j + 1] = ent_w[j];
+        --j;
+      }
+      key[j + 1] = k;
+      ent[j + 1] = e;
+      if (ent_w) ent_w[j + 1] = w;
+    }
+  }
+}
+
+__global__ void k_pairs_from_samples(const int16_t* __restrict__ codes, int H, int W, const int32_t* __restrict__ off,
+                                     int64_t* src, int64_t* dst, uint8_t* temporal) {
+  const int N = H * W;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
+    int o = off[p];
+    const int x = p % W, y = p / W;
+    for (int k = 0; k < 4; ++k) {
+      const int16_t c = codes[4 * p + k];
+      if (c < 0) continue;
+      const int code = c & 0xff;
+      const int dy = code / kWin - kHalf, dx = code % kWin - kHalf;
+      src[o] = p;
+      dst[o] = (int64_t)(y + dy) * W + (x + dx);
+      temporal[o] = (c & kEntTemporal) ? 1 : 0;
+      ++o;
+    }
+  }
+}
+
+// ---- segmentation (palette.py:195-224) --------------------------------------
+__global__ void k_segment_raw(const float* __restrict__ img, const double* __restrict__ ch, int N, int K,
+                              const double* __restrict__ pal, int32_t* ids_raw, int32_t* key, int* first_valid) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const double c0 = ch[i], c1 = ch[N + i];
+    int best = 0;
+    double bd = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const double d = norm2d(__dsub_rn(c0, pal[2 * k]), __dsub_rn(c1, pal[2 * k + 1]));
+      if (k == 0 || d < bd) { bd = d; best = k; }    // argmin: first minimum wins
+    }
+    ids_raw[i] = best + 1;
+    const double s = __dadd_rn(__dadd_rn((double)img[i], (double)img[N + i]), (double)img[2 * N + i]);
+    const bool dark = s < 0.02;
+    key[i] = dark ? -1 : i;
+    if (!dark) atomicMin(first_valid, i);
+  }
+}
+
+__global__ void k_segment_final(int N, const int32_t* __restrict__ ids_raw, const int32_t* __restrict__ last,
+                                const int* first_valid, int32_t* ids) {
+  const int fv = *first_valid;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    if (fv >= N) { ids[i] = 1; continue; }            // every pixel dark
+    int l = last[i];
+    if (l < 0) l = fv;
+    ids[i] = ids_raw[l];
+  }
+}
+
+// ---- first-frame initialisation (solver.py:295-308) ------------------------
+__global__ void k_initialize(const float* __restrict__ img, const int32_t* __restrict__ ids, int N, int NT,
+                             const double* __restrict__ colors, float* __restrict__ X) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const int id = ids[i] - 1;
+    double ratio_sum = 0.0;
+    for (int c = 0; c < 3; ++c) {
+      const double rc = colors[3 * id + c];
+      const double fl = rc > 1e-4 ? rc : 1e-4;
+      X[(size_t)c * N + i] = (float)log(fl);
+      ratio_sum += (double)img[(size_t)c * N + i] / fl;
+    }
+    double t0 = ratio_sum / 3.0;
+    t0 = t0 < 0.0 ? 0.0 : (t0 > 2.0 ? 2.0 : t0);
+    X[(size_t)3 * N + i] = (float)t0;
+    for (int k = 1; k < NT; ++k) X[(size_t)(3 + k) * N + i] = 0.f;
+  }
+}
+
+__global__ void k_set_i32(int32_t* p, int n, int32_t v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
+}
+
+// ---- launchers ---------------------------------------------------------------
+static inline int grid_for(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 65535) g = 65535;
+  return (int)g;
+}
+
+void launch_pack_hwc(cudaStream_t s, const float* hwc, int C, int N, float* planes) {
+  k_pack<<<grid_for((int64_t)C * N), 256, 0, s>>>(hwc, C, N, planes);
+}
+void launch_unpack_hwc(cudaStream_t s, const float* planes, int C, int N, float* hwc) {
+  k_unpack<<<grid_for((int64_t)C * N), 256, 0, s>>>(planes, C, N, hwc);
+}
+void launch_image(cudaStream_t s, const float* hwc, int N, float* img, double* chroma) {
+  k_image<<<grid_for(N), 256, 0, s>>>(hwc, N, img, chroma);
+}
+void launch_edge(cudaStream_t s, const double* chroma, int H, int W, float* edge) {
+  k_edge<<<grid_for((int64_t)H * W), 256, 0, s>>>(chroma, H, W, edge);
+}
+void launch_sample(cudaStream_t s, const SampleParams& P, const double* chroma, const double* prev_chroma, int H,
+                   int W, int16_t* codes, int32_t* out_cnt, int32_t* in_cnt, unsigned long long* new_zero) {
+  k_sample<<<grid_for((int64_t)H * W, 128), 128, 0, s>>>(P, chroma, prev_chroma, H, W, codes, out_cnt, in_cnt,
+                                                        new_zero);
+}
+void launch_pairs_count(cudaStream_t s, int64_t n, const int64_t* src, const int64_t* dst, const uint8_t* temporal,
+                        int H, int W, int32_t* out_cnt, int32_t* in_cnt, int* bad) {
+  if (n > 0) k_pairs_count<<<grid_for(n), 256, 0, s>>>(n, src, dst, temporal, H, W, out_cnt, in_cnt, bad);
+}
+void launch_degree(cudaStream_t s, int N, const int32_t* a, const int32_t* b, int32_t* deg) {
+  k_degree<<<grid_for(N), 256, 0, s>>>(N, a, b, deg);
+}
+void launch_fill_from_samples(cudaStream_t s, const int16_t* codes, int H, int W, const int32_t* row_ptr,
+                              int32_t* fill, uint16_t* ent, uint32_t* key) {
+  k_fill_samples<<<grid_for((int64_t)H * W), 256, 0, s>>>(codes, H, W, row_ptr, fill, ent, key);
+}
+void launch_fill_from_pairs(cudaStream_t s, int64_t n, const int64_t* src, const int64_t* dst,
+                            const uint8_t* temporal, const double* weight, int W, const int32_t* row_ptr,
+                            int32_t* fill, uint16_t* ent, uint32_t* key, float* ent_w) {
+  if (n > 0) k_fill_pairs<<<grid_for(n), 256, 0, s>>>(n, src, dst, temporal, weight, W, row_ptr, fill, ent, key, ent_w);
+}
+void launch_sort_rows(cudaStream_t s, int N, const int32_t* row_ptr, uint16_t* ent, uint32_t* key, float* ent_w) {
+  k_sort_rows<<<grid_for(N), 256, 0, s>>>(N, row_ptr, ent, key, ent_w);
+}
+void launch_pairs_from_samples(cudaStream_t s, const int16_t* codes, int H, int W, const int32_t* off, int64_t* src,
+                               int64_t* dst, uint8_t* temporal) {
+  k_pairs_from_samples<<<grid_for((int64_t)H * W), 256, 0, s>>>(codes, H, W, off, src, dst, temporal);
+}
+void launch_segment_raw(cudaStream_t s, const float* img, const double* chroma, int N, int K, const double* pal,
+                        int32_t* ids_raw, int32_t* key, int* first_valid) {
+  k_segment_raw<<<grid_for(N), 256, 0, s>>>(img, chroma, N, K, pal, ids_raw, key, first_valid);
+}
+void launch_segment_final(cudaStream_t s, int N, const int32_t* ids_raw, const int32_t* last, const int* first_valid,
+                          int32_t* ids) {
+  k_segment_final<<<grid_for(N), 256, 0, s>>>(N, ids_raw, last, first_valid, ids);
+}
+void launch_initialize(cudaStream_t s, const float* img, const int32_t* ids, int N, int NT, const double* colors,
+                       float* X) {
+  k_initialize<<<grid_for(N), 256, 0, s>>>(img, ids, N, NT, colors, X);
+}
+void launch_set_i32(cudaStream_t s, int32_t* p, int n, int32_t v) {
+  k_set_i32<<<grid_for(n), 256, 0, s>>>(p, n, v);
+}
+
+}  // namespace ls

@@ -1,0 +1,740 @@
+// Context, workspace and the C ABI (include/lumisplit_b200.h).
+//
+// The context owns every device buffer the hot path touches, allocated once
+// in ls_ctx_create: no cudaMalloc in the per-frame or per-step calls (the
+// adjacency is regrown only if a hand-made pair list outgrows it).  The
+// Gauss-Newton step is orchestrated here, natively: 1 fused energy/gradient
+// kernel, PCG iterations of (apply, update) with device-resident scalars,
+// and line-search trials; the host synchronises once per trial to read the
+// energies (the accept/reject branch of solver.py:169-178).
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lumisplit_b200.h"
+#include "ls_kernels.h"
+
+using namespace ls;
+
+static thread_local std::string g_err;
+
+#define LS_CK(call)                                                         \
+  do {                                                                      \
+    cudaError_t e_ = (call);                                                \
+    if (e_ != cudaSuccess) {                                                \
+      g_err = std::string(#call) + ": " + cudaGetErrorString(e_);           \
+      return LS_ERR_CUDA;                                                   \
+    }                                                                       \
+  } while (0)
+
+#define LS_ARG(cond, msg)        \
+  do {                           \
+    if (!(cond)) {               \
+      g_err = (msg);             \
+      return LS_ERR_ARG;         \
+    }                            \
+  } while (0)
+
+struct MaxOp {
+  __host__ __device__ int operator()(int a, int b) const { return a > b ? a : b; }
+};
+
+struct ls_ctx {
+  int dev = 0, H = 0, W = 0, N = 0, K = 0, NT = 0, U = 0;
+  ls_weights w{};
+  ls_solve_cfg cfg{};
+  cudaStream_t stream = nullptr;
+  int nsm = 0, ntiles = 0, grid_energy = 0, grid_apply = 0, grid_update = 0, grid_dense = 0;
+  // per-frame aux
+  float* img = nullptr;
+  double* chroma = nullptr;
+  double* prev_chroma = nullptr;
+  float* scratch_img = nullptr;
+  float* edge = nullptr;
+  int32_t* ids = nullptr;
+  float* anchor = nullptr;
+  float* prev_r = nullptr;
+  bool has_image = false, has_ids = false, has_anchor = false, has_prev_r = false;
+  // adjacency
+  int32_t* row_ptr = nullptr;
+  uint16_t* ent = nullptr;
+  float* ent_w = nullptr;
+  uint32_t* key = nullptr;
+  int64_t ent_cap = 0;
+  bool has_ent_w = false, has_pairs = false, pairs_from_sampler = false;
+  int64_t n_pairs = 0;
+  int n_temporal = 0;
+  int16_t* codes = nullptr;
+  int32_t *out_cnt = nullptr, *in_cnt = nullptr, *deg = nullptr, *fill = nullptr, *pair_off = nullptr;
+  int* small_i = nullptr;                     // [0] bad flag, [1] temporal count, [2] first_valid
+  unsigned long long* zero_flag = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  int32_t *seg_raw = nullptr, *seg_key = nullptr, *seg_last = nullptr;
+  double* pal_chroma = nullptr;
+  // PCG workspace
+  float *r = nullptr, *d = nullptr, *u = nullptr, *wv = nullptr, *p = nullptr, *s = nullptr, *x = nullptr;
+  double* part = nullptr;
+  size_t part_len = 0;
+  unsigned* tickets = nullptr;
+  Scalars* sc = nullptr;
+  Scalars* sc_host = nullptr;
+  // dense
+  double *dense_sums = nullptr, *colors_dev = nullptr, *dense_A = nullptr, *dense_rhs = nullptr,
+         *dense_x = nullptr;
+  double* host_buf = nullptr;   // pinned, 2 * 36 * 36 + 64 doubles
+  std::vector<void*> allocs;
+};
+
+template <typename T>
+static cudaError_t dalloc(ls_ctx* c, T** p, size_t n) {
+  cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T));
+  if (e == cudaSuccess) c->allocs.push_back((void*)*p);
+  return e;
+}
+
+template <typename R>
+static Coef<R> make_coef(const ls_weights& w, const double* colors, int K) {
+  Coef<R> c;
+  std::memset(&c, 0, sizeof(c));
+  for (int k = 0; k <= K; ++k) {
+    double b[3];
+    for (int ch = 0; ch < 3; ++ch) b[ch] = (k == 0) ? 1.0 : colors[3 * (k - 1) + ch];
+    const double mean = ((b[0] + b[1]) + b[2]) / 3.0;
+    for (int ch = 0; ch < 3; ++ch) {
+      c.B[k][ch] = (R)b[ch];
+      c.G[k][ch] = (R)(b[ch] - mean);
+      c.anchor[k][ch] = (k == 0) ? R(0) : (R)std::log(std::max(b[ch], 1e-4));
+    }
+  }
+  c.lam_d = (R)w.lambda_data;
+  c.lam_cl = (R)w.lambda_clustering;
+  c.lam_rs = (R)w.lambda_r_sparsity;
+  c.p = (R)w.p;
+  c.lam_rc = (R)w.lambda_r_consistency;
+  c.lam_m = (R)w.lambda_monochrome;
+  c.lam_is = (R)w.lambda_i_sparsity;
+  c.lam_sm = (R)w.lambda_smoothness;
+  c.lam_nn = (R)w.lambda_non_neg;
+  c.eps_nn = (R)w.eps_nonneg;
+  c.eps_irls = (R)w.eps_irls;
+  c.inv_eps = (R)(1.0 / w.eps_irls);
+  c.floor_rs = (R)(w.p < 2.0 ? std::pow(w.eps_irls, 1.0 / (2.0 - w.p)) : 0.0);
+  return c;
+}
+
+static Frame frame_of(const ls_ctx* c) {
+  Frame f;
+  f.H = c->H;
+  f.W = c->W;
+  f.N = c->N;
+  f.NT = c->NT;
+  f.img = c->img;
+  f.edge = c->edge;
+  f.ids = c->has_ids ? c->ids : nullptr;
+  f.anchor = c->has_anchor ? c->anchor : nullptr;
+  f.prev_r = c->has_prev_r ? c->prev_r : nullptr;
+  f.row_ptr = c->row_ptr;
+  f.ent = c->ent;
+  f.ent_w = c->has_ent_w ? c->ent_w : nullptr;
+  return f;
+}
+
+static int check_ready(ls_ctx* c) {
+  LS_ARG(c != nullptr, "null context");
+  LS_ARG(c->has_image, "no frame image set (ls_set_image)");
+  LS_ARG(c->has_pairs, "no consistency partners (ls_sample_consistency / ls_set_pairs)");
+  LS_ARG(c->has_ids || c->has_anchor, "EnergyAux needs cluster_ids or r_cluster_log");
+  LS_ARG(c->n_temporal == 0 || c->has_prev_r, "temporal partners need the previous frame's reflectance");
+  return LS_OK;
+}
+
+extern "C" {
+
+const char* ls_version(void) { return "lumisplit_b200 0.1 (sm_100a)"; }
+const char* ls_last_error(void) { return g_err.c_str(); }
+
+int ls_set_weights(ls_ctx* c, const ls_weights* w, const ls_solve_cfg* cfg) {
+  LS_ARG(c && w && cfg, "null argument");
+  LS_ARG(w->eps_irls > 0.0, "eps_irls must be positive");
+  LS_ARG(cfg->pcg_iterations >= 0 && cfg->max_halvings >= 0, "bad solve config");
+  c->w = *w;
+  c->cfg = *cfg;
+  return LS_OK;
+}
+
+int ls_set_stream(ls_ctx* c, void* stream) {
+  LS_ARG(c, "null context");
+  c->stream = (cudaStream_t)stream;
+  return LS_OK;
+}
+
+int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls_solve_cfg* cfg, ls_ctx** out) {
+  LS_ARG(out && w && cfg, "null argument");
+  LS_ARG(H >= 1 && W >= 1 && (int64_t)H * W < (1LL << 28), "bad frame size");
+  LS_ARG(K >= 0 && K <= LS_MAX_K, "K must be in [0, 12]");
+  LS_CK(cudaSetDevice(device));
+  ls_ctx* c = new ls_ctx();
+  c->dev = device;
+  c->H = H;
+  c->W = W;
+  c->N = H * W;
+  c->K = K;
+  c->NT = K + 1;
+  c->U = K + 4;
+  int rc = ls_set_weights(c, w, cfg);
+  if (rc != LS_OK) { delete c; return rc; }
+  cudaDeviceProp prop;
+  LS_CK(cudaGetDeviceProperties(&prop, device));
+  c->nsm = prop.multiProcessorCount;
+  const int N = c->N, U = c->U;
+  const int64_t M = (int64_t)U * N;
+  c->ntiles = ((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH);
+  c->grid_energy = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, energy_grid_limit(c->NT)), kMaxBlocks}));
+  c->grid_apply = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, apply_grid_limit(c->NT)), kMaxBlocks}));
+  const int64_t upd_blocks = (M / 4 + kThreads - 1) / kThreads;
+  c->grid_update = (int)std::max<int64_t>(1, std::min<int64_t>({upd_blocks, (int64_t)c->nsm * std::max(1, update_grid_limit()), (int64_t)kMaxBlocks}));
+  c->grid_dense = std::max(1, std::min(c->nsm * 4, (N + 127) / 128));
+  cudaError_t e = cudaSuccess;
+#define A_(expr) \
+  if (e == cudaSuccess) e = (expr)
+  A_(dalloc(c, &c->img, 3 * (size_t)N));
+  A_(dalloc(c, &c->chroma, 2 * (size_t)N));
+  A_(dalloc(c, &c->prev_chroma, 2 * (size_t)N));
+  A_(dalloc(c, &c->scratch_img, 3 * (size_t)N));
+  A_(dalloc(c, &c->edge, (size_t)N));
+  A_(dalloc(c, &c->ids, (size_t)N));
+  A_(dalloc(c, &c->anchor, 3 * (size_t)N));
+  A_(dalloc(c, &c->prev_r, 3 * (size_t)N));
+  A_(dalloc(c, &c->row_ptr, (size_t)N + 1));
+  c->ent_cap = 8 * (int64_t)N + 16;
+  A_(cudaMalloc((void**)&c->ent, sizeof(uint16_t) * c->ent_cap));
+  A_(cudaMalloc((void**)&c->ent_w, sizeof(float) * c->ent_cap));
+  A_(cudaMalloc((void**)&c->key, sizeof(uint32_t) * c->ent_cap));
+  A_(dalloc(c, &c->codes, 4 * (size_t)N));
+  A_(dalloc(c, &c->out_cnt, (size_t)N + 1));
+  A_(dalloc(c, &c->in_cnt, (size_t)N + 1));
+  A_(dalloc(c, &c->deg, (size_t)N + 1));
+  A_(dalloc(c, &c->fill, (size_t)N + 1));
+  A_(dalloc(c, &c->pair_off, (size_t)N + 1));
+  A_(dalloc(c, &c->small_i, 8));
+  A_(dalloc(c, &c->zero_flag, 1));
+  A_(dalloc(c, &c->seg_raw, (size_t)N));
+  A_(dalloc(c, &c->seg_key, (size_t)N));
+  A_(dalloc(c, &c->seg_last, (size_t)N));
+  A_(dalloc(c, &c->pal_chroma, 2 * LS_MAX_K));
+  for (float** v : {&c->r, &c->d, &c->u, &c->wv, &c->p, &c->s, &c->x}) A_(dalloc(c, v, (size_t)M));
+  c->part_len = std::max<size_t>((size_t)kMaxBlocks * 12, (size_t)c->grid_dense * 320);
+  A_(dalloc(c, &c->part, c->part_len));
+  A_(dalloc(c, &c->tickets, 8));
+  A_(dalloc(c, &c->sc, 1));
+  A_(dalloc(c, &c->dense_sums, 512));
+  A_(dalloc(c, &c->colors_dev, 3 * LS_MAX_K));
+  A_(dalloc(c, &c->dense_A, 36 * 36));
+  A_(dalloc(c, &c->dense_rhs, 36));
+  A_(dalloc(c, &c->dense_x, 36));
+  A_(cudaMallocHost((void**)&c->sc_host, sizeof(Scalars)));
+  A_(cudaMallocHost((void**)&c->host_buf, sizeof(double) * (2 * 36 * 36 + 64)));
+  A_(cudaMemset(c->tickets, 0, 8 * sizeof(unsigned)));
+  A_(cudaMemset(c->sc, 0, sizeof(Scalars)));
+  // CUB scratch: max of the int exclusive-sum over N+1 and the max-scan over N
+  size_t b1 = 0, b2 = 0;
+  A_(cub::DeviceScan::ExclusiveSum(nullptr, b1, c->deg, c->row_ptr, N + 1));
+  A_(cub::DeviceScan::InclusiveScan(nullptr, b2, c->seg_key, c->seg_last, MaxOp(), N));
+  c->cub_bytes = std::max(b1, b2);
+  A_(dalloc(c, (char**)&c->cub_tmp, c->cub_bytes));
+#undef A_
+  if (e != cudaSuccess) {
+    g_err = std::string("ls_ctx_create: ") + cudaGetErrorString(e);
+    ls_ctx_destroy(c);
+    return LS_ERR_CUDA;
+  }
+  *out = c;
+  return LS_OK;
+}
+
+int ls_ctx_destroy(ls_ctx* c) {
+  if (!c) return LS_OK;
+  cudaSetDevice(c->dev);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->allocs) cudaFree(p);
+  cudaFree(c->ent);
+  cudaFree(c->ent_w);
+  cudaFree(c->key);
+  if (c->sc_host) cudaFreeHost(c->sc_host);
+  if (c->host_buf) cudaFreeHost(c->host_buf);
+  delete c;
+  return LS_OK;
+}
+
+int ls_pack_hwc(ls_ctx* c, const float* hwc, int C, float* planes) {
+  LS_ARG(c && hwc && planes && C > 0, "bad arguments");
+  launch_pack_hwc(c->stream, hwc, C, c->N, planes);
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_unpack_hwc(ls_ctx* c, const float* planes, int C, float* hwc) {
+  LS_ARG(c && hwc && planes && C > 0, "bad arguments");
+  launch_unpack_hwc(c->stream, planes, C, c->N, hwc);
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_set_image(ls_ctx* c, const float* image_hwc) {
+  LS_ARG(c && image_hwc, "bad arguments");
+  LS_CK(cudaSetDevice(c->dev));
+  launch_image(c->stream, image_hwc, c->N, c->img, c->chroma);
+  launch_edge(c->stream, c->chroma, c->H, c->W, c->edge);
+  LS_CK(cudaGetLastError());
+  c->has_image = true;
+  return LS_OK;
+}
+
+int ls_set_edge(ls_ctx* c, const float* edge) {
+  LS_ARG(c && edge, "bad arguments");
+  LS_CK(cudaMemcpyAsync(c->edge, edge, sizeof(float) * c->N, cudaMemcpyDeviceToDevice, c->stream));
+  return LS_OK;
+}
+
+int ls_get_edge(ls_ctx* c, float* out) {
+  LS_ARG(c && out, "bad arguments");
+  LS_CK(cudaMemcpyAsync(out, c->edge, sizeof(float) * c->N, cudaMemcpyDeviceToDevice, c->stream));
+  return LS_OK;
+}
+
+int ls_get_chroma(ls_ctx* c, double* out) {
+  LS_ARG(c && out, "bad arguments");
+  LS_CK(cudaMemcpyAsync(out, c->chroma, sizeof(double) * 2 * c->N, cudaMemcpyDeviceToDevice, c->stream));
+  return LS_OK;
+}
+
+int ls_set_prev_r(ls_ctx* c, const float* prev) {
+  LS_ARG(c, "null context");
+  if (!prev) {
+    c->has_prev_r = false;
+    return LS_OK;
+  }
+  LS_CK(cudaMemcpyAsync(c->prev_r, prev, sizeof(float) * 3 * c->N, cudaMemcpyDeviceToDevice, c->stream));
+  c->has_prev_r = true;
+  return LS_OK;
+}
+
+int ls_set_anchor(ls_ctx* c, const int32_t* ids, const float* anchor) {
+  LS_ARG(c, "null context");
+  LS_ARG((ids != nullptr) != (anchor != nullptr), "exactly one of cluster_ids / r_cluster_log");
+  if (ids) {
+    LS_CK(cudaMemcpyAsync(c->ids, ids, sizeof(int32_t) * c->N, cudaMemcpyDeviceToDevice, c->stream));
+    c->has_ids = true;
+    c->has_anchor = false;
+  } else {
+    LS_CK(cudaMemcpyAsync(c->anchor, anchor, sizeof(float) * 3 * c->N, cudaMemcpyDeviceToDevice, c->stream));
+    c->has_anchor = true;
+    c->has_ids = false;
+  }
+  return LS_OK;
+}
+
+// build row_ptr from out/in counts; returns total entries (host sync)
+static int build_rows(ls_ctx* c, int64_t* total) {
+  const int N = c->N;
+  launch_degree(c->stream, N, c->out_cnt, c->in_cnt, c->deg);
+  LS_CK(cudaMemsetAsync(c->deg + N, 0, sizeof(int32_t), c->stream));
+  size_t bytes = c->cub_bytes;
+  LS_CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->deg, c->row_ptr, N + 1, c->stream));
+  int32_t tot = 0;
+  LS_CK(cudaMemcpyAsync(&tot, c->row_ptr + N, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaStreamSynchronize(c->stream));
+  *total = tot;
+  return LS_OK;
+}
+
+int ls_chromaticity(const float* image_hwc, int H, int W, double* out, void* stream) {
+  LS_ARG(image_hwc && out && H >= 1 && W >= 1, "bad arguments");
+  // planar image copy is not needed: write it into the second half of a scratch-free path
+  launch_image((cudaStream_t)stream, image_hwc, H * W, nullptr, out);
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_edge_from_chroma(const double* chroma, int H, int W, float* edge, void* stream) {
+  LS_ARG(chroma && edge && H >= 1 && W >= 1, "bad arguments");
+  launch_edge((cudaStream_t)stream, chroma, H, W, edge);
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_sample_consistency(ls_ctx* c, const double* chroma, const double* prev_chroma, uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi,
+                          uint64_t inc_lo, int64_t* n_pairs_out) {
+  LS_ARG(c && (chroma || c->has_image), "ls_set_image first");
+  LS_CK(cudaSetDevice(c->dev));
+  const int N = c->N;
+  const double* cur = chroma ? chroma : c->chroma;
+  SampleParams P;
+  std::memset(&P, 0, sizeof(P));
+  P.st_hi = st_hi;
+  P.st_lo = st_lo;
+  P.inc_hi = inc_hi;
+  P.inc_lo = inc_lo;
+  P.has_prev = prev_chroma ? 1 : 0;
+  for (;;) {
+    LS_CK(cudaMemsetAsync(c->out_cnt, 0, sizeof(int32_t) * (N + 1), c->stream));
+    LS_CK(cudaMemsetAsync(c->in_cnt, 0, sizeof(int32_t) * (N + 1), c->stream));
+    LS_CK(cudaMemsetAsync(c->zero_flag, 0xff, sizeof(unsigned long long), c->stream));
+    launch_sample(c->stream, P, cur, prev_chroma, c->H, c->W, c->codes, c->out_cnt, c->in_cnt,
+                  c->zero_flag);
+    LS_CK(cudaGetLastError());
+    unsigned long long z = 0;
+    LS_CK(cudaMemcpyAsync(&z, c->zero_flag, sizeof(z), cudaMemcpyDeviceToHost, c->stream));
+    LS_CK(cudaStreamSynchronize(c->stream));
+    if (z == ~0ULL) break;
+    // a Lemire rejection (u32 == 0, p = 2^-32 per draw) shifts the stream
+    LS_ARG(P.nz < 8, "too many PCG64 rejections in one frame");
+    int at = P.nz;
+    while (at > 0 && (unsigned long long)P.z[at - 1] > z) {
+      P.z[at] = P.z[at - 1];
+      --at;
+    }
+    P.z[at] = (long long)z;
+    ++P.nz;
+  }
+  int64_t total = 0;
+  int rc = build_rows(c, &total);
+  if (rc != LS_OK) return rc;
+  LS_CK(cudaMemsetAsync(c->fill, 0, sizeof(int32_t) * N, c->stream));
+  launch_fill_from_samples(c->stream, c->codes, c->H, c->W, c->row_ptr, c->fill, c->ent, c->key);
+  launch_sort_rows(c->stream, N, c->row_ptr, c->ent, c->key, nullptr);
+  // pair offsets (src-major, slot order) for ls_get_pairs and the pair count
+  size_t bytes = c->cub_bytes;
+  LS_CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->out_cnt, c->pair_off, N + 1, c->stream));
+  int32_t np = 0;
+  LS_CK(cudaMemcpyAsync(&np, c->pair_off + N, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaStreamSynchronize(c->stream));
+  LS_CK(cudaGetLastError());
+  c->n_pairs = np;
+  c->n_temporal = P.has_prev ? (int)(np - (total - np)) : 0;   // out entries minus spatial incoming ones
+  c->has_ent_w = false;
+  c->has_pairs = true;
+  c->pairs_from_sampler = true;
+  if (n_pairs_out) *n_pairs_out = np;
+  return LS_OK;
+}
+
+int ls_get_pairs(ls_ctx* c, int64_t* src, int64_t* dst, uint8_t* temporal) {
+  LS_ARG(c && c->has_pairs && c->pairs_from_sampler, "no sampled pairs");
+  launch_pairs_from_samples(c->stream, c->codes, c->H, c->W, c->pair_off, src, dst, temporal);
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_set_pairs(ls_ctx* c, int64_t n, const int64_t* src, const int64_t* dst, const uint8_t* temporal,
+                 const double* weight) {
+  LS_ARG(c && n >= 0, "bad arguments");
+  LS_ARG(n == 0 || (src && dst && temporal), "null pair arrays");
+  LS_CK(cudaSetDevice(c->dev));
+  const int N = c->N;
+  LS_CK(cudaMemsetAsync(c->out_cnt, 0, sizeof(int32_t) * (N + 1), c->stream));
+  LS_CK(cudaMemsetAsync(c->in_cnt, 0, sizeof(int32_t) * (N + 1), c->stream));
+  LS_CK(cudaMemsetAsync(c->small_i, 0, sizeof(int) * 8, c->stream));
+  launch_pairs_count(c->stream, n, src, dst, temporal, c->H, c->W, c->out_cnt, c->in_cnt, c->small_i);
+  int bad = 0;
+  LS_CK(cudaMemcpyAsync(&bad, c->small_i, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaStreamSynchronize(c->stream));
+  LS_ARG(!bad, "consistency partners must be valid pixels within the 15x15 window");
+  int64_t total = 0;
+  int rc = build_rows(c, &total);
+  if (rc != LS_OK) return rc;
+  if (total + 16 > c->ent_cap) {   // only hand-made pair lists can outgrow 8N
+    cudaFree(c->ent);
+    cudaFree(c->ent_w);
+    cudaFree(c->key);
+    c->ent = nullptr; c->ent_w = nullptr; c->key = nullptr;
+    c->ent_cap = total + 16;
+    LS_CK(cudaMalloc((void**)&c->ent, sizeof(uint16_t) * c->ent_cap));
+    LS_CK(cudaMalloc((void**)&c->ent_w, sizeof(float) * c->ent_cap));
+    LS_CK(cudaMalloc((void**)&c->key, sizeof(uint32_t) * c->ent_cap));
+  }
+  LS_CK(cudaMemsetAsync(c->fill, 0, sizeof(int32_t) * N, c->stream));
+  launch_fill_from_pairs(c->stream, n, src, dst, temporal, weight, c->W, c->row_ptr, c->fill, c->ent, c->key,
+                         weight ? c->ent_w : nullptr);
+  launch_sort_rows(c->stream, N, c->row_ptr, c->ent, c->key, weight ? c->ent_w : nullptr);
+  LS_CK(cudaGetLastError());
+  c->n_pairs = n;
+  c->n_temporal = (int)(n - (total - n));
+  c->has_ent_w = weight != nullptr;
+  c->has_pairs = true;
+  c->pairs_from_sampler = false;
+  return LS_OK;
+}
+
+int ls_segment(ls_ctx* c, const double* colors, int32_t* ids_out) {
+  LS_ARG(c && c->has_image && colors && ids_out, "bad arguments");
+  LS_ARG(c->K >= 1, "segment needs K >= 1");
+  const int N = c->N, K = c->K;
+  double pc[2 * LS_MAX_K];
+  for (int k = 0; k < K; ++k) {   // chroma_of_color (imaging.py:174-180)
+    const double s = (colors[3 * k] + colors[3 * k + 1]) + colors[3 * k + 2];
+    pc[2 * k] = s > 1e-12 ? colors[3 * k] / s : 1.0 / 3.0;
+    pc[2 * k + 1] = s > 1e-12 ? colors[3 * k + 1] / s : 1.0 / 3.0;
+  }
+  LS_CK(cudaMemcpyAsync(c->pal_chroma, pc, sizeof(double) * 2 * K, cudaMemcpyHostToDevice, c->stream));
+  launch_set_i32(c->stream, c->small_i + 2, 1, N);
+  launch_segment_raw(c->stream, c->img, c->chroma, N, K, c->pal_chroma, c->seg_raw, c->seg_key, c->small_i + 2);
+  size_t bytes = c->cub_bytes;
+  LS_CK(cub::DeviceScan::InclusiveScan(c->cub_tmp, bytes, c->seg_key, c->seg_last, MaxOp(), N, c->stream));
+  launch_segment_final(c->stream, N, c->seg_raw, c->seg_last, c->small_i + 2, ids_out);
+  LS_CK(cudaGetLastError());
+  // pageable source: wait before the host array goes out of scope
+  LS_CK(cudaStreamSynchronize(c->stream));
+  return LS_OK;
+}
+
+int ls_initialize(ls_ctx* c, const double* colors, const int32_t* ids, float* X) {
+  LS_ARG(c && c->has_image && colors && ids && X, "bad arguments");
+  LS_CK(cudaMemcpyAsync(c->colors_dev, colors, sizeof(double) * 3 * c->K, cudaMemcpyHostToDevice, c->stream));
+  launch_initialize(c->stream, c->img, ids, c->N, c->NT, c->colors_dev, X);
+  LS_CK(cudaGetLastError());
+  LS_CK(cudaStreamSynchronize(c->stream));
+  return LS_OK;
+}
+
+static Launch L_energy(ls_ctx* c) { return Launch{c->grid_energy, c->ntiles, c->stream}; }
+static Launch L_apply(ls_ctx* c) { return Launch{c->grid_apply, c->ntiles, c->stream}; }
+static Launch L_update(ls_ctx* c) { return Launch{c->grid_update, 0, c->stream}; }
+
+int ls_energy_terms(ls_ctx* c, const double* colors, const float* X, const float* Y, double* terms) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  LS_ARG(colors || c->K == 0, "null palette");
+  LS_ARG(X && Y && terms, "bad arguments");
+  LS_CK(cudaSetDevice(c->dev));
+  const Coef<double> cd = make_coef<double>(c->w, colors, c->K);
+  launch_energy_ext(L_energy(c), frame_of(c), cd, X, Y, c->part, c->tickets + 0, c->sc);
+  LS_CK(cudaGetLastError());
+  LS_CK(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaStreamSynchronize(c->stream));
+  for (int j = 0; j < kTerms; ++j) terms[j] = c->sc_host->terms1[j];
+  return LS_OK;
+}
+
+int ls_grad_diag(ls_ctx* c, const double* colors, const float* X, float* b, float* diag) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  LS_ARG(X && b && diag, "bad arguments");
+  LS_CK(cudaSetDevice(c->dev));
+  const Coef<double> cd = make_coef<double>(c->w, colors, c->K);
+  launch_energy(0, L_energy(c), frame_of(c), cd, X, nullptr, 0.f, nullptr, nullptr, nullptr, nullptr, b, diag,
+                c->part, c->tickets + 0, c->sc);
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_apply_normal(ls_ctx* c, const double* colors, const float* X, const float* p, float* Ap) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  LS_ARG(X && p && Ap, "bad arguments");
+  LS_CK(cudaSetDevice(c->dev));
+  const Coef<float> cf = make_coef<float>(c->w, colors, c->K);
+  launch_apply(L_apply(c), frame_of(c), cf, X, p, Ap, c->part, c->tickets + 1, nullptr, 0);
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+// fused energy/gradient + PCG loop; x receives the step
+static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, float* x) {
+  const Frame f = frame_of(c);
+  const Coef<double> cd = make_coef<double>(c->w, colors, c->K);
+  const Coef<float> cf = make_coef<float>(c->w, colors, c->K);
+  launch_energy(0, L_energy(c), f, cd, X, nullptr, 0.f, nullptr, c->r, c->d, c->u, nullptr, nullptr, c->part,
+                c->tickets + 0, c->sc);
+  const int64_t M = (int64_t)c->U * c->N;
+  for (int it = 0; it < iters; ++it) {
+    launch_apply(L_apply(c), f, cf, X, c->u, c->wv, c->part, c->tickets + 1, c->sc, it);
+    launch_update(L_update(c), M, x, c->r, c->p, c->s, c->wv, c->d, c->u, c->part, c->tickets + 2, c->sc, it);
+  }
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_pcg(ls_ctx* c, const double* colors, const float* X, int iterations, float* x, double* info) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  LS_ARG(X && x && info && iterations >= 0, "bad arguments");
+  LS_CK(cudaSetDevice(c->dev));
+  LS_CK(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)c->U * c->N, c->stream));
+  rc = run_pcg(c, colors, X, iterations, x);
+  if (rc) return rc;
+  LS_CK(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaStreamSynchronize(c->stream));
+  info[0] = c->sc_host->iterations;
+  info[1] = std::sqrt(c->sc_host->bnorm2);
+  info[2] = std::sqrt(c->sc_host->rnorm2);
+  return LS_OK;
+}
+
+static double sum_terms(const double* t) {
+  double s = 0.0;   // Python sum() order over the blocks (solver.py:139-140)
+  for (int j = 0; j < kTerms; ++j) s += t[j];
+  return s;
+}
+
+int ls_gn_step(ls_ctx* c, const double* colors, const float* X, float* X_out, ls_gn_record* rec) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  LS_ARG(X && X_out && rec && X != X_out, "bad arguments");
+  LS_CK(cudaSetDevice(c->dev));
+  std::memset(rec, 0, sizeof(*rec));
+  rc = run_pcg(c, colors, X, c->cfg.pcg_iterations, c->x);
+  if (rc) return rc;
+  const Frame f = frame_of(c);
+  const Coef<double> cd = make_coef<double>(c->w, colors, c->K);
+  double alpha = 1.0;
+  double e0 = 0.0, e1 = 0.0;
+  bool accepted = false;
+  for (int h = 0; h <= c->cfg.max_halvings; ++h) {
+    launch_energy(1, L_energy(c), f, cd, X, c->x, (float)alpha, X_out, nullptr, nullptr, nullptr, nullptr,
+                  nullptr, c->part, c->tickets + 0, c->sc);
+    LS_CK(cudaGetLastError());
+    LS_CK(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
+    LS_CK(cudaStreamSynchronize(c->stream));
+    const Scalars& s = *c->sc_host;
+    if (h == 0) {
+      std::memcpy(rec->terms_before, s.terms0, sizeof(rec->terms_before));
+      e0 = sum_terms(s.terms0);
+      rec->energy_before = e0;
+      rec->pcg_iterations = s.iterations;
+      rec->initial_residual = std::sqrt(s.bnorm2);
+      rec->final_residual = std::sqrt(s.rnorm2);
+      if (!std::isfinite(e0)) {
+        std::memcpy(rec->terms, s.terms0, sizeof(rec->terms));
+        g_err = "non-finite residuals in sparse phase";
+        return LS_ERR_NONFINITE;
+      }
+    }
+    e1 = sum_terms(s.terms1);
+    if (std::isfinite(e1) && e1 <= e0) {
+      accepted = true;
+      std::memcpy(rec->terms, s.terms1, sizeof(rec->terms));
+      break;
+    }
+    alpha *= 0.5;
+  }
+  rec->accepted = accepted ? 1 : 0;
+  rec->alpha = accepted ? alpha : 0.0;
+  rec->energy_after = accepted ? e1 : e0;
+  if (!accepted) std::memcpy(rec->terms, rec->terms_before, sizeof(rec->terms));
+  return LS_OK;
+}
+
+static int dense_system(ls_ctx* c, const double* colors, const float* X, int use_ids) {
+  LS_CK(cudaMemcpyAsync(c->colors_dev, colors, sizeof(double) * 3 * c->K, cudaMemcpyHostToDevice, c->stream));
+  launch_dense_accum(c->stream, c->grid_dense, frame_of(c), c->colors_dev, c->K, X, use_ids, c->part,
+                     c->tickets + 3, c->dense_sums);
+  launch_dense_assemble_solve(c->stream, c->dense_sums, c->K, c->colors_dev, use_ids, c->w.lambda_data,
+                              c->w.lambda_clustering, c->w.lambda_ir, c->w.lambda_cr, c->w.chroma_reg,
+                              c->cfg.svd_truncation, c->dense_A, c->dense_rhs, c->dense_x);
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_dense_normal(ls_ctx* c, const double* colors, const float* X, int use_ids, double* A, double* rhs) {
+  LS_ARG(c && c->has_image && colors && X && A && rhs, "bad arguments");
+  LS_ARG(c->K >= 1, "dense system needs K >= 1");
+  LS_ARG(!use_ids || c->has_ids, "no cluster ids set");
+  LS_CK(cudaSetDevice(c->dev));
+  int rc = dense_system(c, colors, X, use_ids);
+  if (rc) return rc;
+  const int n = 3 * c->K;
+  LS_CK(cudaMemcpyAsync(c->host_buf, c->dense_A, sizeof(double) * n * n, cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaMemcpyAsync(c->host_buf + n * n, c->dense_rhs, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaStreamSynchronize(c->stream));
+  std::memcpy(A, c->host_buf, sizeof(double) * n * n);
+  std::memcpy(rhs, c->host_buf + n * n, sizeof(double) * n);
+  return LS_OK;
+}
+
+int ls_svd_solve(ls_ctx* c, int n, const double* A, const double* rhs, double trunc, double* x) {
+  LS_ARG(c && A && rhs && x && n >= 1 && n <= 3 * LS_MAX_K, "bad arguments");
+  LS_CK(cudaSetDevice(c->dev));
+  std::memcpy(c->host_buf, A, sizeof(double) * n * n);
+  std::memcpy(c->host_buf + n * n, rhs, sizeof(double) * n);
+  LS_CK(cudaMemcpyAsync(c->dense_A, c->host_buf, sizeof(double) * n * n, cudaMemcpyHostToDevice, c->stream));
+  LS_CK(cudaMemcpyAsync(c->dense_rhs, c->host_buf + n * n, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  launch_svd_solve(c->stream, n, c->dense_A, c->dense_rhs, trunc, c->dense_x);
+  LS_CK(cudaGetLastError());
+  LS_CK(cudaMemcpyAsync(c->host_buf, c->dense_x, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaStreamSynchronize(c->stream));
+  std::memcpy(x, c->host_buf, sizeof(double) * n);
+  return LS_OK;
+}
+
+int ls_dense_step(ls_ctx* c, double* colors, const float* X, double* applied, ls_dense_record* rec) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  LS_ARG(colors && X && applied && rec, "bad arguments");
+  LS_ARG(c->K >= 1, "dense step needs K >= 1");
+  LS_CK(cudaSetDevice(c->dev));
+  std::memset(rec, 0, sizeof(*rec));
+  const int K = c->K, n = 3 * K;
+  rc = dense_system(c, colors, X, c->has_ids ? 1 : 0);
+  if (rc) return rc;
+  LS_CK(cudaMemcpyAsync(c->host_buf, c->dense_x, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaStreamSynchronize(c->stream));
+  std::vector<double> db(c->host_buf, c->host_buf + n);
+  for (int i = 0; i < n; ++i) applied[i] = 0.0;
+  bool any = false;
+  double big = 0.0;
+  for (double v : db) {
+    any = any || v != 0.0;
+    big = std::max(big, std::fabs(v));
+  }
+  if (!any) return LS_OK;   // solver.py:218-219: no record
+  rec->solved_nonzero = 1;
+  if (big > c->cfg.max_delta_b)
+    for (double& v : db) v = v * (c->cfg.max_delta_b / big);
+  const Frame f = frame_of(c);
+  auto energy_with = [&](const double* cols, double* out) -> int {
+    const Coef<double> cd = make_coef<double>(c->w, cols, K);
+    launch_energy_ext(L_energy(c), f, cd, X, X, c->part, c->tickets + 0, c->sc);
+    LS_CK(cudaGetLastError());
+    LS_CK(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
+    LS_CK(cudaStreamSynchronize(c->stream));
+    *out = sum_terms(c->sc_host->terms1);
+    return LS_OK;
+  };
+  double e0 = 0.0;
+  if ((rc = energy_with(colors, &e0))) return rc;
+  double alpha = 1.0, e1 = e0;
+  bool accepted = false;
+  std::vector<double> cand(n);
+  for (int h = 0; h <= c->cfg.max_halvings; ++h) {
+    for (int i = 0; i < n; ++i) cand[i] = std::min(1.0, std::max(0.0, colors[i] + alpha * db[i]));
+    double et = 0.0;
+    if ((rc = energy_with(cand.data(), &et))) return rc;
+    if (std::isfinite(et) && et <= e0) {
+      double nrm = 0.0;
+      for (int i = 0; i < n; ++i) {
+        applied[i] = cand[i] - colors[i];
+        nrm += applied[i] * applied[i];
+        colors[i] = cand[i];
+      }
+      rec->delta_b_norm = std::sqrt(nrm);
+      e1 = et;
+      accepted = true;
+      break;
+    }
+    alpha *= 0.5;
+  }
+  rec->energy_before = e0;
+  rec->energy_after = accepted ? e1 : e0;
+  rec->accepted = accepted ? 1 : 0;
+  rec->alpha = accepted ? alpha : 0.0;
+  return LS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,155 @@
+// Shared device-side definitions for the lumisplit B200 kernels.
+//
+// Data layout in HBM: every per-pixel field is a
+// set of planes of N = H*W float32 values, row-major.  The layer state X has
+// U = NT + 3 planes: r (3) then T_0..T_{NT-1} (NT = K+1).  PCG vectors use
+// the same plane order, i.e. the reference vector [r.ravel(), T.ravel()]
+// (solver.py:110-122) up to the (H,W,C) -> (C,H,W) permutation.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ls {
+
+constexpr int kMaxNT = 13;        // K <= 12
+constexpr int kTerms = 8;
+constexpr int kHalf = 7;          // CONSISTENCY_WINDOW // 2 (energy.py:23)
+constexpr int kWin = 15;
+constexpr int kTileW = 32;        // one warp per tile row
+constexpr int kTileH = 8;         // 8 warps per block
+constexpr int kThreads = kTileW * kTileH;
+constexpr int kHaloW = kTileW + 2 * kHalf;
+constexpr int kHaloH = kTileH + 2 * kHalf;
+constexpr int kMaxBlocks = 4096;  // partial-sum slots per reduction
+
+// adjacency entry: bits 0-7 offset code (dy+7)*15+(dx+7); bit 8 temporal;
+// bit 9 incoming (this pixel is the pair's dst).
+constexpr uint16_t kEntTemporal = 1u << 8;
+constexpr uint16_t kEntIncoming = 1u << 9;
+
+enum Term { T_DATA = 0, T_CLUSTER, T_RSPARSE, T_CONSIST, T_MONO, T_ISPARSE, T_SMOOTH, T_NONNEG };
+
+// Frozen coefficients of the energy (EnergyWeights + palette), both in fp32
+// (the PCG operator) and fp64 (energies, gradient, diagonal).
+template <typename R>
+struct Coef {
+  R B[kMaxNT][3];      // palette matrix, row 0 white (palette.py:64-66)
+  R G[kMaxNT][3];      // B - rowmean(B) (energy.py:396)
+  R anchor[kMaxNT][3]; // log(max(color[id-1], 1e-4)) indexed by id (energy.py:470-472)
+  R lam_d, lam_cl, lam_rs, p, lam_rc, lam_m, lam_is, lam_sm, lam_nn;
+  R eps_nn, eps_irls, inv_eps, floor_rs;
+};
+
+struct Frame {
+  int H, W, N, NT;
+  const float* img;       // 3 planes
+  const float* edge;      // N
+  const int32_t* ids;     // N or nullptr
+  const float* anchor;    // 3 planes or nullptr (fixed log anchor)
+  const float* prev_r;    // 3 planes or nullptr
+  const int32_t* row_ptr; // N + 1
+  const uint16_t* ent;    // adjacency entries
+  const float* ent_w;     // per-entry pair weight or nullptr (all 1)
+};
+
+// device-resident PCG / step scalars (Chronopoulos-Gear PCG)
+struct Scalars {
+  double gamma, gamma_prev, delta, alpha, alpha_prev, beta;
+  double bnorm2, rnorm2;
+  double terms0[kTerms];   // energies at the linearisation point
+  double terms1[kTerms];   // energies at the last trial point
+  int iterations;
+  int stop;
+  int pad[2];
+};
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+template <typename R>
+__device__ __forceinline__ R irls1(R mag, R eps, R inv_eps) {
+  // energy.py:102-112 with p = 1: 1/|m| above the floor eps, else 1/eps
+  mag = mag < R(0) ? -mag : mag;
+  return mag >= eps ? R(1) / mag : inv_eps;
+}
+
+template <typename R>
+__device__ __forceinline__ R irlsp(R mag, const Coef<R>& c) {
+  // general p (r-sparsity only): min(|m|^(p-2), 1/eps), floor eps^(1/(2-p))
+  if (c.p >= R(2)) return R(1);
+  mag = mag < R(0) ? -mag : mag;
+  if (!(mag >= c.floor_rs)) return c.inv_eps;
+  if (c.p == R(1)) return R(1) / mag;
+  return pow(mag, c.p - R(2));
+}
+
+template <typename R>
+__device__ __forceinline__ R nonneg_w(R t, R eps) {
+  // energy.py:115-118
+  return t > R(0) ? R(0) : R(1) / ((t < R(0) ? -t : t) + eps);
+}
+
+__device__ __forceinline__ void decode_offset(uint16_t e, int& dy, int& dx) {
+  int code = e & 0xff;
+  dy = code / kWin - kHalf;
+  dx = code % kWin - kHalf;
+}
+
+// ---- deterministic block reduction + last-block finalisation -------------
+// Each block reduces NV doubles (fixed shuffle tree), writes them to
+// part[blockIdx.x * NV + j]; the last block to arrive (ticket) sums the
+// partials over blocks in a fixed order and calls fin(j, total).
+template <int NV>
+__device__ __forceinline__ void block_reduce_store(double (&v)[NV], double* part) {
+  __shared__ double red[kThreads / 32][NV];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    double a = v[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    if (lane == 0) red[wid][j] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][threadIdx.x];
+    part[(size_t)blockIdx.x * NV + threadIdx.x] = s;
+  }
+}
+
+// returns true in the (whole) last block after all partials are visible
+__device__ __forceinline__ bool last_block(unsigned* ticket) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = atomicAdd(ticket, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
+// sum partial j over all blocks with a fixed assignment + fixed tree;
+// result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ double sum_partials(const double* part, int nblocks, int j) {
+  __shared__ double red2[kThreads / 32];
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) s += ((volatile const double*)part)[(size_t)b * NV + j];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  __syncthreads();
+  if (lane == 0) red2[wid] = s;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red2[w];
+  __syncthreads();
+  return t;
+}
+
+}  // namespace ls

@@ -1,0 +1,76 @@
+// Internal launcher declarations shared by the .cu translation units.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ls_common.cuh"
+
+namespace ls {
+
+struct Launch {
+  int grid;
+  int ntiles;
+  cudaStream_t stream;
+};
+
+// ls_solver.cu
+void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<double>& c, const float* X,
+                   const float* dx, float alpha, float* Xout, float* r_out, float* d_out, float* u_out,
+                   float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc);
+void launch_energy_ext(const Launch& L, const Frame& f, const Coef<double>& c, const float* X,
+                       const float* Y, double* part, unsigned* ticket, Scalars* sc);
+void launch_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* u,
+                  float* w, double* part, unsigned* ticket, Scalars* sc, int iter);
+void launch_update(const Launch& L, int64_t M, float* x, float* r, float* p, float* s, const float* w,
+                   const float* d, float* u, double* part, unsigned* ticket, Scalars* sc, int iter);
+int energy_grid_limit(int NT);
+int apply_grid_limit(int NT);
+int update_grid_limit();
+
+// ls_aux.cu
+struct SampleParams {
+  unsigned long long st_hi, st_lo, inc_hi, inc_lo;
+  int has_prev;
+  int nz;                       // known rejected stream positions
+  long long z[8];
+};
+void launch_pack_hwc(cudaStream_t s, const float* hwc, int C, int N, float* planes);
+void launch_unpack_hwc(cudaStream_t s, const float* planes, int C, int N, float* hwc);
+void launch_image(cudaStream_t s, const float* hwc, int N, float* img_planes, double* chroma);
+void launch_edge(cudaStream_t s, const double* chroma, int H, int W, float* edge);
+void launch_sample(cudaStream_t s, const SampleParams& P, const double* chroma, const double* prev_chroma,
+                   int H, int W, int16_t* codes, int32_t* out_cnt, int32_t* in_cnt,
+                   unsigned long long* new_zero);
+void launch_pairs_count(cudaStream_t s, int64_t n, const int64_t* src, const int64_t* dst,
+                        const uint8_t* temporal, int H, int W, int32_t* out_cnt, int32_t* in_cnt, int* bad);
+void launch_degree(cudaStream_t s, int N, const int32_t* out_cnt, const int32_t* in_cnt, int32_t* deg);
+void launch_fill_from_samples(cudaStream_t s, const int16_t* codes, int H, int W, const int32_t* row_ptr,
+                              int32_t* fill, uint16_t* ent, uint32_t* key);
+void launch_fill_from_pairs(cudaStream_t s, int64_t n, const int64_t* src, const int64_t* dst,
+                            const uint8_t* temporal, const double* weight, int W, const int32_t* row_ptr,
+                            int32_t* fill, uint16_t* ent, uint32_t* key, float* ent_w);
+void launch_sort_rows(cudaStream_t s, int N, const int32_t* row_ptr, uint16_t* ent, uint32_t* key,
+                      float* ent_w);
+void launch_pairs_from_samples(cudaStream_t s, const int16_t* codes, int H, int W, const int32_t* pair_off,
+                               int64_t* src, int64_t* dst, uint8_t* temporal);
+void launch_segment_raw(cudaStream_t s, const float* img, const double* chroma, int N, int K,
+                        const double* pal_chroma /*device K*2*/, int32_t* ids_raw, int32_t* key,
+                        int* first_valid);
+void launch_segment_final(cudaStream_t s, int N, const int32_t* ids_raw, const int32_t* last,
+                          const int* first_valid, int32_t* ids);
+void launch_initialize(cudaStream_t s, const float* img, const int32_t* ids, int N, int NT,
+                       const double* colors /*device K*3*/, float* X);
+void launch_set_i32(cudaStream_t s, int32_t* p, int n, int32_t v);
+
+// ls_dense.cu
+int dense_nsums(int K);
+void launch_dense_accum(cudaStream_t s, int grid, const Frame& f, const double* colors_dev, int K,
+                        const float* X, int use_ids, double* part, unsigned* ticket, double* sums);
+void launch_dense_assemble_solve(cudaStream_t s, const double* sums, int K, const double* colors_dev,
+                                 int use_ids, double lam_d, double lam_cl, double lam_ir, double lam_cr,
+                                 int chroma_identity, double trunc, double* A_out, double* rhs_out,
+                                 double* x_out);
+void launch_svd_solve(cudaStream_t s, int n, const double* A, const double* rhs, double trunc, double* x);
+
+}  // namespace ls

@@ -1,0 +1,115 @@
+"""Clip decomposition entry point (reference pipeline.py:87-167).
+
+`decompose_frames` keeps the reference signature and flow: frame 1 is
+clustered (or takes the palette / cluster map given), refined and solved;
+frames 2..N are re-segmented with the frozen palette and solved warm-started
+with temporal consistency pairs.  Interactive misclustering correction
+(`clicks`, correction.py) is outside this framework's scope (SURVEY.md
+section 2, row 7) and is rejected explicitly.
+"""
+
+from __future__ import annotations
+
+import logging
+import time
+from dataclasses import dataclass, field, replace
+
+import torch
+
+from .energy import EnergyWeights, LayerStack
+from .imaging import Frame, as_cuda, chromaticity
+from .palette import BaseColorPalette, ClusterMap, estimate_palette, segment
+from .refine import refine_palette
+from .solver import SolveConfig, SolverState, build_aux, flip_flop, initialize
+
+log = logging.getLogger(__name__)
+
+
+@dataclass
+class PipelineResult:
+    """pipeline.py:33-47."""
+
+    palette: BaseColorPalette
+    layer_stacks: list
+    cluster_maps: list
+    regions: list
+    records: list
+    statuses: list
+    frame_seconds: list = field(default_factory=list)
+
+    def reflectances(self) -> list:
+        return [torch.exp(ls.r) for ls in self.layer_stacks]
+
+    def illuminations(self) -> list:
+        return [ls.illumination(self.palette) for ls in self.layer_stacks]
+
+
+def _as_frame(f) -> Frame:
+    return f if isinstance(f, Frame) else Frame(as_cuda(f))
+
+
+def decompose_frames(frames: list, weights: EnergyWeights, config: SolveConfig, seed: int = 0,
+                     k_max: int = 10, clicks: list | None = None, streaming_outer: int = 2,
+                     palette: BaseColorPalette | None = None,
+                     cluster_map: ClusterMap | None = None,
+                     on_frame=None) -> PipelineResult:
+    """Decompose an in-memory frame sequence (pipeline.py:87-167).
+
+    Extra keyword arguments (not in the reference): `palette` /
+    `cluster_map` skip first-frame estimation (SURVEY.md section 8d uses the
+    generator palette); `on_frame(index, state)` is called after each frame
+    (streams results out without keeping them)."""
+    if not frames:
+        raise ValueError("no frames")
+    if clicks:
+        raise NotImplementedError("misclustering correction (clicks) is outside lumisplit_b200's scope")
+    f0 = _as_frame(frames[0])
+    if palette is None:
+        palette, cluster_map = estimate_palette(f0, k_max=k_max, seed=seed)
+    elif cluster_map is None:
+        cluster_map = segment(f0, palette)
+    result = PipelineResult(palette=palette, layer_stacks=[], cluster_maps=[], regions=[],
+                            records=[], statuses=[])
+    t0 = time.perf_counter()
+    aux = build_aux(f0, cluster_map, seed=seed)
+    layers = initialize(f0, cluster_map, palette)
+    state = SolverState(frame=f0, palette=palette, layers=layers, aux=aux, weights=weights,
+                        config=config)
+    if config.refine:
+        palette, _ = refine_palette(state)
+    else:
+        state.config = replace(state.config, refine=False)
+        flip_flop(state)
+        palette = state.palette
+    result.palette = palette
+    result.layer_stacks.append(state.layers)
+    result.cluster_maps.append(cluster_map)
+    result.records.append(state.records)
+    result.statuses.append(state.status)
+    result.frame_seconds.append(time.perf_counter() - t0)
+    if on_frame is not None:
+        on_frame(0, state)
+
+    stream_cfg = replace(config, refine=False, outer_iterations=streaming_outer)
+    prev_layers = state.layers
+    prev_chroma = chromaticity(f0)
+    for idx in range(1, len(frames)):
+        t0 = time.perf_counter()
+        frame = _as_frame(frames[idx])
+        cmap = segment(frame, palette)
+        aux = build_aux(frame, cmap, seed=seed + idx, prev_chroma=prev_chroma,
+                        prev_r=prev_layers.r)
+        layers = initialize(frame, cmap, palette, previous=prev_layers)
+        state = SolverState(frame=frame, palette=palette, layers=layers, aux=aux,
+                            weights=weights, config=stream_cfg)
+        flip_flop(state)
+        result.layer_stacks.append(state.layers)
+        result.cluster_maps.append(cmap)
+        result.records.append(state.records)
+        result.statuses.append(state.status)
+        result.frame_seconds.append(time.perf_counter() - t0)
+        if on_frame is not None:
+            on_frame(idx, state)
+        prev_layers = state.layers
+        prev_chroma = chromaticity(frame)
+    return result
