@@ -91,6 +91,13 @@ LS_API int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w,
 LS_API int ls_ctx_destroy(ls_ctx* ctx);
 LS_API int ls_set_weights(ls_ctx* ctx, const ls_weights* w, const ls_solve_cfg* cfg);
 LS_API int ls_set_stream(ls_ctx* ctx, void* cuda_stream);
+/* Instrumentation: enable=1 starts CUDA-event timing of the solver kernels
+ * (resets counters); ls_profile_read fills 11 doubles: (count, total ms) for
+ * {energy+gradient, J^T J apply, PCG update, line-search trial, dense
+ * reduction}, then the number of kernels this context launched, the number
+ * of adjacency entries and of partner pairs of the installed frame (13). */
+LS_API int ls_profile(ls_ctx* ctx, int enable);
+LS_API int ls_profile_read(ls_ctx* ctx, double* out13);
 
 /* ---- layout helpers ---------------------------------------------------- */
 /* (H, W, C) interleaved <-> C planes of H*W. */

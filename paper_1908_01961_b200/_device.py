@@ -93,6 +93,21 @@ class DeviceSolver:
         self._chk(self.lib.ls_set_weights(self.ctx, C.byref(weights_struct(weights)),
                                           C.byref(config_struct(config))))
 
+    def profile(self, enable: bool):
+        self._enter()
+        self._chk(self.lib.ls_profile(self.ctx, int(bool(enable))))
+
+    def profile_read(self) -> dict:
+        out = np.zeros(13)
+        self._enter()
+        self._chk(self.lib.ls_profile_read(self.ctx, out.ctypes.data_as(L.DBL_P)))
+        names = ("energy_grad", "apply", "update", "trial", "dense")
+        d = {n: {"count": int(out[2 * i]), "ms": float(out[2 * i + 1])} for i, n in enumerate(names)}
+        d["launches"] = int(out[10])
+        d["adjacency_entries"] = int(out[11])
+        d["pairs"] = int(out[12])
+        return d
+
     # -- per-frame context --------------------------------------------------------
     def set_image(self, image_hwc: torch.Tensor):
         self._enter()

@@ -59,6 +59,8 @@ SIGNATURES = {
     "ls_ctx_destroy": [P],
     "ls_set_weights": [P, C.POINTER(Weights), C.POINTER(SolveCfg)],
     "ls_set_stream": [P, P],
+    "ls_profile": [P, C.c_int],
+    "ls_profile_read": [P, DBL_P],
     "ls_pack_hwc": [P, P, C.c_int, P],
     "ls_unpack_hwc": [P, P, C.c_int, P],
     "ls_set_image": [P, P],

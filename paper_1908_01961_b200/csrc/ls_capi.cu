@@ -44,7 +44,20 @@ struct MaxOp {
   __host__ __device__ int operator()(int a, int b) const { return a > b ? a : b; }
 };
 
+// CUDA-event timing of the solver kernels by class (bench.py roofline)
+enum { PC_EG = 0, PC_APPLY, PC_UPDATE, PC_TRIAL, PC_DENSE, PC_N };
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  std::vector<std::pair<int, size_t>> pend;   // (class, index of start event)
+  double ms[PC_N] = {0};
+  long long cnt[PC_N] = {0};
+};
+
 struct ls_ctx {
+  long long launches = 0;                      // every kernel this context launched
+  Prof prof;
   int dev = 0, H = 0, W = 0, N = 0, K = 0, NT = 0, U = 0;
   ls_weights w{};
   ls_solve_cfg cfg{};
@@ -68,6 +81,7 @@ struct ls_ctx {
   int64_t ent_cap = 0;
   bool has_ent_w = false, has_pairs = false, pairs_from_sampler = false;
   int64_t n_pairs = 0;
+  int64_t n_entries = 0;
   int n_temporal = 0;
   int16_t* codes = nullptr;
   int32_t *out_cnt = nullptr, *in_cnt = nullptr, *deg = nullptr, *fill = nullptr, *pair_off = nullptr;
@@ -90,6 +104,10 @@ struct ls_ctx {
   double* host_buf = nullptr;   // pinned, 2 * 36 * 36 + 64 doubles
   std::vector<void*> allocs;
 };
+
+extern "C" {
+static void prof_harvest(ls_ctx* c);
+}
 
 template <typename T>
 static cudaError_t dalloc(ls_ctx* c, T** p, size_t n) {
@@ -258,11 +276,40 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   return LS_OK;
 }
 
+int ls_profile(ls_ctx* c, int enable) {
+  LS_ARG(c, "null context");
+  if (enable && c->prof.pool.empty()) {
+    c->prof.pool.resize(4096);
+    for (auto& e : c->prof.pool) LS_CK(cudaEventCreate(&e));
+  }
+  LS_CK(cudaStreamSynchronize(c->stream));
+  prof_harvest(c);
+  for (int i = 0; i < PC_N; ++i) { c->prof.ms[i] = 0.0; c->prof.cnt[i] = 0; }
+  c->prof.on = enable != 0;
+  c->launches = 0;
+  return LS_OK;
+}
+
+int ls_profile_read(ls_ctx* c, double* out) {
+  LS_ARG(c && out, "bad arguments");
+  LS_CK(cudaStreamSynchronize(c->stream));
+  prof_harvest(c);
+  for (int i = 0; i < PC_N; ++i) {
+    out[2 * i] = (double)c->prof.cnt[i];
+    out[2 * i + 1] = c->prof.ms[i];
+  }
+  out[2 * PC_N] = (double)c->launches;
+  out[2 * PC_N + 1] = (double)c->n_entries;
+  out[2 * PC_N + 2] = (double)c->n_pairs;
+  return LS_OK;
+}
+
 int ls_ctx_destroy(ls_ctx* c) {
   if (!c) return LS_OK;
   cudaSetDevice(c->dev);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : c->allocs) cudaFree(p);
+  for (auto& e : c->prof.pool) cudaEventDestroy(e);
   cudaFree(c->ent);
   cudaFree(c->ent_w);
   cudaFree(c->key);
@@ -291,6 +338,7 @@ int ls_set_image(ls_ctx* c, const float* image_hwc) {
   LS_CK(cudaSetDevice(c->dev));
   launch_image(c->stream, image_hwc, c->N, c->img, c->chroma);
   launch_edge(c->stream, c->chroma, c->H, c->W, c->edge);
+  c->launches += 2;
   LS_CK(cudaGetLastError());
   c->has_image = true;
   return LS_OK;
@@ -388,6 +436,7 @@ int ls_sample_consistency(ls_ctx* c, const double* chroma, const double* prev_ch
     LS_CK(cudaMemsetAsync(c->zero_flag, 0xff, sizeof(unsigned long long), c->stream));
     launch_sample(c->stream, P, cur, prev_chroma, c->H, c->W, c->codes, c->out_cnt, c->in_cnt,
                   c->zero_flag);
+    c->launches += 1;
     LS_CK(cudaGetLastError());
     unsigned long long z = 0;
     LS_CK(cudaMemcpyAsync(&z, c->zero_flag, sizeof(z), cudaMemcpyDeviceToHost, c->stream));
@@ -409,6 +458,7 @@ int ls_sample_consistency(ls_ctx* c, const double* chroma, const double* prev_ch
   LS_CK(cudaMemsetAsync(c->fill, 0, sizeof(int32_t) * N, c->stream));
   launch_fill_from_samples(c->stream, c->codes, c->H, c->W, c->row_ptr, c->fill, c->ent, c->key);
   launch_sort_rows(c->stream, N, c->row_ptr, c->ent, c->key, nullptr);
+  c->launches += 6;   // degree, 2 scans, fill, sort (+ scan kernels counted as 1 each)
   // pair offsets (src-major, slot order) for ls_get_pairs and the pair count
   size_t bytes = c->cub_bytes;
   LS_CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->out_cnt, c->pair_off, N + 1, c->stream));
@@ -417,6 +467,7 @@ int ls_sample_consistency(ls_ctx* c, const double* chroma, const double* prev_ch
   LS_CK(cudaStreamSynchronize(c->stream));
   LS_CK(cudaGetLastError());
   c->n_pairs = np;
+  c->n_entries = total;
   c->n_temporal = P.has_prev ? (int)(np - (total - np)) : 0;   // out entries minus spatial incoming ones
   c->has_ent_w = false;
   c->has_pairs = true;
@@ -465,6 +516,7 @@ int ls_set_pairs(ls_ctx* c, int64_t n, const int64_t* src, const int64_t* dst, c
   launch_sort_rows(c->stream, N, c->row_ptr, c->ent, c->key, weight ? c->ent_w : nullptr);
   LS_CK(cudaGetLastError());
   c->n_pairs = n;
+  c->n_entries = total;
   c->n_temporal = (int)(n - (total - n));
   c->has_ent_w = weight != nullptr;
   c->has_pairs = true;
@@ -488,6 +540,7 @@ int ls_segment(ls_ctx* c, const double* colors, int32_t* ids_out) {
   size_t bytes = c->cub_bytes;
   LS_CK(cub::DeviceScan::InclusiveScan(c->cub_tmp, bytes, c->seg_key, c->seg_last, MaxOp(), N, c->stream));
   launch_segment_final(c->stream, N, c->seg_raw, c->seg_last, c->small_i + 2, ids_out);
+  c->launches += 4;
   LS_CK(cudaGetLastError());
   // pageable source: wait before the host array goes out of scope
   LS_CK(cudaStreamSynchronize(c->stream));
@@ -501,6 +554,32 @@ int ls_initialize(ls_ctx* c, const double* colors, const int32_t* ids, float* X)
   LS_CK(cudaGetLastError());
   LS_CK(cudaStreamSynchronize(c->stream));
   return LS_OK;
+}
+
+static size_t prof_begin(ls_ctx* c) {
+  if (!c->prof.on) return 0;
+  if (c->prof.next + 2 > c->prof.pool.size()) return (size_t)-1;   // pool full: skip sample
+  const size_t i = c->prof.next;
+  c->prof.next += 2;
+  cudaEventRecord(c->prof.pool[i], c->stream);
+  return i;
+}
+static void prof_end(ls_ctx* c, int cls, size_t i) {
+  if (!c->prof.on || i == (size_t)-1) return;
+  cudaEventRecord(c->prof.pool[i + 1], c->stream);
+  c->prof.pend.emplace_back(cls, i);
+}
+// call only after a stream synchronisation
+static void prof_harvest(ls_ctx* c) {
+  for (auto& pe : c->prof.pend) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, c->prof.pool[pe.second], c->prof.pool[pe.second + 1]) == cudaSuccess) {
+      c->prof.ms[pe.first] += t;
+      c->prof.cnt[pe.first] += 1;
+    }
+  }
+  c->prof.pend.clear();
+  c->prof.next = 0;
 }
 
 static Launch L_energy(ls_ctx* c) { return Launch{c->grid_energy, c->ntiles, c->stream}; }
@@ -550,13 +629,20 @@ static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, f
   const Frame f = frame_of(c);
   const Coef<double> cd = make_coef<double>(c->w, colors, c->K);
   const Coef<float> cf = make_coef<float>(c->w, colors, c->K);
+  size_t pi = prof_begin(c);
   launch_energy(0, L_energy(c), f, cd, X, nullptr, 0.f, nullptr, c->r, c->d, c->u, nullptr, nullptr, c->part,
                 c->tickets + 0, c->sc);
+  prof_end(c, PC_EG, pi);
   const int64_t M = (int64_t)c->U * c->N;
   for (int it = 0; it < iters; ++it) {
+    pi = prof_begin(c);
     launch_apply(L_apply(c), f, cf, X, c->u, c->wv, c->part, c->tickets + 1, c->sc, it);
+    prof_end(c, PC_APPLY, pi);
+    pi = prof_begin(c);
     launch_update(L_update(c), M, x, c->r, c->p, c->s, c->wv, c->d, c->u, c->part, c->tickets + 2, c->sc, it);
+    prof_end(c, PC_UPDATE, pi);
   }
+  c->launches += 1 + 2LL * iters;
   LS_CK(cudaGetLastError());
   return LS_OK;
 }
@@ -597,11 +683,15 @@ int ls_gn_step(ls_ctx* c, const double* colors, const float* X, float* X_out, ls
   double e0 = 0.0, e1 = 0.0;
   bool accepted = false;
   for (int h = 0; h <= c->cfg.max_halvings; ++h) {
+    const size_t pi = prof_begin(c);
     launch_energy(1, L_energy(c), f, cd, X, c->x, (float)alpha, X_out, nullptr, nullptr, nullptr, nullptr,
                   nullptr, c->part, c->tickets + 0, c->sc);
+    prof_end(c, PC_TRIAL, pi);
+    c->launches += 1;
     LS_CK(cudaGetLastError());
     LS_CK(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
     LS_CK(cudaStreamSynchronize(c->stream));
+    prof_harvest(c);
     const Scalars& s = *c->sc_host;
     if (h == 0) {
       std::memcpy(rec->terms_before, s.terms0, sizeof(rec->terms_before));
@@ -633,8 +723,11 @@ int ls_gn_step(ls_ctx* c, const double* colors, const float* X, float* X_out, ls
 
 static int dense_system(ls_ctx* c, const double* colors, const float* X, int use_ids) {
   LS_CK(cudaMemcpyAsync(c->colors_dev, colors, sizeof(double) * 3 * c->K, cudaMemcpyHostToDevice, c->stream));
+  const size_t pi = prof_begin(c);
   launch_dense_accum(c->stream, c->grid_dense, frame_of(c), c->colors_dev, c->K, X, use_ids, c->part,
                      c->tickets + 3, c->dense_sums);
+  prof_end(c, PC_DENSE, pi);
+  c->launches += 2;
   launch_dense_assemble_solve(c->stream, c->dense_sums, c->K, c->colors_dev, use_ids, c->w.lambda_data,
                               c->w.lambda_clustering, c->w.lambda_ir, c->w.lambda_cr, c->w.chroma_reg,
                               c->cfg.svd_truncation, c->dense_A, c->dense_rhs, c->dense_x);
@@ -701,9 +794,11 @@ int ls_dense_step(ls_ctx* c, double* colors, const float* X, double* applied, ls
   auto energy_with = [&](const double* cols, double* out) -> int {
     const Coef<double> cd = make_coef<double>(c->w, cols, K);
     launch_energy_ext(L_energy(c), f, cd, X, X, c->part, c->tickets + 0, c->sc);
+    c->launches += 1;
     LS_CK(cudaGetLastError());
     LS_CK(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
     LS_CK(cudaStreamSynchronize(c->stream));
+    prof_harvest(c);
     *out = sum_terms(c->sc_host->terms1);
     return LS_OK;
   };

@@ -48,6 +48,59 @@ def _as_frame(f) -> Frame:
     return f if isinstance(f, Frame) else Frame(as_cuda(f))
 
 
+class StreamingDecomposer:
+    """The per-frame loop of decompose_frames (pipeline.py:113-166) as an
+    object: `first(frame)` solves frame 1 (refinement when enabled), each
+    `step(frame)` re-segments with the frozen palette and solves the frame
+    warm-started from the previous one."""
+
+    def __init__(self, palette: BaseColorPalette, weights: EnergyWeights, config: SolveConfig,
+                 seed: int = 0, streaming_outer: int = 2):
+        self.palette = palette
+        self.weights = weights
+        self.config = config
+        self.seed = seed
+        self.stream_cfg = replace(config, refine=False, outer_iterations=streaming_outer)
+        self.index = 0
+        self.prev_layers = None
+        self.prev_chroma = None
+
+    def first(self, frame, cluster_map: ClusterMap | None = None) -> SolverState:
+        frame = _as_frame(frame)
+        if cluster_map is None:
+            cluster_map = segment(frame, self.palette)
+        aux = build_aux(frame, cluster_map, seed=self.seed)
+        layers = initialize(frame, cluster_map, self.palette)
+        state = SolverState(frame=frame, palette=self.palette, layers=layers, aux=aux,
+                            weights=self.weights, config=self.config)
+        if self.config.refine:
+            self.palette, _ = refine_palette(state)
+        else:
+            state.config = replace(state.config, refine=False)
+            flip_flop(state)
+            self.palette = state.palette
+        state.cluster_map = cluster_map
+        self.index = 1
+        self.prev_layers = state.layers
+        self.prev_chroma = chromaticity(frame)
+        return state
+
+    def step(self, frame) -> SolverState:
+        frame = _as_frame(frame)
+        cmap = segment(frame, self.palette)
+        aux = build_aux(frame, cmap, seed=self.seed + self.index, prev_chroma=self.prev_chroma,
+                        prev_r=self.prev_layers.r)
+        layers = initialize(frame, cmap, self.palette, previous=self.prev_layers)
+        state = SolverState(frame=frame, palette=self.palette, layers=layers, aux=aux,
+                            weights=self.weights, config=self.stream_cfg)
+        flip_flop(state)
+        state.cluster_map = cmap
+        self.index += 1
+        self.prev_layers = state.layers
+        self.prev_chroma = chromaticity(frame)
+        return state
+
+
 def decompose_frames(frames: list, weights: EnergyWeights, config: SolveConfig, seed: int = 0,
                      k_max: int = 10, clicks: list | None = None, streaming_outer: int = 2,
                      palette: BaseColorPalette | None = None,
@@ -66,50 +119,18 @@ def decompose_frames(frames: list, weights: EnergyWeights, config: SolveConfig, 
     f0 = _as_frame(frames[0])
     if palette is None:
         palette, cluster_map = estimate_palette(f0, k_max=k_max, seed=seed)
-    elif cluster_map is None:
-        cluster_map = segment(f0, palette)
     result = PipelineResult(palette=palette, layer_stacks=[], cluster_maps=[], regions=[],
                             records=[], statuses=[])
-    t0 = time.perf_counter()
-    aux = build_aux(f0, cluster_map, seed=seed)
-    layers = initialize(f0, cluster_map, palette)
-    state = SolverState(frame=f0, palette=palette, layers=layers, aux=aux, weights=weights,
-                        config=config)
-    if config.refine:
-        palette, _ = refine_palette(state)
-    else:
-        state.config = replace(state.config, refine=False)
-        flip_flop(state)
-        palette = state.palette
-    result.palette = palette
-    result.layer_stacks.append(state.layers)
-    result.cluster_maps.append(cluster_map)
-    result.records.append(state.records)
-    result.statuses.append(state.status)
-    result.frame_seconds.append(time.perf_counter() - t0)
-    if on_frame is not None:
-        on_frame(0, state)
-
-    stream_cfg = replace(config, refine=False, outer_iterations=streaming_outer)
-    prev_layers = state.layers
-    prev_chroma = chromaticity(f0)
-    for idx in range(1, len(frames)):
+    dec = StreamingDecomposer(palette, weights, config, seed=seed, streaming_outer=streaming_outer)
+    for idx, f in enumerate(frames):
         t0 = time.perf_counter()
-        frame = _as_frame(frames[idx])
-        cmap = segment(frame, palette)
-        aux = build_aux(frame, cmap, seed=seed + idx, prev_chroma=prev_chroma,
-                        prev_r=prev_layers.r)
-        layers = initialize(frame, cmap, palette, previous=prev_layers)
-        state = SolverState(frame=frame, palette=palette, layers=layers, aux=aux,
-                            weights=weights, config=stream_cfg)
-        flip_flop(state)
+        state = dec.first(f0, cluster_map) if idx == 0 else dec.step(f)
         result.layer_stacks.append(state.layers)
-        result.cluster_maps.append(cmap)
+        result.cluster_maps.append(state.cluster_map)
         result.records.append(state.records)
         result.statuses.append(state.status)
         result.frame_seconds.append(time.perf_counter() - t0)
         if on_frame is not None:
             on_frame(idx, state)
-        prev_layers = state.layers
-        prev_chroma = chromaticity(frame)
+    result.palette = dec.palette
     return result
