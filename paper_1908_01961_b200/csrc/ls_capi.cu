@@ -8,10 +8,12 @@
 // and line-search trials; the host synchronises once per trial to read the
 // energies (the accept/reject branch of solver.py:169-178).
 #include <cub/device/device_scan.cuh>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -40,6 +42,34 @@ static thread_local std::string g_err;
     }                            \
   } while (0)
 
+// ---- TMA descriptors (driver entry point fetched through the runtime) ------
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// planes x H x W float32 tensor, box (boxw, boxh, planes)
+static bool make_map(CUtensorMap* m, const float* base, int W, int H, int planes, int boxw, int boxh) {
+  auto fn = tma_encode_fn();
+  if (!fn || ((uintptr_t)base & 15) || (W % 4) != 0) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * H * 4};
+  cuuint32_t box[3] = {(cuuint32_t)boxw, (cuuint32_t)boxh, (cuuint32_t)planes};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct MaxOp {
   __host__ __device__ int operator()(int a, int b) const { return a > b ? a : b; }
 };
@@ -58,6 +88,7 @@ struct Prof {
 struct ls_ctx {
   long long launches = 0;                      // every kernel this context launched
   Prof prof;
+  bool use_tma = false;
   int dev = 0, H = 0, W = 0, N = 0, K = 0, NT = 0, U = 0;
   ls_weights w{};
   ls_solve_cfg cfg{};
@@ -218,6 +249,7 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   const int64_t upd_blocks = (M / 4 + kThreads - 1) / kThreads;
   c->grid_update = (int)std::max<int64_t>(1, std::min<int64_t>({upd_blocks, (int64_t)c->nsm * std::max(1, update_grid_limit()), (int64_t)kMaxBlocks}));
   c->grid_dense = std::max(1, std::min(c->nsm * 4, (N + 127) / 128));
+  c->use_tma = (W % 4 == 0) && tma_encode_fn() != nullptr && std::getenv("LS_NO_TMA") == nullptr;
   cudaError_t e = cudaSuccess;
 #define A_(expr) \
   if (e == cudaSuccess) e = (expr)
@@ -582,6 +614,16 @@ static void prof_harvest(ls_ctx* c) {
   c->prof.next = 0;
 }
 
+// tile descriptors for state X and operand v (both U planes); false -> no TMA
+static bool tile_maps(ls_ctx* c, const float* X, const float* v, TileMaps* m) {
+  if (!c->use_tma) return false;
+  const int U = c->U, NT = c->NT, W = c->W, H = c->H;
+  const size_t N = (size_t)c->N;
+  return make_map(&m->X, X, W, H, U, tile_box_w(), kTileH + 2) &&
+         make_map(&m->T, v + 3 * N, W, H, NT, tile_box_w(), kTileH + 2) &&
+         make_map(&m->R, v, W, H, 3, tile_box_rw(), kTileH + 2 * kHalf);
+}
+
 static Launch L_energy(ls_ctx* c) { return Launch{c->grid_energy, c->ntiles, c->stream}; }
 static Launch L_apply(ls_ctx* c) { return Launch{c->grid_apply, c->ntiles, c->stream}; }
 static Launch L_update(ls_ctx* c) { return Launch{c->grid_update, 0, c->stream}; }
@@ -592,7 +634,7 @@ int ls_energy_terms(ls_ctx* c, const double* colors, const float* X, const float
   LS_ARG(colors || c->K == 0, "null palette");
   LS_ARG(X && Y && terms, "bad arguments");
   LS_CK(cudaSetDevice(c->dev));
-  const Coef<double> cd = make_coef<double>(c->w, colors, c->K);
+  const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
   launch_energy_ext(L_energy(c), frame_of(c), cd, X, Y, c->part, c->tickets + 0, c->sc);
   LS_CK(cudaGetLastError());
   LS_CK(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
@@ -606,7 +648,7 @@ int ls_grad_diag(ls_ctx* c, const double* colors, const float* X, float* b, floa
   if (rc) return rc;
   LS_ARG(X && b && diag, "bad arguments");
   LS_CK(cudaSetDevice(c->dev));
-  const Coef<double> cd = make_coef<double>(c->w, colors, c->K);
+  const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
   launch_energy(0, L_energy(c), frame_of(c), cd, X, nullptr, 0.f, nullptr, nullptr, nullptr, nullptr, b, diag,
                 c->part, c->tickets + 0, c->sc);
   LS_CK(cudaGetLastError());
@@ -619,7 +661,9 @@ int ls_apply_normal(ls_ctx* c, const double* colors, const float* X, const float
   LS_ARG(X && p && Ap, "bad arguments");
   LS_CK(cudaSetDevice(c->dev));
   const Coef<float> cf = make_coef<float>(c->w, colors, c->K);
-  launch_apply(L_apply(c), frame_of(c), cf, X, p, Ap, c->part, c->tickets + 1, nullptr, 0);
+  TileMaps maps;
+  const bool tma = tile_maps(c, X, p, &maps);
+  launch_apply(L_apply(c), frame_of(c), cf, X, p, Ap, c->part, c->tickets + 1, nullptr, 0, tma ? &maps : nullptr);
   LS_CK(cudaGetLastError());
   return LS_OK;
 }
@@ -627,16 +671,18 @@ int ls_apply_normal(ls_ctx* c, const double* colors, const float* X, const float
 // fused energy/gradient + PCG loop; x receives the step
 static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, float* x) {
   const Frame f = frame_of(c);
-  const Coef<double> cd = make_coef<double>(c->w, colors, c->K);
+  const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
   const Coef<float> cf = make_coef<float>(c->w, colors, c->K);
   size_t pi = prof_begin(c);
   launch_energy(0, L_energy(c), f, cd, X, nullptr, 0.f, nullptr, c->r, c->d, c->u, nullptr, nullptr, c->part,
                 c->tickets + 0, c->sc);
   prof_end(c, PC_EG, pi);
   const int64_t M = (int64_t)c->U * c->N;
+  TileMaps maps;
+  const bool tma = tile_maps(c, X, c->u, &maps);
   for (int it = 0; it < iters; ++it) {
     pi = prof_begin(c);
-    launch_apply(L_apply(c), f, cf, X, c->u, c->wv, c->part, c->tickets + 1, c->sc, it);
+    launch_apply(L_apply(c), f, cf, X, c->u, c->wv, c->part, c->tickets + 1, c->sc, it, tma ? &maps : nullptr);
     prof_end(c, PC_APPLY, pi);
     pi = prof_begin(c);
     launch_update(L_update(c), M, x, c->r, c->p, c->s, c->wv, c->d, c->u, c->part, c->tickets + 2, c->sc, it);
@@ -678,7 +724,7 @@ int ls_gn_step(ls_ctx* c, const double* colors, const float* X, float* X_out, ls
   rc = run_pcg(c, colors, X, c->cfg.pcg_iterations, c->x);
   if (rc) return rc;
   const Frame f = frame_of(c);
-  const Coef<double> cd = make_coef<double>(c->w, colors, c->K);
+  const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
   double alpha = 1.0;
   double e0 = 0.0, e1 = 0.0;
   bool accepted = false;
@@ -792,7 +838,7 @@ int ls_dense_step(ls_ctx* c, double* colors, const float* X, double* applied, ls
     for (double& v : db) v = v * (c->cfg.max_delta_b / big);
   const Frame f = frame_of(c);
   auto energy_with = [&](const double* cols, double* out) -> int {
-    const Coef<double> cd = make_coef<double>(c->w, cols, K);
+    const Coef<float> cd = make_coef<float>(c->w, cols, K);
     launch_energy_ext(L_energy(c), f, cd, X, X, c->part, c->tickets + 0, c->sc);
     c->launches += 1;
     LS_CK(cudaGetLastError());

@@ -8,6 +8,14 @@
 
 namespace ls {
 
+// TMA descriptors of one tile (built on the host per operand buffer):
+//   X  state planes,   box {kSW, kTileH+2, U}   at (tx0-1, ty0-1, 0)
+//   T  operand T part,  box {kSW, kTileH+2, NT}  at (tx0-1, ty0-1, 0)
+//   R  operand r part,  box {kRW, kTileH+14, 3}  at (tx0-7, ty0-7, 0)
+struct TileMaps {
+  CUtensorMap X, T, R;
+};
+
 struct Launch {
   int grid;
   int ntiles;
@@ -15,16 +23,19 @@ struct Launch {
 };
 
 // ls_solver.cu
-void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<double>& c, const float* X,
+void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
                    const float* dx, float alpha, float* Xout, float* r_out, float* d_out, float* u_out,
                    float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc);
-void launch_energy_ext(const Launch& L, const Frame& f, const Coef<double>& c, const float* X,
+void launch_energy_ext(const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
                        const float* Y, double* part, unsigned* ticket, Scalars* sc);
 void launch_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* u,
-                  float* w, double* part, unsigned* ticket, Scalars* sc, int iter);
+                  float* w, double* part, unsigned* ticket, Scalars* sc, int iter, const TileMaps* maps);
+int tile_box_w();
+int tile_box_rw();
 void launch_update(const Launch& L, int64_t M, float* x, float* r, float* p, float* s, const float* w,
                    const float* d, float* u, double* part, unsigned* ticket, Scalars* sc, int iter);
 int energy_grid_limit(int NT);
+void prepare_kernels(int NT);
 int apply_grid_limit(int NT);
 int update_grid_limit();
 

@@ -3,18 +3,25 @@
 //   k_energy<NT, MODE_EG>    fused: 8 term energies at the linearisation point,
 //                            b = -J^T F, diag(J^T J), Jacobi PCG init
 //                            (energy.py:194-511, solver.py:125-140, 79-91)
-//   k_energy<NT, MODE_TRIAL> line-search trial: candidate X + a*dx written,
-//                            8 energies with weights frozen at X
-//                            (solver.py:166-178)
+//   k_energy<NT, MODE_TRIAL> line-search trial: candidate Y = X + a*dx (or an
+//                            external Y) written, 8 energies with the IRLS
+//                            weights frozen at X (solver.py:166-178)
 //   k_apply<NT>              w = J^T J u (matrix-free, solver.py:110-122)
 //                            + <w,u>; last block advances the PCG scalars
 //   k_update                 Chronopoulos-Gear vector update + <r,u>, |r|^2
 //
-// All heavy kernels are persistent over 32x8 pixel tiles (one warp per tile
-// row, one pixel per thread, coalesced plane rows); the 3 log-reflectance
-// planes of the operand are staged in shared memory with the 7-pixel halo
-// the consistency window needs (energy.py:23, 161-173).  Reductions are
-// fp64, fixed-order, finished by the last block (no float atomics).
+// Tile scheme: persistent blocks of 256 threads walk 32x8 pixel tiles (one
+// warp per tile row).  Each tile stages in shared memory
+//   sX  all U state planes, tile + 1-pixel halo   (frozen weights, data term)
+//   sT  the T planes of the operand, + 1 halo     (smoothness stencil)
+//   sR  the 3 r planes of the operand, + 7 halo   (r-sparsity stencil and the
+//                                                   15x15 consistency window,
+//                                                   energy.py:23, 161-173)
+// with coalesced row loads, so every HBM word is read once per tile and all
+// neighbour / partner reads hit shared memory.  IRLS weights are recomputed
+// from sX (cheaper than storing 2K+3 weight planes).  Per-pixel arithmetic is
+// fp32 (the data residual exactly rounded via fp64 FMA); reductions are fp64,
+// fixed order, finished by the last block (no float atomics).
 #include "ls_common.cuh"
 #include "ls_kernels.h"
 
@@ -22,37 +29,21 @@ namespace ls {
 
 enum { MODE_EG = 0, MODE_TRIAL = 1 };
 
-template <typename R>
-struct PixCtx {
-  int x, y, i, W, H, N;
-};
+// shared-memory tile geometry (row widths padded to 16-byte TMA boxes)
+// TMA requires the innermost box start to be 16-byte aligned, so the 1-halo
+// window starts 4 columns left of the tile and the 7-halo window 8 columns.
+constexpr int kSX = 4;                // column of tile x = 0 in a 1-halo row
+constexpr int kSW = 40;               // 1-halo rows: cols tx0-4 .. tx0+35
+constexpr int kSH = kTileH + 2;       // rows ty0-1 .. ty0+8
+constexpr int kSP = kSW * kSH;        // floats per 1-halo plane
+constexpr int kRX = 8;                // column of tile x = 0 in a 7-halo row
+constexpr int kRW = 48;               // 7-halo rows: cols tx0-8 .. tx0+39
+constexpr int kRP = kRW * kHaloH;     // rows ty0-7 .. ty0+14 (48 x 22)
 
-// r-sparsity weight at pixel (x, y) from the state planes (energy.py:301-305)
-template <typename R>
-__device__ __forceinline__ R w_rs_at(const float* __restrict__ X, int N, int W, int H, int x, int y,
-                                     const Coef<R>& c) {
-  const int i = y * W + x;
-  R sx = 0, sy = 0;
-#pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    const R v = (R)__ldg(X + ch * N + i);
-    const R gx = (x < W - 1) ? (R)__ldg(X + ch * N + i + 1) - v : R(0);
-    const R gy = (y < H - 1) ? (R)__ldg(X + ch * N + i + W) - v : R(0);
-    sx += gx * gx;
-    sy += gy * gy;
-  }
-  return c.lam_rs * irlsp<R>(sqrt(sx + sy), c);
-}
-
-// smoothness weights of layer k at (x,y) in x and y (energy.py:314-318)
-template <typename R>
-__device__ __forceinline__ R w_smx_at(const float* __restrict__ Tk, int W, int i, const Coef<R>& c) {
-  return c.lam_sm * irls1<R>((R)__ldg(Tk + i + 1) - (R)__ldg(Tk + i), c.eps_irls, c.inv_eps);
-}
-template <typename R>
-__device__ __forceinline__ R w_smy_at(const float* __restrict__ Tk, int W, int i, const Coef<R>& c) {
-  return c.lam_sm * irls1<R>((R)__ldg(Tk + i + W) - (R)__ldg(Tk + i), c.eps_irls, c.inv_eps);
-}
+__host__ __device__ constexpr int pad32(int v) { return (v + 31) & ~31; }   // 128-byte regions
+__host__ __device__ constexpr int off_T(int NT) { return pad32((NT + 3) * kSP); }
+__host__ __device__ constexpr int off_R(int NT, bool has_T) { return off_T(NT) + (has_T ? pad32(NT * kSP) : 0); }
+__host__ __device__ constexpr int tile_floats(int NT, bool has_T) { return off_R(NT, has_T) + pad32(3 * kRP); }
 
 __device__ __forceinline__ void tile_coords(int tile, int W, int& tx0, int& ty0) {
   const int ntx = (W + kTileW - 1) / kTileW;
@@ -60,233 +51,345 @@ __device__ __forceinline__ void tile_coords(int tile, int W, int& tx0, int& ty0)
   ty0 = (tile / ntx) * kTileH;
 }
 
+// MUFU reciprocal / rsqrt (one instruction).  The IRLS weights only have to
+// be the same deterministic function in every kernel; 1-ulp differences to
+// the fp64 reference are far below the solver's tolerance.
+__device__ __forceinline__ float rcpf(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float rsqrtf_fast(float v) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+// smoothness / i-sparsity IRLS factor (p = 1): 1/|g| above eps, else 1/eps
+__device__ __forceinline__ float irls1f(float g, const Coef<float>& c) {
+  g = fabsf(g);
+  return g >= c.eps_irls ? rcpf(g) : c.inv_eps;
+}
+
+// r-sparsity IRLS factor from the squared gradient magnitude s = |grad r|^2
+__device__ __forceinline__ float irls_sq(float s, const Coef<float>& c) {
+  if (c.p == 1.f) return s >= c.eps_irls * c.eps_irls ? rsqrtf_fast(s) : c.inv_eps;
+  if (c.p >= 2.f) return 1.f;
+  const float mag = sqrtf(s);
+  if (!(mag >= c.floor_rs)) return c.inv_eps;
+  return powf(mag, c.p - 2.f);
+}
+
+// r-sparsity weight at smem coords (ix, iy) of the 1-halo state tile; hx / hy
+// say whether the pixel has a right / lower neighbour in the image
+__device__ __forceinline__ float wrs_s(const float* sX, int ix, int iy, bool hx, bool hy, const Coef<float>& c) {
+  float sx = 0.f, syy = 0.f;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    const float* P = sX + ch * kSP;
+    const float v = P[iy * kSW + ix];
+    const float gx = hx ? P[iy * kSW + ix + 1] - v : 0.f;
+    const float gy = hy ? P[(iy + 1) * kSW + ix] - v : 0.f;
+    sx = fmaf(gx, gx, sx);
+    syy = fmaf(gy, gy, syy);
+  }
+  return c.lam_rs * irls_sq(sx + syy, c);
+}
+
+// cooperative row loads of one tile: each warp takes whole (plane, row)
+// segments, lanes walk the columns -- coalesced, no per-element div/mod.
+// WIDTH x ROWS window starting HALO pixels up/left of the tile corner;
+// optional Y = X + alpha*dx on the fly.
+template <int NPL, int WIDTH, int ROWS, int XOFF, int HALO>
+__device__ __forceinline__ void load_rows(float* dst, const float* __restrict__ src, const float* __restrict__ dx,
+                                          float alpha, int N, int W, int H, int tx0, int ty0) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int NW = kThreads / 32;
+#pragma unroll 2
+  for (int pr = wid; pr < NPL * ROWS; pr += NW) {
+    const int p = pr / ROWS, r = pr - p * ROWS;
+    const int gy = ty0 - HALO + r;
+    const bool rowok = gy >= 0 && gy < H;
+    const size_t rowoff = (size_t)p * N + (size_t)(rowok ? gy : 0) * W;
+    float* d = dst + p * (ROWS * WIDTH) + r * WIDTH;
+#pragma unroll
+    for (int cc = lane; cc < WIDTH; cc += 32) {
+      const int gx = tx0 - XOFF + cc;
+      float v = 0.f;
+      if (rowok && gx >= 0 && gx < W) {
+        v = __ldg(src + rowoff + gx);
+        if (dx) v = __fmaf_rn(alpha, __ldg(dx + rowoff + gx), v);
+      }
+      d[cc] = v;
+    }
+  }
+}
+
+template <int NPL>
+__device__ __forceinline__ void load_halo1(float* dst, const float* __restrict__ src, int N, int W, int H, int tx0,
+                                           int ty0) {
+  load_rows<NPL, kSW, kSH, kSX, 1>(dst, src, nullptr, 0.f, N, W, H, tx0, ty0);
+}
+
+template <int NPL>
+__device__ __forceinline__ void load_halo1_axpy(float* dst, const float* __restrict__ X, const float* __restrict__ dx,
+                                                float alpha, int N, int W, int H, int tx0, int ty0) {
+  load_rows<NPL, kSW, kSH, kSX, 1>(dst, X, dx, alpha, N, W, H, tx0, ty0);
+}
+
+__device__ __forceinline__ void load_halo7(float* dst, const float* __restrict__ src, const float* __restrict__ dx,
+                                           float alpha, int N, int W, int H, int tx0, int ty0) {
+  load_rows<3, kRW, kHaloH, kRX, kHalf>(dst, src, dx, alpha, N, W, H, tx0, ty0);
+}
+
+// TMA boxes of one tile: all state planes / operand T planes (1 halo) and the
+// operand r planes (7 halo); see TileMaps in ls_kernels.h
+template <int NT>
+__device__ __forceinline__ void tma_issue_tile(float* stage, const TileMaps& m, uint64_t* bar, int tx0, int ty0) {
+  constexpr uint32_t bytes = sizeof(float) * ((NT + 3) * kSP + NT * kSP + 3 * kRP);
+  mbar_expect_tx(bar, bytes);
+  tma_load_3d(stage, &m.X, bar, tx0 - kSX, ty0 - 1, 0);
+  tma_load_3d(stage + off_T(NT), &m.T, bar, tx0 - kSX, ty0 - 1, 0);
+  tma_load_3d(stage + off_R(NT, true), &m.R, bar, tx0 - kRX, ty0 - kHalf, 0);
+}
+
 // ---------------------------------------------------------------------------
-// energy (+ gradient / diagonal / PCG init) kernel, fp64 per-pixel arithmetic
+// energy (+ gradient / diagonal / PCG init) kernel
 // ---------------------------------------------------------------------------
 template <int NT, int MODE>
-__global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<double> c, const float* __restrict__ X,
+__global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, const float* __restrict__ X,
                                                      const float* __restrict__ dx, float alpha,
                                                      const float* __restrict__ Yext, float* __restrict__ Xout,
                                                      float* __restrict__ r_out, float* __restrict__ d_out,
                                                      float* __restrict__ u_out, float* __restrict__ b_raw,
                                                      float* __restrict__ diag_raw, double* part,
                                                      unsigned* ticket, Scalars* sc, int ntiles) {
+  constexpr int U = NT + 3;
   constexpr int NV = (MODE == MODE_EG) ? kTerms + 2 : kTerms;
-  __shared__ float sy[3][kHaloH][kHaloW];
+  extern __shared__ float smem[];
+  float* sX = smem;                                        // U 1-halo planes (frozen state)
+  float* sT = smem + off_T(NT);                            // NT 1-halo planes (eval point), trial only
+  float* sR = smem + off_R(NT, MODE == MODE_TRIAL);        // 3 7-halo planes (eval point r)
   const int W = f.W, H = f.H, N = f.N;
   const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+  const int cx = lx + kSX, cy = ly + 1, rx = lx + kRX, ry = ly + kHalf;
   double acc[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) acc[j] = 0.0;
-  // trial: with an empty PCG step the update is zero (solver.py:85-86)
-  bool use_dx = (MODE == MODE_TRIAL) && dx != nullptr && sc->iterations > 0;
-  const float a = alpha;
-  auto Yat = [&](int plane, int idx) -> float {
-    if (MODE == MODE_TRIAL && Yext) return __ldg(Yext + (size_t)plane * N + idx);
-    float v = __ldg(X + (size_t)plane * N + idx);
-    if (MODE == MODE_TRIAL && use_dx) v = __fmaf_rn(a, __ldg(dx + (size_t)plane * N + idx), v);
-    return v;
-  };
+  // trial: an empty PCG step means a zero update (solver.py:85-86)
+  const float* dxe = (MODE == MODE_TRIAL && dx != nullptr && sc->iterations > 0) ? dx : nullptr;
+  const float* Ysrc = (MODE == MODE_TRIAL && Yext) ? Yext : X;
+  if (MODE == MODE_TRIAL && Yext) dxe = nullptr;
+  const float* sYT = (MODE == MODE_TRIAL) ? sT : sX + 3 * kSP;   // eval-point T planes
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     int tx0, ty0;
     tile_coords(tile, W, tx0, ty0);
     __syncthreads();
-    for (int e = threadIdx.x; e < 3 * kHaloH * kHaloW; e += kThreads) {
-      const int ch = e / (kHaloH * kHaloW), rem = e % (kHaloH * kHaloW);
-      const int yy = rem / kHaloW, xx = rem % kHaloW;
-      const int gy = ty0 + yy - kHalf, gx = tx0 + xx - kHalf;
-      sy[ch][yy][xx] = (gx >= 0 && gx < W && gy >= 0 && gy < H) ? Yat(ch, gy * W + gx) : 0.f;
-    }
+    load_halo1<U>(sX, X, N, W, H, tx0, ty0);
+    if (MODE == MODE_TRIAL) load_halo1_axpy<NT>(sT, Ysrc + 3 * (size_t)N, dxe ? dxe + 3 * (size_t)N : nullptr, alpha,
+                                                N, W, H, tx0, ty0);
+    load_halo7(sR, Ysrc, dxe, alpha, N, W, H, tx0, ty0);
     __syncthreads();
     const int x = tx0 + lx, y = ty0 + ly;
     if (x >= W || y >= H) continue;
     const int i = y * W + x;
+    const bool hx = x < W - 1, hy = y < H - 1, hl = x > 0, hu = y > 0;
 
-    // --- state at x (linearisation point) and evaluation point Y ---
-    double r0[3], T0[NT], yr[3], yT[NT];
+    float r0[3], T0[NT], yr[3], yT[NT];
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      r0[ch] = (double)__ldg(X + ch * N + i);
-      yr[ch] = (double)sy[ch][ly + kHalf][lx + kHalf];
+      r0[ch] = sX[ch * kSP + cy * kSW + cx];
+      yr[ch] = sR[ch * kRP + ry * kRW + rx];
     }
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
-      T0[k] = (double)__ldg(X + (size_t)(3 + k) * N + i);
-      yT[k] = (MODE == MODE_EG) ? T0[k] : (double)Yat(3 + k, i);
+      T0[k] = sX[(3 + k) * kSP + cy * kSW + cx];
+      yT[k] = sYT[k * kSP + cy * kSW + cx];
     }
-    double img[3], anc[3];
+    float img[3], anc[3];
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) img[ch] = (double)__ldg(f.img + ch * N + i);
+    for (int ch = 0; ch < 3; ++ch) img[ch] = __ldg(f.img + ch * N + i);
     if (f.ids) {
       const int id = __ldg(f.ids + i);
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) anc[ch] = c.anchor[id][ch];
     } else {
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch) anc[ch] = (double)__ldg(f.anchor + ch * N + i);
+      for (int ch = 0; ch < 3; ++ch) anc[ch] = __ldg(f.anchor + ch * N + i);
     }
-    const double edge = (double)__ldg(f.edge + i);
+    const float lm = c.lam_m * __ldg(f.edge + i);
 
-    // --- data (energy.py:207-209) and monochrome (energy.py:399-401) ---
-    double S[3], R[3];
+    // data (energy.py:207-209), clustering (234-235), monochrome (399-401)
+    float S[3], R[3], res[3], m[3];
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      double s = 0.0;
+      float s = 0.f;
 #pragma unroll
-      for (int k = 0; k < NT; ++k) s += yT[k] * c.B[k][ch];
+      for (int k = 0; k < NT; ++k) s = fmaf(yT[k], c.B[k][ch], s);
       S[ch] = s;
-      R[ch] = exp(yr[ch]);
+      R[ch] = expf(yr[ch]);
+      res[ch] = (float)fma(-(double)R[ch], (double)S[ch], (double)img[ch]);   // exactly rounded
+      acc[T_DATA] += (double)c.lam_d * ((double)res[ch] * (double)res[ch]);
+      const float dc = yr[ch] - anc[ch];
+      acc[T_CLUSTER] += (double)(c.lam_cl * dc * dc);
     }
-    double res[3];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      res[ch] = img[ch] - R[ch] * S[ch];
-      acc[T_DATA] += c.lam_d * res[ch] * res[ch];
-      const double dc = yr[ch] - anc[ch];
-      acc[T_CLUSTER] += c.lam_cl * dc * dc;
-    }
-    const double mean = (S[0] + S[1] + S[2]) / 3.0;
-    double m[3];
+    const float mean = (S[0] + S[1] + S[2]) * (1.f / 3.f);
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
       m[ch] = S[ch] - mean;
-      acc[T_MONO] += c.lam_m * edge * m[ch] * m[ch];
+      acc[T_MONO] += (double)(lm * m[ch] * m[ch]);
     }
 
-    // --- r-sparsity at x (weights from X, gradient of Y) ---
-    const double wrs = w_rs_at<double>(X, N, W, H, x, y, c);
+    // r-sparsity: weight from X, gradient of Y (energy.py:264-267, 301-305)
+    const float wrs = wrs_s(sX, cx, cy, hx, hy, c);
     {
-      double e = 0.0;
+      float e = 0.f;
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
-        const double gx = (x < W - 1) ? (double)sy[ch][ly + kHalf][lx + kHalf + 1] - yr[ch] : 0.0;
-        const double gy = (y < H - 1) ? (double)sy[ch][ly + kHalf + 1][lx + kHalf] - yr[ch] : 0.0;
-        e += gx * gx + gy * gy;
+        const float* P = sR + ch * kRP;
+        const float gx = hx ? P[ry * kRW + rx + 1] - yr[ch] : 0.f;
+        const float gy = hy ? P[(ry + 1) * kRW + rx] - yr[ch] : 0.f;
+        e = fmaf(gx, gx, fmaf(gy, gy, e));
       }
-      acc[T_RSPARSE] += wrs * e;
+      acc[T_RSPARSE] += (double)(wrs * e);
     }
 
-    // --- per-layer diagonal terms and smoothness ---
-    double wis[NT], wnn[NT], axx[NT], ayy[NT];
+    // per-layer diagonal terms and smoothness (energy.py:414-452, 308-318)
+    float wd[NT];
+    {
+      float eis = 0.f, enn = 0.f, esm = 0.f;
 #pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      wis[k] = (k >= 1) ? c.lam_is * irls1<double>(T0[k], c.eps_irls, c.inv_eps) : 0.0;
-      wnn[k] = c.lam_nn * nonneg_w<double>(T0[k], c.eps_nn);
-      acc[T_ISPARSE] += wis[k] * yT[k] * yT[k];
-      acc[T_NONNEG] += wnn[k] * yT[k] * yT[k];
-      const float* Tk = X + (size_t)(3 + k) * N;
-      axx[k] = (x < W - 1) ? w_smx_at<double>(Tk, W, i, c) : 0.0;
-      ayy[k] = (y < H - 1) ? w_smy_at<double>(Tk, W, i, c) : 0.0;
-      const double gx = (x < W - 1) ? (double)Yat(3 + k, i + 1) - yT[k] : 0.0;
-      const double gy = (y < H - 1) ? (double)Yat(3 + k, i + W) - yT[k] : 0.0;
-      acc[T_SMOOTH] += axx[k] * gx * gx + ayy[k] * gy * gy;
-    }
-
-    // --- consistency pairs (energy.py:348-350); each pair counted at its src ---
-    double gcons[3] = {0.0, 0.0, 0.0}, dcons = 0.0;
-    const int e0 = __ldg(f.row_ptr + i), e1 = __ldg(f.row_ptr + i + 1);
-    for (int e = e0; e < e1; ++e) {
-      const uint16_t ent = __ldg(f.ent + e);
-      const double we = c.lam_rc * (f.ent_w ? (double)__ldg(f.ent_w + e) : 1.0);
-      int ddy, ddx;
-      decode_offset(ent, ddy, ddx);
-      double part_v[3];
-      if (ent & kEntTemporal) {
-        const int q = i + ddy * W + ddx;
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) part_v[ch] = (double)__ldg(f.prev_r + ch * N + q);
-      } else {
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) part_v[ch] = (double)sy[ch][ly + kHalf + ddy][lx + kHalf + ddx];
-      }
-      if (!(ent & kEntIncoming)) {
-        double e2 = 0.0;
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const double dd = yr[ch] - part_v[ch];
-          e2 += dd * dd;
+      for (int k = 0; k < NT; ++k) {
+        const float* P = sX + (3 + k) * kSP;
+        const float* Q = sYT + k * kSP;
+        const float wis = (k >= 1) ? c.lam_is * irls1f(T0[k], c) : 0.f;
+        const float wnn = c.lam_nn * nonneg_w<float>(T0[k], c.eps_nn);
+        wd[k] = wis + wnn;
+        eis = fmaf(wis * yT[k], yT[k], eis);
+        enn = fmaf(wnn * yT[k], yT[k], enn);
+        if (hx) {
+          const float ax = c.lam_sm * irls1f(P[cy * kSW + cx + 1] - T0[k], c);
+          const float g = Q[cy * kSW + cx + 1] - yT[k];
+          esm = fmaf(ax * g, g, esm);
         }
-        acc[T_CONSIST] += we * e2;
+        if (hy) {
+          const float ay = c.lam_sm * irls1f(P[(cy + 1) * kSW + cx] - T0[k], c);
+          const float g = Q[(cy + 1) * kSW + cx] - yT[k];
+          esm = fmaf(ay * g, g, esm);
+        }
       }
-      if (MODE == MODE_EG) {
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) gcons[ch] += we * (yr[ch] - part_v[ch]);
+      acc[T_ISPARSE] += (double)eis;
+      acc[T_NONNEG] += (double)enn;
+      acc[T_SMOOTH] += (double)esm;
+    }
+
+    // consistency pairs (energy.py:348-350): energy counted at each pair's
+    // src; gradient / diagonal from every incident pair (energy.py:359-381)
+    float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, dcons = 0.f;
+    {
+      const int e0 = __ldg(f.row_ptr + i), e1 = __ldg(f.row_ptr + i + 1);
+      float ec = 0.f;
+      for (int e = e0; e < e1; ++e) {
+        const uint16_t ent = __ldg(f.ent + e);
+        const float we = c.lam_rc * (f.ent_w ? __ldg(f.ent_w + e) : 1.f);
+        int ddy, ddx;
+        decode_offset(ent, ddy, ddx);
+        float p0, p1, p2;
+        if (ent & kEntTemporal) {
+          const int q = i + ddy * W + ddx;
+          p0 = __ldg(f.prev_r + q);
+          p1 = __ldg(f.prev_r + N + q);
+          p2 = __ldg(f.prev_r + 2 * N + q);
+        } else {
+          const int o = (ry + ddy) * kRW + rx + ddx;
+          p0 = sR[o];
+          p1 = sR[kRP + o];
+          p2 = sR[2 * kRP + o];
+        }
+        const float d0 = yr[0] - p0, d1 = yr[1] - p1, d2 = yr[2] - p2;
+        if (!(ent & kEntIncoming)) ec = fmaf(we, d0 * d0 + d1 * d1 + d2 * d2, ec);
+        gc0 = fmaf(we, d0, gc0);
+        gc1 = fmaf(we, d1, gc1);
+        gc2 = fmaf(we, d2, gc2);
         dcons += we;
       }
+      acc[T_CONSIST] += (double)ec;
     }
 
     if (MODE == MODE_TRIAL) {
       if (Xout) {
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) Xout[ch * N + i] = (float)yr[ch];
+        for (int ch = 0; ch < 3; ++ch) Xout[ch * N + i] = yr[ch];
 #pragma unroll
-        for (int k = 0; k < NT; ++k) Xout[(size_t)(3 + k) * N + i] = (float)yT[k];
+        for (int k = 0; k < NT; ++k) Xout[(size_t)(3 + k) * N + i] = yT[k];
       }
       continue;
     }
 
-    // ======== MODE_EG: gradient g = J^T F, diag, PCG init ========
-    const double wrs_l = (x > 0) ? w_rs_at<double>(X, N, W, H, x - 1, y, c) : 0.0;
-    const double wrs_u = (y > 0) ? w_rs_at<double>(X, N, W, H, x, y - 1, c) : 0.0;
-    double gr[3], dr[3];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      const double rs = R[ch] * S[ch];
-      double g = -c.lam_d * rs * res[ch] + c.lam_cl * (r0[ch] - anc[ch]);
-      double d = c.lam_d * rs * rs + c.lam_cl;
-      // D^T W D r0 at x (energy.py:272-282), weights shared by channels
-      if (x < W - 1) { g += wrs * (r0[ch] - (double)sy[ch][ly + kHalf][lx + kHalf + 1]); d += wrs; }
-      if (x > 0)     { g += wrs_l * (r0[ch] - (double)sy[ch][ly + kHalf][lx + kHalf - 1]); d += wrs_l; }
-      if (y < H - 1) { g += wrs * (r0[ch] - (double)sy[ch][ly + kHalf + 1][lx + kHalf]); d += wrs; }
-      if (y > 0)     { g += wrs_u * (r0[ch] - (double)sy[ch][ly + kHalf - 1][lx + kHalf]); d += wrs_u; }
-      gr[ch] = g + gcons[ch];
-      dr[ch] = d + dcons;
-    }
+    // ======== MODE_EG: g = J^T F, diag(J^T J), PCG init (Y == X) ========
+    const float wl = hl ? wrs_s(sX, cx - 1, cy, true, hy, c) : 0.f;
+    const float wu = hu ? wrs_s(sX, cx, cy - 1, hx, true, c) : 0.f;
+    const float gcons[3] = {gc0, gc1, gc2};
     double rz = 0.0, bb = 0.0;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      const float bf = (float)(-gr[ch]);
-      const float df = (float)dr[ch];
-      const float dd = df > 0.f ? df : 1.f;
+      const float* P = sX + ch * kSP;
+      const float rs = R[ch] * S[ch];
+      float g = fmaf(-c.lam_d * rs, res[ch], c.lam_cl * (r0[ch] - anc[ch]));
+      float d = fmaf(c.lam_d * rs, rs, c.lam_cl);
+      const float v = r0[ch];
+      if (hx) { g = fmaf(wrs, v - P[cy * kSW + cx + 1], g); d += wrs; }
+      if (hl) { g = fmaf(wl, v - P[cy * kSW + cx - 1], g); d += wl; }
+      if (hy) { g = fmaf(wrs, v - P[(cy + 1) * kSW + cx], g); d += wrs; }
+      if (hu) { g = fmaf(wu, v - P[(cy - 1) * kSW + cx], g); d += wu; }
+      g += gcons[ch];
+      d += dcons;
+      const float bf = -g;
+      const float dd = d > 0.f ? d : 1.f;
       const float uf = bf / dd;
       if (r_out) { r_out[ch * N + i] = bf; d_out[ch * N + i] = dd; u_out[ch * N + i] = uf; }
-      if (b_raw) { b_raw[ch * N + i] = bf; diag_raw[ch * N + i] = df; }
+      if (b_raw) { b_raw[ch * N + i] = bf; diag_raw[ch * N + i] = d; }
       rz += (double)bf * (double)uf;
       bb += (double)bf * (double)bf;
     }
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
-      double g = 0.0, d = 0.0, gm = 0.0, g2 = 0.0;
+      const float* P = sX + (3 + k) * kSP;
+      float g = 0.f, d = 0.f, gm = 0.f, g2 = 0.f;
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
-        g += R[ch] * c.B[k][ch] * res[ch];
-        d += R[ch] * R[ch] * c.B[k][ch] * c.B[k][ch];
-        gm += c.G[k][ch] * m[ch];
-        g2 += c.G[k][ch] * c.G[k][ch];
+        const float rb = R[ch] * c.B[k][ch];
+        g = fmaf(rb, res[ch], g);
+        d = fmaf(rb, rb, d);
+        gm = fmaf(c.G[k][ch], m[ch], gm);
+        g2 = fmaf(c.G[k][ch], c.G[k][ch], g2);
       }
-      g = -c.lam_d * g + c.lam_m * edge * gm + (wis[k] + wnn[k]) * T0[k];
-      d = c.lam_d * d + c.lam_m * edge * g2 + wis[k] + wnn[k];
-      const float* Tk = X + (size_t)(3 + k) * N;
-      if (x < W - 1) { g += axx[k] * (T0[k] - (double)__ldg(Tk + i + 1)); d += axx[k]; }
-      if (x > 0) {
-        const double wl = w_smx_at<double>(Tk, W, i - 1, c);
-        g += wl * (T0[k] - (double)__ldg(Tk + i - 1));
-        d += wl;
+      g = fmaf(-c.lam_d, g, fmaf(lm, gm, wd[k] * T0[k]));
+      d = fmaf(c.lam_d, d, fmaf(lm, g2, wd[k]));
+      const float v = T0[k];
+      if (hx) {
+        const float a = c.lam_sm * irls1f(P[cy * kSW + cx + 1] - v, c);
+        g = fmaf(a, v - P[cy * kSW + cx + 1], g); d += a;
       }
-      if (y < H - 1) { g += ayy[k] * (T0[k] - (double)__ldg(Tk + i + W)); d += ayy[k]; }
-      if (y > 0) {
-        const double wu = w_smy_at<double>(Tk, W, i - W, c);
-        g += wu * (T0[k] - (double)__ldg(Tk + i - W));
-        d += wu;
+      if (hl) {
+        const float a = c.lam_sm * irls1f(v - P[cy * kSW + cx - 1], c);
+        g = fmaf(a, v - P[cy * kSW + cx - 1], g); d += a;
       }
-      const float bf = (float)(-g);
-      const float df = (float)d;
-      const float dd = df > 0.f ? df : 1.f;
+      if (hy) {
+        const float a = c.lam_sm * irls1f(P[(cy + 1) * kSW + cx] - v, c);
+        g = fmaf(a, v - P[(cy + 1) * kSW + cx], g); d += a;
+      }
+      if (hu) {
+        const float a = c.lam_sm * irls1f(v - P[(cy - 1) * kSW + cx], c);
+        g = fmaf(a, v - P[(cy - 1) * kSW + cx], g); d += a;
+      }
+      const float bf = -g;
+      const float dd = d > 0.f ? d : 1.f;
       const float uf = bf / dd;
       const size_t o = (size_t)(3 + k) * N + i;
       if (r_out) { r_out[o] = bf; d_out[o] = dd; u_out[o] = uf; }
-      if (b_raw) { b_raw[o] = bf; diag_raw[o] = df; }
+      if (b_raw) { b_raw[o] = bf; diag_raw[o] = d; }
       rz += (double)bf * (double)uf;
       bb += (double)bf * (double)bf;
     }
@@ -324,147 +427,185 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<double> c, co
 // ---------------------------------------------------------------------------
 // matrix-free normal operator w = J^T J u (fp32), frozen at X
 // ---------------------------------------------------------------------------
-template <int NT>
-__global__ void __launch_bounds__(kThreads) k_apply(Frame f, Coef<float> c, const float* __restrict__ X,
-                                                    const float* __restrict__ u, float* __restrict__ w,
-                                                    double* part, unsigned* ticket, Scalars* sc,
-                                                    int iter, int ntiles) {
-  __shared__ float su[3][kHaloH][kHaloW];
+// TMA path: a 2-stage pipeline per persistent CTA -- thread 0 issues the
+// three boxes of tile j+2 into the stage tile j just released, all threads
+// wait on that stage's mbarrier; no load instructions in the SM.  The
+// fallback (row widths not 16-byte multiples) stages the same layout with
+// cooperative loads.  Image borders are handled by zero-filled halos and
+// multiplicative 0/1 masks (branch-free stencils).
+template <int NT, bool TMA>
+__global__ void __launch_bounds__(kThreads, 2) k_apply(Frame f, Coef<float> c, const float* __restrict__ X,
+                                                       const float* __restrict__ u, float* __restrict__ w,
+                                                       double* part, unsigned* ticket, Scalars* sc, int iter,
+                                                       int ntiles, const __grid_constant__ TileMaps maps) {
+  constexpr int U = NT + 3;
+  constexpr int STAGE = tile_floats(NT, true);
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t bars[2];
   if (sc && sc->stop) return;
   const int W = f.W, H = f.H, N = f.N;
   const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
-  double acc[1] = {0.0};
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    int tx0, ty0;
-    tile_coords(tile, W, tx0, ty0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < 3 * kHaloH * kHaloW; e += kThreads) {
-      const int ch = e / (kHaloH * kHaloW), rem = e % (kHaloH * kHaloW);
-      const int yy = rem / kHaloW, xx = rem % kHaloW;
-      const int gy = ty0 + yy - kHalf, gx = tx0 + xx - kHalf;
-      su[ch][yy][xx] = (gx >= 0 && gx < W && gy >= 0 && gy < H) ? __ldg(u + ch * N + gy * W + gx) : 0.f;
+  const int cx = lx + kSX, cy = ly + 1, rx = lx + kRX, ry = ly + kHalf;
+  const int ntx = (W + kTileW - 1) / kTileW;
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      fence_barrier_init();
+      tma_prefetch_desc(&maps.X);
+      tma_prefetch_desc(&maps.T);
+      tma_prefetch_desc(&maps.R);
+      for (int j = 0; j < 2; ++j) {
+        const int t = blockIdx.x + j * gridDim.x;
+        if (t < ntiles)
+          tma_issue_tile<NT>(smem + j * STAGE, maps, &bars[j], (t % ntx) * kTileW, (t / ntx) * kTileH);
+      }
     }
     __syncthreads();
+  }
+  uint32_t phase = 0;   // bit s: parity of the next wait on stage s
+  float acc = 0.f;
+  double accd = 0.0;
+  for (int j = 0;; ++j) {
+    const int tile = blockIdx.x + j * gridDim.x;
+    if (tile >= ntiles) break;
+    const int tx0 = (tile % ntx) * kTileW, ty0 = (tile / ntx) * kTileH;
+    const int st = TMA ? (j & 1) : 0;
+    float* sX = smem + st * STAGE;
+    float* sT = sX + off_T(NT);
+    float* sR = sX + off_R(NT, true);
+    if (TMA) {
+      mbar_wait(&bars[st], (phase >> st) & 1u);
+      phase ^= 1u << st;
+    } else {
+      __syncthreads();
+      load_halo1<U>(sX, X, N, W, H, tx0, ty0);
+      load_halo1<NT>(sT, u + 3 * (size_t)N, N, W, H, tx0, ty0);
+      load_halo7(sR, u, nullptr, 0.f, N, W, H, tx0, ty0);
+      __syncthreads();
+    }
     const int x = tx0 + lx, y = ty0 + ly;
-    if (x >= W || y >= H) continue;
-    const int i = y * W + x;
+    if (x < W && y < H) {
+      const int i = y * W + x;
+      const float mx = (x < W - 1) ? 1.f : 0.f, ml = (x > 0) ? 1.f : 0.f;
+      const float my = (y < H - 1) ? 1.f : 0.f, mu = (y > 0) ? 1.f : 0.f;
+      const int sc0 = cy * kSW + cx, rc0 = ry * kRW + rx;
 
-    float ur[3], uT[NT], R0[3], S0[3], T0[NT];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      ur[ch] = su[ch][ly + kHalf][lx + kHalf];
-      R0[ch] = expf(__ldg(X + ch * N + i));
-    }
-#pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      uT[k] = __ldg(u + (size_t)(3 + k) * N + i);
-      T0[k] = __ldg(X + (size_t)(3 + k) * N + i);
-    }
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < NT; ++k) s = fmaf(T0[k], c.B[k][ch], s);
-      S0[ch] = s;
-    }
-    // data rows: rho_c = R0 (S0 u_r + sum_k b_kc u_Tk)   (energy.py:211-218)
-    float rho[3], outr[3], outT[NT];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < NT; ++k) s = fmaf(uT[k], c.B[k][ch], s);
-      rho[ch] = R0[ch] * fmaf(S0[ch], ur[ch], s);
-      outr[ch] = c.lam_d * R0[ch] * S0[ch] * rho[ch] + c.lam_cl * ur[ch];
-    }
-    // monochrome: q_c = sum_k G_kc u_Tk  (energy.py:403-408)
-    float q[3];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < NT; ++k) s = fmaf(uT[k], c.G[k][ch], s);
-      q[ch] = s * c.lam_m * __ldg(f.edge + i);
-    }
-#pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      float s = 0.f, m = 0.f;
+      float ur[3], R0[3], S0[3] = {0.f, 0.f, 0.f};
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
-        s = fmaf(R0[ch] * c.B[k][ch], rho[ch], s);
-        m = fmaf(c.G[k][ch], q[ch], m);
+        ur[ch] = sR[ch * kRP + rc0];
+        R0[ch] = __expf(sX[ch * kSP + sc0]);
       }
-      const float wis = (k >= 1) ? c.lam_is * irls1<float>(T0[k], c.eps_irls, c.inv_eps) : 0.f;
-      const float wnn = c.lam_nn * nonneg_w<float>(T0[k], c.eps_nn);
-      outT[k] = c.lam_d * s + m + (wis + wnn) * uT[k];
-    }
-    // r-sparsity: D^T W D u_r
-    {
-      const float wrs = w_rs_at<float>(X, N, W, H, x, y, c);
-      const float wl = (x > 0) ? w_rs_at<float>(X, N, W, H, x - 1, y, c) : 0.f;
-      const float wu = (y > 0) ? w_rs_at<float>(X, N, W, H, x, y - 1, c) : 0.f;
+      float uT[NT], T0[NT];
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        uT[k] = sT[k * kSP + sc0];
+        T0[k] = sX[(3 + k) * kSP + sc0];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) S0[ch] = fmaf(T0[k], c.B[k][ch], S0[ch]);
+      }
+      // data rows rho_c = R0 (S0 u_r + sum_k b_kc u_Tk) (energy.py:211-218),
+      // monochrome q_c = w_edge sum_k G_kc u_Tk (energy.py:403-408)
+      float rho[3], q[3], outr[3];
+      const float lm = c.lam_m * __ldg(f.edge + i);
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
-        const float v = ur[ch];
+        float s = 0.f, qq = 0.f;
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+          s = fmaf(uT[k], c.B[k][ch], s);
+          qq = fmaf(uT[k], c.G[k][ch], qq);
+        }
+        rho[ch] = R0[ch] * fmaf(S0[ch], ur[ch], s);
+        outr[ch] = fmaf(c.lam_d * R0[ch] * S0[ch], rho[ch], c.lam_cl * ur[ch]);
+        q[ch] = qq * lm;
+        rho[ch] *= c.lam_d * R0[ch];
+      }
+      float dot = 0.f;
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        const float* P = sX + (3 + k) * kSP + sc0;
+        const float* Q = sT + k * kSP + sc0;
         float a = 0.f;
-        if (x < W - 1) a += wrs * (v - su[ch][ly + kHalf][lx + kHalf + 1]);
-        if (x > 0)     a += wl * (v - su[ch][ly + kHalf][lx + kHalf - 1]);
-        if (y < H - 1) a += wrs * (v - su[ch][ly + kHalf + 1][lx + kHalf]);
-        if (y > 0)     a += wu * (v - su[ch][ly + kHalf - 1][lx + kHalf]);
-        outr[ch] += a;
-      }
-    }
-    // smoothness: per layer D^T W_k D u_Tk
 #pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      const float* Tk = X + (size_t)(3 + k) * N;
-      const float* uk = u + (size_t)(3 + k) * N;
-      float a = 0.f;
-      if (x < W - 1) a += w_smx_at<float>(Tk, W, i, c) * (uT[k] - __ldg(uk + i + 1));
-      if (x > 0)     a += w_smx_at<float>(Tk, W, i - 1, c) * (uT[k] - __ldg(uk + i - 1));
-      if (y < H - 1) a += w_smy_at<float>(Tk, W, i, c) * (uT[k] - __ldg(uk + i + W));
-      if (y > 0)     a += w_smy_at<float>(Tk, W, i - W, c) * (uT[k] - __ldg(uk + i - W));
-      outT[k] += a;
-    }
-    // consistency graph Laplacian (energy.py:352-370): spatial pairs couple
-    // u(x) - u(q); temporal partners are constant (energy.py:356)
-    {
-      const int e0 = __ldg(f.row_ptr + i), e1 = __ldg(f.row_ptr + i + 1);
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-      for (int e = e0; e < e1; ++e) {
-        const uint16_t ent = __ldg(f.ent + e);
-        const float we = c.lam_rc * (f.ent_w ? __ldg(f.ent_w + e) : 1.f);
-        if (ent & kEntTemporal) {
-          a0 += we * ur[0]; a1 += we * ur[1]; a2 += we * ur[2];
-        } else {
-          int ddy, ddx;
-          decode_offset(ent, ddy, ddx);
-          a0 += we * (ur[0] - su[0][ly + kHalf + ddy][lx + kHalf + ddx]);
-          a1 += we * (ur[1] - su[1][ly + kHalf + ddy][lx + kHalf + ddx]);
-          a2 += we * (ur[2] - su[2][ly + kHalf + ddy][lx + kHalf + ddx]);
+        for (int ch = 0; ch < 3; ++ch) a = fmaf(c.B[k][ch], rho[ch], fmaf(c.G[k][ch], q[ch], a));
+        const float v = T0[k], uv = uT[k];
+        const float wis = (k >= 1) ? c.lam_is * irls1f(v, c) : 0.f;
+        const float wnn = c.lam_nn * nonneg_w<float>(v, c.eps_nn);
+        a = fmaf(wis + wnn, uv, a);
+        // smoothness D^T W_k D u_Tk (energy.py:272-282), weights from X
+        const float axc = mx * irls1f(P[1] - v, c), axl = ml * irls1f(v - P[-1], c);
+        const float ayc = my * irls1f(P[kSW] - v, c), ayu = mu * irls1f(v - P[-kSW], c);
+        float sm = axc * (uv - Q[1]);
+        sm = fmaf(axl, uv - Q[-1], sm);
+        sm = fmaf(ayc, uv - Q[kSW], sm);
+        sm = fmaf(ayu, uv - Q[-kSW], sm);
+        a = fmaf(c.lam_sm, sm, a);
+        w[(size_t)(3 + k) * N + i] = a;
+        dot = fmaf(a, uv, dot);
+      }
+      // r-sparsity D^T W D u_r, one weight per pixel shared by the channels
+      {
+        const float wc = wrs_s(sX, cx, cy, x < W - 1, y < H - 1, c);
+        const float wl = ml * wrs_s(sX, cx - 1, cy, true, y < H - 1, c);
+        const float wu = mu * wrs_s(sX, cx, cy - 1, x < W - 1, true, c);
+        const float wcx = mx * wc, wcy = my * wc;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const float* P = sR + ch * kRP + rc0;
+          const float v = ur[ch];
+          float a = wcx * (v - P[1]);
+          a = fmaf(wl, v - P[-1], a);
+          a = fmaf(wcy, v - P[kRW], a);
+          a = fmaf(wu, v - P[-kRW], a);
+          outr[ch] += a;
         }
       }
-      outr[0] += a0; outr[1] += a1; outr[2] += a2;
-    }
-    double dot = 0.0;
+      // consistency graph Laplacian (energy.py:352-370): spatial pairs couple
+      // u(x) - u(q); temporal partners are constant (energy.py:356)
+      {
+        const int e0 = __ldg(f.row_ptr + i), e1 = __ldg(f.row_ptr + i + 1);
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+        for (int e = e0; e < e1; ++e) {
+          const uint16_t ent = __ldg(f.ent + e);
+          const float we = c.lam_rc * (f.ent_w ? __ldg(f.ent_w + e) : 1.f);
+          int ddy, ddx;
+          decode_offset(ent, ddy, ddx);
+          const bool tmp = ent & kEntTemporal;
+          const int o = rc0 + (tmp ? 0 : ddy * kRW + ddx);
+          const float k0 = tmp ? 0.f : sR[o], k1 = tmp ? 0.f : sR[kRP + o], k2 = tmp ? 0.f : sR[2 * kRP + o];
+          a0 = fmaf(we, ur[0] - k0, a0);
+          a1 = fmaf(we, ur[1] - k1, a1);
+          a2 = fmaf(we, ur[2] - k2, a2);
+        }
+        outr[0] += a0; outr[1] += a1; outr[2] += a2;
+      }
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      w[ch * N + i] = outr[ch];
-      dot += (double)outr[ch] * (double)ur[ch];
+      for (int ch = 0; ch < 3; ++ch) {
+        w[(size_t)ch * N + i] = outr[ch];
+        dot = fmaf(outr[ch], ur[ch], dot);
+      }
+      acc += dot;
     }
-#pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      w[(size_t)(3 + k) * N + i] = outT[k];
-      dot += (double)outT[k] * (double)uT[k];
+    if (TMA) {
+      __syncthreads();   // every thread is done with this stage
+      if (threadIdx.x == 0) {
+        const int t = blockIdx.x + (j + 2) * gridDim.x;
+        if (t < ntiles) tma_issue_tile<NT>(sX, maps, &bars[st], (t % ntx) * kTileW, (t / ntx) * kTileH);
+      }
     }
-    acc[0] += dot;
+    accd += (double)acc;   // fp64 across tiles
+    acc = 0.f;
   }
   if (!sc) return;
-  block_reduce_store<1>(acc, part);
+  double accv[1] = {accd};
+  block_reduce_store<1>(accv, part);
   if (!last_block(ticket)) return;
   const double delta = sum_partials<1>(part, gridDim.x, 0);
   if (threadIdx.x == 0) {
-    // Chronopoulos-Gear: denominator == p.Ap of the textbook loop (solver.py:93-97)
+    // Chronopoulos-Gear: the denominator equals p.Ap of the textbook loop
+    // (solver.py:93-97); same break rule
     double beta = 0.0, denom = delta;
     if (iter > 0) {
       beta = sc->gamma / sc->gamma_prev;
@@ -549,33 +690,6 @@ __global__ void __launch_bounds__(kThreads) k_update(int64_t M, float* __restric
 // ---------------------------------------------------------------------------
 // host-side launchers (dispatch on NT)
 // ---------------------------------------------------------------------------
-template <int NT>
-static void launch_energy_nt(int mode, const Launch& L, const Frame& f, const Coef<double>& c,
-                             const float* X, const float* dx, float alpha, float* Xout, float* r_out,
-                             float* d_out, float* u_out, float* b_raw, float* diag_raw, double* part,
-                             unsigned* ticket, Scalars* sc) {
-  if (mode == MODE_EG)
-    k_energy<NT, MODE_EG><<<L.grid, kThreads, 0, L.stream>>>(f, c, X, dx, alpha, nullptr, Xout, r_out, d_out,
-                                                             u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles);
-  else
-    k_energy<NT, MODE_TRIAL><<<L.grid, kThreads, 0, L.stream>>>(f, c, X, dx, alpha, nullptr, Xout, r_out, d_out,
-                                                                u_out, b_raw, diag_raw, part, ticket, sc,
-                                                                L.ntiles);
-}
-
-template <int NT>
-static void launch_energy_ext_nt(const Launch& L, const Frame& f, const Coef<double>& c, const float* X,
-                                 const float* Y, double* part, unsigned* ticket, Scalars* sc) {
-  k_energy<NT, MODE_TRIAL><<<L.grid, kThreads, 0, L.stream>>>(f, c, X, nullptr, 0.f, Y, nullptr, nullptr, nullptr,
-                                                              nullptr, nullptr, nullptr, part, ticket, sc, L.ntiles);
-}
-
-template <int NT>
-static void launch_apply_nt(const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
-                            const float* u, float* w, double* part, unsigned* ticket, Scalars* sc, int iter) {
-  k_apply<NT><<<L.grid, kThreads, 0, L.stream>>>(f, c, X, u, w, part, ticket, sc, iter, L.ntiles);
-}
-
 #define LS_DISPATCH_NT(NTV, CALL)                       \
   switch (NTV) {                                        \
     case 1: { constexpr int NT_ = 1; CALL; } break;     \
@@ -594,21 +708,67 @@ static void launch_apply_nt(const Launch& L, const Frame& f, const Coef<float>& 
     default: break;                                     \
   }
 
-void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<double>& c, const float* X,
+template <int NT>
+static size_t energy_smem(int mode) { return sizeof(float) * tile_floats(NT, mode == MODE_TRIAL); }
+template <int NT>
+static size_t apply_smem(bool tma) { return sizeof(float) * tile_floats(NT, true) * (tma ? 2 : 1); }
+
+template <int NT>
+static void prepare_nt() {
+  cudaFuncSetAttribute(k_energy<NT, MODE_EG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)energy_smem<NT>(MODE_EG));
+  cudaFuncSetAttribute(k_energy<NT, MODE_TRIAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)energy_smem<NT>(MODE_TRIAL));
+  cudaFuncSetAttribute(k_apply<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem<NT>(true));
+  cudaFuncSetAttribute(k_apply<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem<NT>(false));
+}
+
+void prepare_kernels(int NT) { LS_DISPATCH_NT(NT, (prepare_nt<NT_>())); }
+
+template <int NT>
+static void launch_energy_nt(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
+                             const float* dx, float alpha, float* Xout, float* r_out, float* d_out, float* u_out,
+                             float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc) {
+  if (mode == MODE_EG)
+    k_energy<NT, MODE_EG><<<L.grid, kThreads, energy_smem<NT>(MODE_EG), L.stream>>>(
+        f, c, X, dx, alpha, nullptr, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles);
+  else
+    k_energy<NT, MODE_TRIAL><<<L.grid, kThreads, energy_smem<NT>(MODE_TRIAL), L.stream>>>(
+        f, c, X, dx, alpha, nullptr, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles);
+}
+
+template <int NT>
+static void launch_energy_ext_nt(const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
+                                 const float* Y, double* part, unsigned* ticket, Scalars* sc) {
+  k_energy<NT, MODE_TRIAL><<<L.grid, kThreads, energy_smem<NT>(MODE_TRIAL), L.stream>>>(
+      f, c, X, nullptr, 0.f, Y, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, part, ticket, sc, L.ntiles);
+}
+
+template <int NT>
+static void launch_apply_nt(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* u,
+                            float* w, double* part, unsigned* ticket, Scalars* sc, int iter, const TileMaps* maps) {
+  if (maps)
+    k_apply<NT, true><<<L.grid, kThreads, apply_smem<NT>(true), L.stream>>>(f, c, X, u, w, part, ticket, sc, iter,
+                                                                          L.ntiles, *maps);
+  else
+    k_apply<NT, false><<<L.grid, kThreads, apply_smem<NT>(false), L.stream>>>(f, c, X, u, w, part, ticket, sc, iter,
+                                                                            L.ntiles, TileMaps{});
+}
+
+void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
                    const float* dx, float alpha, float* Xout, float* r_out, float* d_out, float* u_out,
                    float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc) {
   LS_DISPATCH_NT(f.NT, (launch_energy_nt<NT_>(mode, L, f, c, X, dx, alpha, Xout, r_out, d_out, u_out, b_raw,
                                               diag_raw, part, ticket, sc)));
 }
 
-void launch_energy_ext(const Launch& L, const Frame& f, const Coef<double>& c, const float* X, const float* Y,
+void launch_energy_ext(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* Y,
                        double* part, unsigned* ticket, Scalars* sc) {
   LS_DISPATCH_NT(f.NT, (launch_energy_ext_nt<NT_>(L, f, c, X, Y, part, ticket, sc)));
 }
 
 void launch_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* u,
-                  float* w, double* part, unsigned* ticket, Scalars* sc, int iter) {
-  LS_DISPATCH_NT(f.NT, (launch_apply_nt<NT_>(L, f, c, X, u, w, part, ticket, sc, iter)));
+                  float* w, double* part, unsigned* ticket, Scalars* sc, int iter, const TileMaps* maps) {
+  LS_DISPATCH_NT(f.NT, (launch_apply_nt<NT_>(L, f, c, X, u, w, part, ticket, sc, iter, maps)));
 }
 
 void launch_update(const Launch& L, int64_t M, float* x, float* r, float* p, float* s, const float* w,
@@ -618,14 +778,19 @@ void launch_update(const Launch& L, int64_t M, float* x, float* r, float* p, flo
 
 int energy_grid_limit(int NT) {
   int nb = 0;
-  LS_DISPATCH_NT(NT, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_energy<NT_, MODE_EG>, kThreads, 0)));
+  LS_DISPATCH_NT(NT, (prepare_nt<NT_>(), cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                             &nb, k_energy<NT_, MODE_TRIAL>, kThreads, energy_smem<NT_>(MODE_TRIAL))));
   return nb;
 }
 int apply_grid_limit(int NT) {
   int nb = 0;
-  LS_DISPATCH_NT(NT, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_apply<NT_>, kThreads, 0)));
+  LS_DISPATCH_NT(NT, (prepare_nt<NT_>(), cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                             &nb, k_apply<NT_, true>, kThreads, apply_smem<NT_>(true))));
   return nb;
 }
+
+int tile_box_w() { return kSW; }
+int tile_box_rw() { return kRW; }
 int update_grid_limit() {
   int nb = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_update, kThreads, 0);
