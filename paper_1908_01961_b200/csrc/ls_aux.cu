@@ -186,7 +186,7 @@ __global__ void k_sample(SampleParams P, const double* __restrict__ ch, const do
       const bool keep = (dist < 0.05) && (tv[k] || q != p);
       int16_t code = -1;
       if (keep) {
-        code = (int16_t)(((py - y + kHalf) * kWin + (px - x + kHalf)) | (tv[k] ? kEntTemporal : 0));
+        code = (int16_t)make_ent(py - y, px - x, tv[k] != 0, false);
         ++cnt;
         if (!tv[k]) atomicAdd(in_cnt + q, 1);
       }
@@ -213,11 +213,11 @@ __global__ void k_fill_samples(const int16_t* __restrict__ codes, int H, int W, 
       ent[row_ptr[p] + pos] = (uint16_t)c;
       key[row_ptr[p] + pos] = (uint32_t)k;
       if (!(c & kEntTemporal)) {
-        const int code = c & 0xff;
-        const int dy = code / kWin - kHalf, dx = code % kWin - kHalf;
+        int dy, dx;
+        decode_offset((uint16_t)c, dy, dx);
         const int q = (y + dy) * W + (x + dx);
         const int pq = atomicAdd(fill + q, 1);
-        ent[row_ptr[q] + pq] = (uint16_t)(((-dy + kHalf) * kWin + (-dx + kHalf)) | kEntIncoming);
+        ent[row_ptr[q] + pq] = make_ent(-dy, -dx, false, true);
         key[row_ptr[q] + pq] = 4u + 4u * (uint32_t)p + (uint32_t)k;
       }
     }
@@ -246,12 +246,12 @@ __global__ void k_fill_pairs(int64_t n, const int64_t* src, const int64_t* dst, 
     const bool t = temporal[e] != 0;
     const float wv = weight ? (float)weight[e] : 1.f;
     int pos = atomicAdd(fill + s, 1);
-    ent[row_ptr[s] + pos] = (uint16_t)(((dy + kHalf) * kWin + (dx + kHalf)) | (t ? kEntTemporal : 0));
+    ent[row_ptr[s] + pos] = make_ent(dy, dx, t, false);
     key[row_ptr[s] + pos] = (uint32_t)e;
     if (ent_w) ent_w[row_ptr[s] + pos] = wv;
     if (!t) {
       pos = atomicAdd(fill + d, 1);
-      ent[row_ptr[d] + pos] = (uint16_t)(((-dy + kHalf) * kWin + (-dx + kHalf)) | kEntIncoming);
+      ent[row_ptr[d] + pos] = make_ent(-dy, -dx, false, true);
       key[row_ptr[d] + pos] = (uint32_t)(n + e);
       if (ent_w) ent_w[row_ptr[d] + pos] = wv;
     }
@@ -289,8 +289,8 @@ __global__ void k_pairs_from_samples(const int16_t* __restrict__ codes, int H, i
     for (int k = 0; k < 4; ++k) {
       const int16_t c = codes[4 * p + k];
       if (c < 0) continue;
-      const int code = c & 0xff;
-      const int dy = code / kWin - kHalf, dx = code % kWin - kHalf;
+      int dy, dx;
+      decode_offset((uint16_t)c, dy, dx);
       src[o] = p;
       dst[o] = (int64_t)(y + dy) * W + (x + dx);
       temporal[o] = (c & kEntTemporal) ? 1 : 0;

@@ -23,10 +23,21 @@ constexpr int kHaloW = kTileW + 2 * kHalf;
 constexpr int kHaloH = kTileH + 2 * kHalf;
 constexpr int kMaxBlocks = 4096;  // partial-sum slots per reduction
 
-// adjacency entry: bits 0-7 offset code (dy+7)*15+(dx+7); bit 8 temporal;
-// bit 9 incoming (this pixel is the pair's dst).
-constexpr uint16_t kEntTemporal = 1u << 8;
-constexpr uint16_t kEntIncoming = 1u << 9;
+// adjacency entry (uint16): bits 0-9 the partner offset pre-encoded for the
+// 48-wide shared-memory window of the operand's r planes,
+// (dy+7)*48 + (dx+7); bit 10 temporal; bit 11 incoming (pixel is the dst).
+constexpr int kEntRW = 48;
+constexpr int kEntBias = kHalf * kEntRW + kHalf;
+constexpr uint16_t kEntOffMask = 0x3ff;
+constexpr uint16_t kEntTemporal = 1u << 10;
+constexpr uint16_t kEntIncoming = 1u << 11;
+
+__host__ __device__ __forceinline__ uint16_t make_ent(int dy, int dx, bool temporal, bool incoming) {
+  return (uint16_t)(((dy + kHalf) * kEntRW + (dx + kHalf)) | (temporal ? kEntTemporal : 0) |
+                    (incoming ? kEntIncoming : 0));
+}
+// partner offset inside the 48-wide smem window
+__host__ __device__ __forceinline__ int ent_soff(uint16_t e) { return (int)(e & kEntOffMask) - kEntBias; }
 
 enum Term { T_DATA = 0, T_CLUSTER, T_RSPARSE, T_CONSIST, T_MONO, T_ISPARSE, T_SMOOTH, T_NONNEG };
 
@@ -89,10 +100,10 @@ __device__ __forceinline__ R nonneg_w(R t, R eps) {
   return t > R(0) ? R(0) : R(1) / ((t < R(0) ? -t : t) + eps);
 }
 
-__device__ __forceinline__ void decode_offset(uint16_t e, int& dy, int& dx) {
-  int code = e & 0xff;
-  dy = code / kWin - kHalf;
-  dx = code % kWin - kHalf;
+__host__ __device__ __forceinline__ void decode_offset(uint16_t e, int& dy, int& dx) {
+  const int code = e & kEntOffMask;
+  dy = code / kEntRW - kHalf;
+  dx = code % kEntRW - kHalf;
 }
 
 // ---- deterministic block reduction + last-block finalisation -------------

@@ -65,6 +65,9 @@ __device__ __forceinline__ float rsqrtf_fast(float v) {
   return r;
 }
 
+// non-negativity weight (energy.py:115-118) with the MUFU reciprocal
+__device__ __forceinline__ float nonneg_wf(float t, float eps) { return t > 0.f ? 0.f : rcpf(fabsf(t) + eps); }
+
 // smoothness / i-sparsity IRLS factor (p = 1): 1/|g| above eps, else 1/eps
 __device__ __forceinline__ float irls1f(float g, const Coef<float>& c) {
   g = fabsf(g);
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
         const float* P = sX + (3 + k) * kSP;
         const float* Q = sYT + k * kSP;
         const float wis = (k >= 1) ? c.lam_is * irls1f(T0[k], c) : 0.f;
-        const float wnn = c.lam_nn * nonneg_w<float>(T0[k], c.eps_nn);
+        const float wnn = c.lam_nn * nonneg_wf(T0[k], c.eps_nn);
         wd[k] = wis + wnn;
         eis = fmaf(wis * yT[k], yT[k], eis);
         enn = fmaf(wnn * yT[k], yT[k], enn);
@@ -433,6 +436,126 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
 // fallback (row widths not 16-byte multiples) stages the same layout with
 // cooperative loads.  Image borders are handled by zero-filled halos and
 // multiplicative 0/1 masks (branch-free stencils).
+// One pixel of w = J^T J u.  IN: interior tile (every stencil neighbour is
+// inside the image) -> no border masks.  Returns the pixel's <w, u>.
+template <int NT, bool IN>
+__device__ __forceinline__ float apply_pixel(const Frame& f, const Coef<float>& c, const float* sX, const float* sT,
+                                             const float* sR, float* __restrict__ w, int x, int y, int cx, int cy,
+                                             int rx, int ry) {
+  const int W = f.W, H = f.H, N = f.N;
+  const int i = y * W + x;
+  const bool hx = IN || x < W - 1, hy = IN || y < H - 1, hl = IN || x > 0, hu = IN || y > 0;
+  const int sc0 = cy * kSW + cx, rc0 = ry * kRW + rx;
+
+  float ur[3], R0[3], S0[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    ur[ch] = sR[ch * kRP + rc0];
+    R0[ch] = __expf(sX[ch * kSP + sc0]);
+  }
+  float uT[NT], T0[NT];
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    uT[k] = sT[k * kSP + sc0];
+    T0[k] = sX[(3 + k) * kSP + sc0];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) S0[ch] = fmaf(T0[k], c.B[k][ch], S0[ch]);
+  }
+  // data rows rho_c = R0 (S0 u_r + sum_k b_kc u_Tk) (energy.py:211-218),
+  // monochrome q_c = w_edge sum_k G_kc u_Tk (energy.py:403-408)
+  float rho[3], q[3], outr[3];
+  const float lm = c.lam_m * __ldg(f.edge + i);
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    float s = 0.f, qq = 0.f;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      s = fmaf(uT[k], c.B[k][ch], s);
+      qq = fmaf(uT[k], c.G[k][ch], qq);
+    }
+    const float r0s0 = R0[ch] * S0[ch];
+    const float rr = fmaf(r0s0, ur[ch], R0[ch] * s);
+    outr[ch] = fmaf(c.lam_d * r0s0, rr, c.lam_cl * ur[ch]);
+    q[ch] = qq * lm;
+    rho[ch] = c.lam_d * R0[ch] * rr;
+  }
+  float dot = 0.f;
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const float* P = sX + (3 + k) * kSP + sc0;
+    const float* Q = sT + k * kSP + sc0;
+    float a = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) a = fmaf(c.B[k][ch], rho[ch], fmaf(c.G[k][ch], q[ch], a));
+    const float v = T0[k], uv = uT[k];
+    const float wis = (k >= 1) ? c.lam_is * irls1f(v, c) : 0.f;
+    const float wnn = c.lam_nn * nonneg_wf(v, c.eps_nn);
+    a = fmaf(wis + wnn, uv, a);
+    // smoothness D^T W_k D u_Tk (energy.py:272-282), weights from X
+    float sm = 0.f;
+    if (hx) sm = fmaf(irls1f(P[1] - v, c), uv - Q[1], sm);
+    if (hl) sm = fmaf(irls1f(v - P[-1], c), uv - Q[-1], sm);
+    if (hy) sm = fmaf(irls1f(P[kSW] - v, c), uv - Q[kSW], sm);
+    if (hu) sm = fmaf(irls1f(v - P[-kSW], c), uv - Q[-kSW], sm);
+    a = fmaf(c.lam_sm, sm, a);
+    w[(size_t)(3 + k) * N + i] = a;
+    dot = fmaf(a, uv, dot);
+  }
+  // r-sparsity D^T W D u_r, one weight per pixel shared by the channels
+  {
+    const float wc = wrs_s(sX, cx, cy, hx, hy, c);
+    const float wl = hl ? wrs_s(sX, cx - 1, cy, true, hy, c) : 0.f;
+    const float wu = hu ? wrs_s(sX, cx, cy - 1, hx, true, c) : 0.f;
+    const float wcx = hx ? wc : 0.f, wcy = hy ? wc : 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const float* P = sR + ch * kRP + rc0;
+      const float v = ur[ch];
+      float a = wcx * (v - P[1]);
+      a = fmaf(wl, v - P[-1], a);
+      a = fmaf(wcy, v - P[kRW], a);
+      a = fmaf(wu, v - P[-kRW], a);
+      outr[ch] += a;
+    }
+  }
+  // consistency graph Laplacian (energy.py:352-370): spatial pairs couple
+  // u(x) - u(q); temporal partners are constant (energy.py:356).  Entries
+  // carry the partner's offset in this smem window.
+  {
+    const int e0 = __ldg(f.row_ptr + i), e1 = __ldg(f.row_ptr + i + 1);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+    const float* R0p = sR + rc0;
+    if (f.ent_w == nullptr) {
+      for (int e = e0; e < e1; ++e) {
+        const uint16_t ent = __ldg(f.ent + e);
+        const int o = ent_soff(ent);
+        const bool tmp = ent & kEntTemporal;
+        a0 += ur[0] - (tmp ? 0.f : R0p[o]);
+        a1 += ur[1] - (tmp ? 0.f : R0p[kRP + o]);
+        a2 += ur[2] - (tmp ? 0.f : R0p[2 * kRP + o]);
+      }
+      a0 *= c.lam_rc; a1 *= c.lam_rc; a2 *= c.lam_rc;
+    } else {
+      for (int e = e0; e < e1; ++e) {
+        const uint16_t ent = __ldg(f.ent + e);
+        const float we = c.lam_rc * __ldg(f.ent_w + e);
+        const int o = ent_soff(ent);
+        const bool tmp = ent & kEntTemporal;
+        a0 = fmaf(we, ur[0] - (tmp ? 0.f : R0p[o]), a0);
+        a1 = fmaf(we, ur[1] - (tmp ? 0.f : R0p[kRP + o]), a1);
+        a2 = fmaf(we, ur[2] - (tmp ? 0.f : R0p[2 * kRP + o]), a2);
+      }
+    }
+    outr[0] += a0; outr[1] += a1; outr[2] += a2;
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    w[(size_t)ch * N + i] = outr[ch];
+    dot = fmaf(outr[ch], ur[ch], dot);
+  }
+  return dot;
+}
+
 template <int NT, bool TMA>
 __global__ void __launch_bounds__(kThreads, 2) k_apply(Frame f, Coef<float> c, const float* __restrict__ X,
                                                        const float* __restrict__ u, float* __restrict__ w,
@@ -484,110 +607,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_apply(Frame f, Coef<float> c, c
       load_halo7(sR, u, nullptr, 0.f, N, W, H, tx0, ty0);
       __syncthreads();
     }
-    const int x = tx0 + lx, y = ty0 + ly;
-    if (x < W && y < H) {
-      const int i = y * W + x;
-      const float mx = (x < W - 1) ? 1.f : 0.f, ml = (x > 0) ? 1.f : 0.f;
-      const float my = (y < H - 1) ? 1.f : 0.f, mu = (y > 0) ? 1.f : 0.f;
-      const int sc0 = cy * kSW + cx, rc0 = ry * kRW + rx;
-
-      float ur[3], R0[3], S0[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        ur[ch] = sR[ch * kRP + rc0];
-        R0[ch] = __expf(sX[ch * kSP + sc0]);
-      }
-      float uT[NT], T0[NT];
-#pragma unroll
-      for (int k = 0; k < NT; ++k) {
-        uT[k] = sT[k * kSP + sc0];
-        T0[k] = sX[(3 + k) * kSP + sc0];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) S0[ch] = fmaf(T0[k], c.B[k][ch], S0[ch]);
-      }
-      // data rows rho_c = R0 (S0 u_r + sum_k b_kc u_Tk) (energy.py:211-218),
-      // monochrome q_c = w_edge sum_k G_kc u_Tk (energy.py:403-408)
-      float rho[3], q[3], outr[3];
-      const float lm = c.lam_m * __ldg(f.edge + i);
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        float s = 0.f, qq = 0.f;
-#pragma unroll
-        for (int k = 0; k < NT; ++k) {
-          s = fmaf(uT[k], c.B[k][ch], s);
-          qq = fmaf(uT[k], c.G[k][ch], qq);
-        }
-        rho[ch] = R0[ch] * fmaf(S0[ch], ur[ch], s);
-        outr[ch] = fmaf(c.lam_d * R0[ch] * S0[ch], rho[ch], c.lam_cl * ur[ch]);
-        q[ch] = qq * lm;
-        rho[ch] *= c.lam_d * R0[ch];
-      }
-      float dot = 0.f;
-#pragma unroll
-      for (int k = 0; k < NT; ++k) {
-        const float* P = sX + (3 + k) * kSP + sc0;
-        const float* Q = sT + k * kSP + sc0;
-        float a = 0.f;
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) a = fmaf(c.B[k][ch], rho[ch], fmaf(c.G[k][ch], q[ch], a));
-        const float v = T0[k], uv = uT[k];
-        const float wis = (k >= 1) ? c.lam_is * irls1f(v, c) : 0.f;
-        const float wnn = c.lam_nn * nonneg_w<float>(v, c.eps_nn);
-        a = fmaf(wis + wnn, uv, a);
-        // smoothness D^T W_k D u_Tk (energy.py:272-282), weights from X
-        const float axc = mx * irls1f(P[1] - v, c), axl = ml * irls1f(v - P[-1], c);
-        const float ayc = my * irls1f(P[kSW] - v, c), ayu = mu * irls1f(v - P[-kSW], c);
-        float sm = axc * (uv - Q[1]);
-        sm = fmaf(axl, uv - Q[-1], sm);
-        sm = fmaf(ayc, uv - Q[kSW], sm);
-        sm = fmaf(ayu, uv - Q[-kSW], sm);
-        a = fmaf(c.lam_sm, sm, a);
-        w[(size_t)(3 + k) * N + i] = a;
-        dot = fmaf(a, uv, dot);
-      }
-      // r-sparsity D^T W D u_r, one weight per pixel shared by the channels
-      {
-        const float wc = wrs_s(sX, cx, cy, x < W - 1, y < H - 1, c);
-        const float wl = ml * wrs_s(sX, cx - 1, cy, true, y < H - 1, c);
-        const float wu = mu * wrs_s(sX, cx, cy - 1, x < W - 1, true, c);
-        const float wcx = mx * wc, wcy = my * wc;
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const float* P = sR + ch * kRP + rc0;
-          const float v = ur[ch];
-          float a = wcx * (v - P[1]);
-          a = fmaf(wl, v - P[-1], a);
-          a = fmaf(wcy, v - P[kRW], a);
-          a = fmaf(wu, v - P[-kRW], a);
-          outr[ch] += a;
-        }
-      }
-      // consistency graph Laplacian (energy.py:352-370): spatial pairs couple
-      // u(x) - u(q); temporal partners are constant (energy.py:356)
-      {
-        const int e0 = __ldg(f.row_ptr + i), e1 = __ldg(f.row_ptr + i + 1);
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-        for (int e = e0; e < e1; ++e) {
-          const uint16_t ent = __ldg(f.ent + e);
-          const float we = c.lam_rc * (f.ent_w ? __ldg(f.ent_w + e) : 1.f);
-          int ddy, ddx;
-          decode_offset(ent, ddy, ddx);
-          const bool tmp = ent & kEntTemporal;
-          const int o = rc0 + (tmp ? 0 : ddy * kRW + ddx);
-          const float k0 = tmp ? 0.f : sR[o], k1 = tmp ? 0.f : sR[kRP + o], k2 = tmp ? 0.f : sR[2 * kRP + o];
-          a0 = fmaf(we, ur[0] - k0, a0);
-          a1 = fmaf(we, ur[1] - k1, a1);
-          a2 = fmaf(we, ur[2] - k2, a2);
-        }
-        outr[0] += a0; outr[1] += a1; outr[2] += a2;
-      }
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        w[(size_t)ch * N + i] = outr[ch];
-        dot = fmaf(outr[ch], ur[ch], dot);
-      }
-      acc += dot;
-    }
+    const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H;
+    if (interior)
+      acc += apply_pixel<NT, true>(f, c, sX, sT, sR, w, tx0 + lx, ty0 + ly, cx, cy, rx, ry);
+    else if (tx0 + lx < W && ty0 + ly < H)
+      acc += apply_pixel<NT, false>(f, c, sX, sT, sR, w, tx0 + lx, ty0 + ly, cx, cy, rx, ry);
     if (TMA) {
       __syncthreads();   // every thread is done with this stage
       if (threadIdx.x == 0) {
