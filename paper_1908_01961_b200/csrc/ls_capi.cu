@@ -624,6 +624,17 @@ static bool tile_maps(ls_ctx* c, const float* X, const float* v, TileMaps* m) {
          make_map(&m->R, v, W, H, 3, tile_box_rw(), kTileH + 2 * kHalf);
 }
 
+static bool energy_maps(ls_ctx* c, const float* X, const float* D, EnergyMaps* m) {
+  if (!c->use_tma) return false;
+  const int U = c->U, W = c->W, H = c->H;
+  bool ok = make_map(&m->X, X, W, H, U, tile_box_w(), kTileH + 2) &&
+            make_map(&m->XR, X, W, H, 3, tile_box_rw(), kTileH + 2 * kHalf);
+  if (ok && D)
+    ok = make_map(&m->D, D, W, H, U, tile_box_w(), kTileH + 2) &&
+         make_map(&m->DR, D, W, H, 3, tile_box_rw(), kTileH + 2 * kHalf);
+  return ok;
+}
+
 static Launch L_energy(ls_ctx* c) { return Launch{c->grid_energy, c->ntiles, c->stream}; }
 static Launch L_apply(ls_ctx* c) { return Launch{c->grid_apply, c->ntiles, c->stream}; }
 static Launch L_update(ls_ctx* c) { return Launch{c->grid_update, 0, c->stream}; }
@@ -635,7 +646,10 @@ int ls_energy_terms(ls_ctx* c, const double* colors, const float* X, const float
   LS_ARG(X && Y && terms, "bad arguments");
   LS_CK(cudaSetDevice(c->dev));
   const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
-  launch_energy_ext(L_energy(c), frame_of(c), cd, X, Y, c->part, c->tickets + 0, c->sc);
+  EnergyMaps em;
+  const bool tma = energy_maps(c, X, Y, &em);
+  launch_energy(1, L_energy(c), frame_of(c), cd, X, nullptr, 0.f, Y, nullptr, nullptr, nullptr, nullptr, nullptr,
+                nullptr, c->part, c->tickets + 0, c->sc, tma ? &em : nullptr);
   LS_CK(cudaGetLastError());
   LS_CK(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
   LS_CK(cudaStreamSynchronize(c->stream));
@@ -649,8 +663,10 @@ int ls_grad_diag(ls_ctx* c, const double* colors, const float* X, float* b, floa
   LS_ARG(X && b && diag, "bad arguments");
   LS_CK(cudaSetDevice(c->dev));
   const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
-  launch_energy(0, L_energy(c), frame_of(c), cd, X, nullptr, 0.f, nullptr, nullptr, nullptr, nullptr, b, diag,
-                c->part, c->tickets + 0, c->sc);
+  EnergyMaps em;
+  const bool tma = energy_maps(c, X, nullptr, &em);
+  launch_energy(0, L_energy(c), frame_of(c), cd, X, nullptr, 0.f, nullptr, nullptr, nullptr, nullptr, nullptr, b,
+                diag, c->part, c->tickets + 0, c->sc, tma ? &em : nullptr);
   LS_CK(cudaGetLastError());
   return LS_OK;
 }
@@ -674,8 +690,10 @@ static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, f
   const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
   const Coef<float> cf = make_coef<float>(c->w, colors, c->K);
   size_t pi = prof_begin(c);
-  launch_energy(0, L_energy(c), f, cd, X, nullptr, 0.f, nullptr, c->r, c->d, c->u, nullptr, nullptr, c->part,
-                c->tickets + 0, c->sc);
+  EnergyMaps em;
+  const bool etma = energy_maps(c, X, nullptr, &em);
+  launch_energy(0, L_energy(c), f, cd, X, nullptr, 0.f, nullptr, nullptr, c->r, c->d, c->u, nullptr, nullptr,
+                c->part, c->tickets + 0, c->sc, etma ? &em : nullptr);
   prof_end(c, PC_EG, pi);
   const int64_t M = (int64_t)c->U * c->N;
   TileMaps maps;
@@ -728,10 +746,12 @@ int ls_gn_step(ls_ctx* c, const double* colors, const float* X, float* X_out, ls
   double alpha = 1.0;
   double e0 = 0.0, e1 = 0.0;
   bool accepted = false;
+  EnergyMaps em;
+  const bool etma = energy_maps(c, X, c->x, &em);
   for (int h = 0; h <= c->cfg.max_halvings; ++h) {
     const size_t pi = prof_begin(c);
-    launch_energy(1, L_energy(c), f, cd, X, c->x, (float)alpha, X_out, nullptr, nullptr, nullptr, nullptr,
-                  nullptr, c->part, c->tickets + 0, c->sc);
+    launch_energy(1, L_energy(c), f, cd, X, c->x, (float)alpha, nullptr, X_out, nullptr, nullptr, nullptr, nullptr,
+                  nullptr, c->part, c->tickets + 0, c->sc, etma ? &em : nullptr);
     prof_end(c, PC_TRIAL, pi);
     c->launches += 1;
     LS_CK(cudaGetLastError());
@@ -839,7 +859,10 @@ int ls_dense_step(ls_ctx* c, double* colors, const float* X, double* applied, ls
   const Frame f = frame_of(c);
   auto energy_with = [&](const double* cols, double* out) -> int {
     const Coef<float> cd = make_coef<float>(c->w, cols, K);
-    launch_energy_ext(L_energy(c), f, cd, X, X, c->part, c->tickets + 0, c->sc);
+    EnergyMaps em;
+    const bool etma = energy_maps(c, X, nullptr, &em);
+    launch_energy(1, L_energy(c), f, cd, X, nullptr, 0.f, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                  nullptr, c->part, c->tickets + 0, c->sc, etma ? &em : nullptr);
     c->launches += 1;
     LS_CK(cudaGetLastError());
     LS_CK(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));

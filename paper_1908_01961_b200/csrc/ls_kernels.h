@@ -16,6 +16,12 @@ struct TileMaps {
   CUtensorMap X, T, R;
 };
 
+// energy kernels: state X (1 halo, U planes; r planes 7 halo) and the second
+// operand D = dx or an external Y (same two boxes)
+struct EnergyMaps {
+  CUtensorMap X, XR, D, DR;
+};
+
 struct Launch {
   int grid;
   int ntiles;
@@ -24,10 +30,9 @@ struct Launch {
 
 // ls_solver.cu
 void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
-                   const float* dx, float alpha, float* Xout, float* r_out, float* d_out, float* u_out,
-                   float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc);
-void launch_energy_ext(const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
-                       const float* Y, double* part, unsigned* ticket, Scalars* sc);
+                   const float* dx, float alpha, const float* Y, float* Xout, float* r_out, float* d_out,
+                   float* u_out, float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc,
+                   const EnergyMaps* maps);
 void launch_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* u,
                   float* w, double* part, unsigned* ticket, Scalars* sc, int iter, const TileMaps* maps);
 int tile_box_w();

@@ -85,14 +85,15 @@ __device__ __forceinline__ float irls_sq(float s, const Coef<float>& c) {
 
 // r-sparsity weight at smem coords (ix, iy) of the 1-halo state tile; hx / hy
 // say whether the pixel has a right / lower neighbour in the image
-__device__ __forceinline__ float wrs_s(const float* sX, int ix, int iy, bool hx, bool hy, const Coef<float>& c) {
+__device__ __forceinline__ float wrs_s(const float* sX, int ix, int iy, bool hx, bool hy, const Coef<float>& c,
+                                       int RW = kSW, int RP = kSP) {
   float sx = 0.f, syy = 0.f;
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
-    const float* P = sX + ch * kSP;
-    const float v = P[iy * kSW + ix];
-    const float gx = hx ? P[iy * kSW + ix + 1] - v : 0.f;
-    const float gy = hy ? P[(iy + 1) * kSW + ix] - v : 0.f;
+    const float* P = sX + ch * RP;
+    const float v = P[iy * RW + ix];
+    const float gx = hx ? P[iy * RW + ix + 1] - v : 0.f;
+    const float gy = hy ? P[(iy + 1) * RW + ix] - v : 0.f;
     sx = fmaf(gx, gx, sx);
     syy = fmaf(gy, gy, syy);
   }
@@ -159,246 +160,327 @@ __device__ __forceinline__ void tma_issue_tile(float* stage, const TileMaps& m, 
 // ---------------------------------------------------------------------------
 // energy (+ gradient / diagonal / PCG init) kernel
 // ---------------------------------------------------------------------------
-template <int NT, int MODE>
+// Shared-memory stage (TMA boxes, zero-filled outside the image):
+//   sX  U state planes, 1 halo       sXR the 3 state r planes, 7 halo
+//   sD  U planes of dx / Y, 1 halo   sDR their r planes, 7 halo   (trial only)
+// In trial mode the evaluation point Y = X + alpha*dx is formed in place in
+// sD / sDR right after the tile lands (the owner writes exactly these values
+// to X_out, so the accepted state is the state that was evaluated).
+__host__ __device__ constexpr int e_off_XR(int NT) { return pad32((NT + 3) * kSP); }
+__host__ __device__ constexpr int e_off_D(int NT) { return e_off_XR(NT) + pad32(3 * kRP); }
+__host__ __device__ constexpr int e_off_DR(int NT) { return e_off_D(NT) + pad32((NT + 3) * kSP); }
+__host__ __device__ constexpr int e_stage(int NT, bool trial) {
+  return trial ? e_off_DR(NT) + pad32(3 * kRP) : e_off_D(NT);
+}
+
+template <int NT>
+__device__ __forceinline__ void tma_issue_energy(float* stage, const EnergyMaps& m, uint64_t* bar, int tx0, int ty0,
+                                                 bool with_d) {
+  constexpr uint32_t half = sizeof(float) * ((NT + 3) * kSP + 3 * kRP);
+  mbar_expect_tx(bar, with_d ? 2 * half : half);
+  tma_load_3d(stage, &m.X, bar, tx0 - kSX, ty0 - 1, 0);
+  tma_load_3d(stage + e_off_XR(NT), &m.XR, bar, tx0 - kRX, ty0 - kHalf, 0);
+  if (with_d) {
+    tma_load_3d(stage + e_off_D(NT), &m.D, bar, tx0 - kSX, ty0 - 1, 0);
+    tma_load_3d(stage + e_off_DR(NT), &m.DR, bar, tx0 - kRX, ty0 - kHalf, 0);
+  }
+}
+
+// per-pixel energy terms (+ gradient / diagonal / PCG init in MODE_EG);
+// acc[] receives the 8 term energies (fp32 per pixel) and rz, |b|^2
+template <int NT, int MODE, bool IN>
+__device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& c, const float* sX, const float* sXR,
+                                             const float* sYT, const float* sYR, int x, int y, int cx, int cy,
+                                             int rx, int ry, float* __restrict__ Xout, float* __restrict__ r_out,
+                                             float* __restrict__ d_out, float* __restrict__ u_out,
+                                             float* __restrict__ b_raw, float* __restrict__ diag_raw,
+                                             double* acc) {
+  const int W = f.W, H = f.H, N = f.N;
+  const int i = y * W + x;
+  const bool hx = IN || x < W - 1, hy = IN || y < H - 1, hl = IN || x > 0, hu = IN || y > 0;
+  const int sc0 = cy * kSW + cx, rc0 = ry * kRW + rx;
+  float r0[3], T0[NT], yr[3], yT[NT];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    r0[ch] = sXR[ch * kRP + rc0];
+    yr[ch] = sYR[ch * kRP + rc0];
+  }
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    T0[k] = sX[(3 + k) * kSP + sc0];
+    yT[k] = sYT[k * kSP + sc0];
+  }
+  float img[3], anc[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) img[ch] = __ldg(f.img + ch * N + i);
+  if (f.ids) {
+    const int id = __ldg(f.ids + i);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) anc[ch] = c.anchor[id][ch];
+  } else {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) anc[ch] = __ldg(f.anchor + ch * N + i);
+  }
+  const float lm = c.lam_m * __ldg(f.edge + i);
+
+  // data (energy.py:207-209), clustering (234-235), monochrome (399-401)
+  float S[3], R[3], res[3], m[3];
+  double e_data = 0.0;
+  float e_cl = 0.f, e_mono = 0.f;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) s = fmaf(yT[k], c.B[k][ch], s);
+    S[ch] = s;
+    R[ch] = expf(yr[ch]);
+    const double rd = fma(-(double)R[ch], (double)S[ch], (double)img[ch]);   // exactly rounded residual
+    e_data = fma(rd, rd, e_data);
+    res[ch] = (float)rd;
+    const float dc = yr[ch] - anc[ch];
+    e_cl = fmaf(dc, dc, e_cl);
+  }
+  const float mean = (S[0] + S[1] + S[2]) * (1.f / 3.f);
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    m[ch] = S[ch] - mean;
+    e_mono = fmaf(m[ch], m[ch], e_mono);
+  }
+  acc[T_DATA] += (double)c.lam_d * e_data;
+  acc[T_CLUSTER] += (double)(c.lam_cl * e_cl);
+  acc[T_MONO] += (double)(lm * e_mono);
+
+  // r-sparsity: weight from X, gradient of Y (energy.py:264-267, 301-305)
+  const float wrs = wrs_s(sXR, rx, ry, hx, hy, c, kRW, kRP);
+  {
+    float e = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const float* P = sYR + ch * kRP + rc0;
+      const float gx = hx ? P[1] - yr[ch] : 0.f;
+      const float gy = hy ? P[kRW] - yr[ch] : 0.f;
+      e = fmaf(gx, gx, fmaf(gy, gy, e));
+    }
+    acc[T_RSPARSE] += (double)(wrs * e);
+  }
+
+  // per-layer diagonal terms and smoothness (energy.py:414-452, 308-318)
+  float wd[NT];
+  {
+    float eis = 0.f, enn = 0.f, esm = 0.f;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const float* P = sX + (3 + k) * kSP + sc0;
+      const float* Q = sYT + k * kSP + sc0;
+      const float wis = (k >= 1) ? c.lam_is * irls1f(T0[k], c) : 0.f;
+      const float wnn = c.lam_nn * nonneg_wf(T0[k], c.eps_nn);
+      wd[k] = wis + wnn;
+      eis = fmaf(wis * yT[k], yT[k], eis);
+      enn = fmaf(wnn * yT[k], yT[k], enn);
+      if (hx) {
+        const float g = Q[1] - yT[k];
+        esm = fmaf(irls1f(P[1] - T0[k], c) * g, g, esm);
+      }
+      if (hy) {
+        const float g = Q[kSW] - yT[k];
+        esm = fmaf(irls1f(P[kSW] - T0[k], c) * g, g, esm);
+      }
+    }
+    acc[T_ISPARSE] += (double)eis;
+    acc[T_NONNEG] += (double)enn;
+    acc[T_SMOOTH] += (double)(c.lam_sm * esm);
+  }
+
+  // consistency pairs (energy.py:348-350): energy counted at each pair's
+  // src; gradient / diagonal from every incident pair (energy.py:359-381)
+  float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, dcons = 0.f;
+  {
+    const int e0 = __ldg(f.row_ptr + i), e1 = __ldg(f.row_ptr + i + 1);
+    float ec = 0.f;
+    const float* YR = sYR + rc0;
+    for (int e = e0; e < e1; ++e) {
+      const uint16_t ent = __ldg(f.ent + e);
+      const float we = c.lam_rc * (f.ent_w ? __ldg(f.ent_w + e) : 1.f);
+      float p0, p1, p2;
+      if (ent & kEntTemporal) {
+        int ddy, ddx;
+        decode_offset(ent, ddy, ddx);
+        const int q = i + ddy * W + ddx;
+        p0 = __ldg(f.prev_r + q);
+        p1 = __ldg(f.prev_r + N + q);
+        p2 = __ldg(f.prev_r + 2 * N + q);
+      } else {
+        const int o = ent_soff(ent);
+        p0 = YR[o];
+        p1 = YR[kRP + o];
+        p2 = YR[2 * kRP + o];
+      }
+      const float d0 = yr[0] - p0, d1 = yr[1] - p1, d2 = yr[2] - p2;
+      if (!(ent & kEntIncoming)) ec = fmaf(we, fmaf(d0, d0, fmaf(d1, d1, d2 * d2)), ec);
+      gc0 = fmaf(we, d0, gc0);
+      gc1 = fmaf(we, d1, gc1);
+      gc2 = fmaf(we, d2, gc2);
+      dcons += we;
+    }
+    acc[T_CONSIST] += (double)ec;
+  }
+
+  if (MODE == MODE_TRIAL) {
+    if (Xout) {
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) Xout[ch * N + i] = yr[ch];
+#pragma unroll
+      for (int k = 0; k < NT; ++k) Xout[(size_t)(3 + k) * N + i] = yT[k];
+    }
+    return;
+  }
+
+  // ======== MODE_EG: g = J^T F, diag(J^T J), PCG init (Y == X) ========
+  const float wl = hl ? wrs_s(sXR, rx - 1, ry, true, hy, c, kRW, kRP) : 0.f;
+  const float wu = hu ? wrs_s(sXR, rx, ry - 1, hx, true, c, kRW, kRP) : 0.f;
+  const float gcons[3] = {gc0, gc1, gc2};
+  float rz = 0.f, bb = 0.f;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    const float* P = sXR + ch * kRP + rc0;
+    const float rs = R[ch] * S[ch];
+    float g = fmaf(-c.lam_d * rs, res[ch], c.lam_cl * (r0[ch] - anc[ch]));
+    float d = fmaf(c.lam_d * rs, rs, c.lam_cl);
+    const float v = r0[ch];
+    if (hx) { g = fmaf(wrs, v - P[1], g); d += wrs; }
+    if (hl) { g = fmaf(wl, v - P[-1], g); d += wl; }
+    if (hy) { g = fmaf(wrs, v - P[kRW], g); d += wrs; }
+    if (hu) { g = fmaf(wu, v - P[-kRW], g); d += wu; }
+    g += gcons[ch];
+    d += dcons;
+    const float bf = -g;
+    const float dd = d > 0.f ? d : 1.f;
+    const float uf = bf / dd;
+    if (r_out) { r_out[ch * N + i] = bf; d_out[ch * N + i] = dd; u_out[ch * N + i] = uf; }
+    if (b_raw) { b_raw[ch * N + i] = bf; diag_raw[ch * N + i] = d; }
+    rz = fmaf(bf, uf, rz);
+    bb = fmaf(bf, bf, bb);
+  }
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const float* P = sX + (3 + k) * kSP + sc0;
+    float g = 0.f, d = 0.f, gm = 0.f, g2 = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const float rb = R[ch] * c.B[k][ch];
+      g = fmaf(rb, res[ch], g);
+      d = fmaf(rb, rb, d);
+      gm = fmaf(c.G[k][ch], m[ch], gm);
+      g2 = fmaf(c.G[k][ch], c.G[k][ch], g2);
+    }
+    g = fmaf(-c.lam_d, g, fmaf(lm, gm, wd[k] * T0[k]));
+    d = fmaf(c.lam_d, d, fmaf(lm, g2, wd[k]));
+    const float v = T0[k];
+    float gs = 0.f, ds = 0.f;
+    if (hx) { const float a = irls1f(P[1] - v, c); gs = fmaf(a, v - P[1], gs); ds += a; }
+    if (hl) { const float a = irls1f(v - P[-1], c); gs = fmaf(a, v - P[-1], gs); ds += a; }
+    if (hy) { const float a = irls1f(P[kSW] - v, c); gs = fmaf(a, v - P[kSW], gs); ds += a; }
+    if (hu) { const float a = irls1f(v - P[-kSW], c); gs = fmaf(a, v - P[-kSW], gs); ds += a; }
+    g = fmaf(c.lam_sm, gs, g);
+    d = fmaf(c.lam_sm, ds, d);
+    const float bf = -g;
+    const float dd = d > 0.f ? d : 1.f;
+    const float uf = bf / dd;
+    const size_t o = (size_t)(3 + k) * N + i;
+    if (r_out) { r_out[o] = bf; d_out[o] = dd; u_out[o] = uf; }
+    if (b_raw) { b_raw[o] = bf; diag_raw[o] = d; }
+    rz = fmaf(bf, uf, rz);
+    bb = fmaf(bf, bf, bb);
+  }
+  acc[kTerms] += (double)rz;
+  acc[kTerms + 1] += (double)bb;
+}
+
+template <int NT, int MODE, bool TMA>
 __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, const float* __restrict__ X,
                                                      const float* __restrict__ dx, float alpha,
                                                      const float* __restrict__ Yext, float* __restrict__ Xout,
                                                      float* __restrict__ r_out, float* __restrict__ d_out,
                                                      float* __restrict__ u_out, float* __restrict__ b_raw,
                                                      float* __restrict__ diag_raw, double* part,
-                                                     unsigned* ticket, Scalars* sc, int ntiles) {
+                                                     unsigned* ticket, Scalars* sc, int ntiles,
+                                                     const __grid_constant__ EnergyMaps maps) {
   constexpr int U = NT + 3;
-  constexpr int NV = (MODE == MODE_EG) ? kTerms + 2 : kTerms;
-  extern __shared__ float smem[];
-  float* sX = smem;                                        // U 1-halo planes (frozen state)
-  float* sT = smem + off_T(NT);                            // NT 1-halo planes (eval point), trial only
-  float* sR = smem + off_R(NT, MODE == MODE_TRIAL);        // 3 7-halo planes (eval point r)
+  constexpr bool TRIAL = MODE == MODE_TRIAL;
+  constexpr int NST = (TMA && !TRIAL) ? 2 : 1;
+  constexpr int STAGE = e_stage(NT, TRIAL);
+  constexpr int NV = TRIAL ? kTerms : kTerms + 2;
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t bars[2];
   const int W = f.W, H = f.H, N = f.N;
   const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
   const int cx = lx + kSX, cy = ly + 1, rx = lx + kRX, ry = ly + kHalf;
+  const int ntx = (W + kTileW - 1) / kTileW;
+  // the evaluation point: X itself, X + alpha*dx, or an external Y
+  const bool ext = TRIAL && Yext != nullptr;
+  const bool step = TRIAL && !ext && dx != nullptr && sc->iterations > 0;
+  const bool with_d = ext || step;
   double acc[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) acc[j] = 0.0;
-  // trial: an empty PCG step means a zero update (solver.py:85-86)
-  const float* dxe = (MODE == MODE_TRIAL && dx != nullptr && sc->iterations > 0) ? dx : nullptr;
-  const float* Ysrc = (MODE == MODE_TRIAL && Yext) ? Yext : X;
-  if (MODE == MODE_TRIAL && Yext) dxe = nullptr;
-  const float* sYT = (MODE == MODE_TRIAL) ? sT : sX + 3 * kSP;   // eval-point T planes
-
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    int tx0, ty0;
-    tile_coords(tile, W, tx0, ty0);
-    __syncthreads();
-    load_halo1<U>(sX, X, N, W, H, tx0, ty0);
-    if (MODE == MODE_TRIAL) load_halo1_axpy<NT>(sT, Ysrc + 3 * (size_t)N, dxe ? dxe + 3 * (size_t)N : nullptr, alpha,
-                                                N, W, H, tx0, ty0);
-    load_halo7(sR, Ysrc, dxe, alpha, N, W, H, tx0, ty0);
-    __syncthreads();
-    const int x = tx0 + lx, y = ty0 + ly;
-    if (x >= W || y >= H) continue;
-    const int i = y * W + x;
-    const bool hx = x < W - 1, hy = y < H - 1, hl = x > 0, hu = y > 0;
-
-    float r0[3], T0[NT], yr[3], yT[NT];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      r0[ch] = sX[ch * kSP + cy * kSW + cx];
-      yr[ch] = sR[ch * kRP + ry * kRW + rx];
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      fence_barrier_init();
+      for (int j = 0; j < NST; ++j) {
+        const int t = blockIdx.x + j * gridDim.x;
+        if (t < ntiles) tma_issue_energy<NT>(smem + j * STAGE, maps, &bars[j], (t % ntx) * kTileW,
+                                             (t / ntx) * kTileH, with_d);
+      }
     }
-#pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      T0[k] = sX[(3 + k) * kSP + cy * kSW + cx];
-      yT[k] = sYT[k * kSP + cy * kSW + cx];
-    }
-    float img[3], anc[3];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) img[ch] = __ldg(f.img + ch * N + i);
-    if (f.ids) {
-      const int id = __ldg(f.ids + i);
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) anc[ch] = c.anchor[id][ch];
+    __syncthreads();
+  }
+  uint32_t phase = 0;
+  for (int j = 0;; ++j) {
+    const int tile = blockIdx.x + j * gridDim.x;
+    if (tile >= ntiles) break;
+    const int tx0 = (tile % ntx) * kTileW, ty0 = (tile / ntx) * kTileH;
+    const int st = (NST == 2) ? (j & 1) : 0;
+    float* sX = smem + st * STAGE;
+    float* sXR = sX + e_off_XR(NT);
+    float* sD = sX + e_off_D(NT);
+    float* sDR = sX + e_off_DR(NT);
+    if (TMA) {
+      mbar_wait(&bars[st], (phase >> st) & 1u);
+      phase ^= 1u << st;
     } else {
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) anc[ch] = __ldg(f.anchor + ch * N + i);
-    }
-    const float lm = c.lam_m * __ldg(f.edge + i);
-
-    // data (energy.py:207-209), clustering (234-235), monochrome (399-401)
-    float S[3], R[3], res[3], m[3];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < NT; ++k) s = fmaf(yT[k], c.B[k][ch], s);
-      S[ch] = s;
-      R[ch] = expf(yr[ch]);
-      res[ch] = (float)fma(-(double)R[ch], (double)S[ch], (double)img[ch]);   // exactly rounded
-      acc[T_DATA] += (double)c.lam_d * ((double)res[ch] * (double)res[ch]);
-      const float dc = yr[ch] - anc[ch];
-      acc[T_CLUSTER] += (double)(c.lam_cl * dc * dc);
-    }
-    const float mean = (S[0] + S[1] + S[2]) * (1.f / 3.f);
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      m[ch] = S[ch] - mean;
-      acc[T_MONO] += (double)(lm * m[ch] * m[ch]);
-    }
-
-    // r-sparsity: weight from X, gradient of Y (energy.py:264-267, 301-305)
-    const float wrs = wrs_s(sX, cx, cy, hx, hy, c);
-    {
-      float e = 0.f;
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        const float* P = sR + ch * kRP;
-        const float gx = hx ? P[ry * kRW + rx + 1] - yr[ch] : 0.f;
-        const float gy = hy ? P[(ry + 1) * kRW + rx] - yr[ch] : 0.f;
-        e = fmaf(gx, gx, fmaf(gy, gy, e));
+      __syncthreads();
+      load_halo1<U>(sX, X, N, W, H, tx0, ty0);
+      load_halo7(sXR, X, nullptr, 0.f, N, W, H, tx0, ty0);
+      if (with_d) {
+        load_halo1<U>(sD, ext ? Yext : dx, N, W, H, tx0, ty0);
+        load_halo7(sDR, ext ? Yext : dx, nullptr, 0.f, N, W, H, tx0, ty0);
       }
-      acc[T_RSPARSE] += (double)(wrs * e);
+      __syncthreads();
     }
-
-    // per-layer diagonal terms and smoothness (energy.py:414-452, 308-318)
-    float wd[NT];
-    {
-      float eis = 0.f, enn = 0.f, esm = 0.f;
-#pragma unroll
-      for (int k = 0; k < NT; ++k) {
-        const float* P = sX + (3 + k) * kSP;
-        const float* Q = sYT + k * kSP;
-        const float wis = (k >= 1) ? c.lam_is * irls1f(T0[k], c) : 0.f;
-        const float wnn = c.lam_nn * nonneg_wf(T0[k], c.eps_nn);
-        wd[k] = wis + wnn;
-        eis = fmaf(wis * yT[k], yT[k], eis);
-        enn = fmaf(wnn * yT[k], yT[k], enn);
-        if (hx) {
-          const float ax = c.lam_sm * irls1f(P[cy * kSW + cx + 1] - T0[k], c);
-          const float g = Q[cy * kSW + cx + 1] - yT[k];
-          esm = fmaf(ax * g, g, esm);
-        }
-        if (hy) {
-          const float ay = c.lam_sm * irls1f(P[(cy + 1) * kSW + cx] - T0[k], c);
-          const float g = Q[(cy + 1) * kSW + cx] - yT[k];
-          esm = fmaf(ay * g, g, esm);
-        }
-      }
-      acc[T_ISPARSE] += (double)eis;
-      acc[T_NONNEG] += (double)enn;
-      acc[T_SMOOTH] += (double)esm;
+    if (step) {   // Y = fma(alpha, dx, X) in place (T planes 1 halo, r planes 7 halo)
+      __syncthreads();
+      for (int e = threadIdx.x; e < NT * kSP; e += kThreads)
+        sD[3 * kSP + e] = __fmaf_rn(alpha, sD[3 * kSP + e], sX[3 * kSP + e]);
+      for (int e = threadIdx.x; e < 3 * kRP; e += kThreads) sDR[e] = __fmaf_rn(alpha, sDR[e], sXR[e]);
+      __syncthreads();
     }
-
-    // consistency pairs (energy.py:348-350): energy counted at each pair's
-    // src; gradient / diagonal from every incident pair (energy.py:359-381)
-    float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, dcons = 0.f;
-    {
-      const int e0 = __ldg(f.row_ptr + i), e1 = __ldg(f.row_ptr + i + 1);
-      float ec = 0.f;
-      for (int e = e0; e < e1; ++e) {
-        const uint16_t ent = __ldg(f.ent + e);
-        const float we = c.lam_rc * (f.ent_w ? __ldg(f.ent_w + e) : 1.f);
-        int ddy, ddx;
-        decode_offset(ent, ddy, ddx);
-        float p0, p1, p2;
-        if (ent & kEntTemporal) {
-          const int q = i + ddy * W + ddx;
-          p0 = __ldg(f.prev_r + q);
-          p1 = __ldg(f.prev_r + N + q);
-          p2 = __ldg(f.prev_r + 2 * N + q);
-        } else {
-          const int o = (ry + ddy) * kRW + rx + ddx;
-          p0 = sR[o];
-          p1 = sR[kRP + o];
-          p2 = sR[2 * kRP + o];
-        }
-        const float d0 = yr[0] - p0, d1 = yr[1] - p1, d2 = yr[2] - p2;
-        if (!(ent & kEntIncoming)) ec = fmaf(we, d0 * d0 + d1 * d1 + d2 * d2, ec);
-        gc0 = fmaf(we, d0, gc0);
-        gc1 = fmaf(we, d1, gc1);
-        gc2 = fmaf(we, d2, gc2);
-        dcons += we;
+    const float* sYT = with_d ? sD + 3 * kSP : sX + 3 * kSP;
+    const float* sYR = with_d ? sDR : sXR;
+    const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H;
+    if (interior)
+      energy_pixel<NT, MODE, true>(f, c, sX, sXR, sYT, sYR, tx0 + lx, ty0 + ly, cx, cy, rx, ry, Xout, r_out, d_out,
+                                   u_out, b_raw, diag_raw, acc);
+    else if (tx0 + lx < W && ty0 + ly < H)
+      energy_pixel<NT, MODE, false>(f, c, sX, sXR, sYT, sYR, tx0 + lx, ty0 + ly, cx, cy, rx, ry, Xout, r_out, d_out,
+                                    u_out, b_raw, diag_raw, acc);
+    if (TMA) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int t = blockIdx.x + (j + NST) * gridDim.x;
+        if (t < ntiles) tma_issue_energy<NT>(sX, maps, &bars[st], (t % ntx) * kTileW, (t / ntx) * kTileH, with_d);
       }
-      acc[T_CONSIST] += (double)ec;
-    }
-
-    if (MODE == MODE_TRIAL) {
-      if (Xout) {
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) Xout[ch * N + i] = yr[ch];
-#pragma unroll
-        for (int k = 0; k < NT; ++k) Xout[(size_t)(3 + k) * N + i] = yT[k];
-      }
-      continue;
-    }
-
-    // ======== MODE_EG: g = J^T F, diag(J^T J), PCG init (Y == X) ========
-    const float wl = hl ? wrs_s(sX, cx - 1, cy, true, hy, c) : 0.f;
-    const float wu = hu ? wrs_s(sX, cx, cy - 1, hx, true, c) : 0.f;
-    const float gcons[3] = {gc0, gc1, gc2};
-    double rz = 0.0, bb = 0.0;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      const float* P = sX + ch * kSP;
-      const float rs = R[ch] * S[ch];
-      float g = fmaf(-c.lam_d * rs, res[ch], c.lam_cl * (r0[ch] - anc[ch]));
-      float d = fmaf(c.lam_d * rs, rs, c.lam_cl);
-      const float v = r0[ch];
-      if (hx) { g = fmaf(wrs, v - P[cy * kSW + cx + 1], g); d += wrs; }
-      if (hl) { g = fmaf(wl, v - P[cy * kSW + cx - 1], g); d += wl; }
-      if (hy) { g = fmaf(wrs, v - P[(cy + 1) * kSW + cx], g); d += wrs; }
-      if (hu) { g = fmaf(wu, v - P[(cy - 1) * kSW + cx], g); d += wu; }
-      g += gcons[ch];
-      d += dcons;
-      const float bf = -g;
-      const float dd = d > 0.f ? d : 1.f;
-      const float uf = bf / dd;
-      if (r_out) { r_out[ch * N + i] = bf; d_out[ch * N + i] = dd; u_out[ch * N + i] = uf; }
-      if (b_raw) { b_raw[ch * N + i] = bf; diag_raw[ch * N + i] = d; }
-      rz += (double)bf * (double)uf;
-      bb += (double)bf * (double)bf;
-    }
-#pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      const float* P = sX + (3 + k) * kSP;
-      float g = 0.f, d = 0.f, gm = 0.f, g2 = 0.f;
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        const float rb = R[ch] * c.B[k][ch];
-        g = fmaf(rb, res[ch], g);
-        d = fmaf(rb, rb, d);
-        gm = fmaf(c.G[k][ch], m[ch], gm);
-        g2 = fmaf(c.G[k][ch], c.G[k][ch], g2);
-      }
-      g = fmaf(-c.lam_d, g, fmaf(lm, gm, wd[k] * T0[k]));
-      d = fmaf(c.lam_d, d, fmaf(lm, g2, wd[k]));
-      const float v = T0[k];
-      if (hx) {
-        const float a = c.lam_sm * irls1f(P[cy * kSW + cx + 1] - v, c);
-        g = fmaf(a, v - P[cy * kSW + cx + 1], g); d += a;
-      }
-      if (hl) {
-        const float a = c.lam_sm * irls1f(v - P[cy * kSW + cx - 1], c);
-        g = fmaf(a, v - P[cy * kSW + cx - 1], g); d += a;
-      }
-      if (hy) {
-        const float a = c.lam_sm * irls1f(P[(cy + 1) * kSW + cx] - v, c);
-        g = fmaf(a, v - P[(cy + 1) * kSW + cx], g); d += a;
-      }
-      if (hu) {
-        const float a = c.lam_sm * irls1f(v - P[(cy - 1) * kSW + cx], c);
-        g = fmaf(a, v - P[(cy - 1) * kSW + cx], g); d += a;
-      }
-      const float bf = -g;
-      const float dd = d > 0.f ? d : 1.f;
-      const float uf = bf / dd;
-      const size_t o = (size_t)(3 + k) * N + i;
-      if (r_out) { r_out[o] = bf; d_out[o] = dd; u_out[o] = uf; }
-      if (b_raw) { b_raw[o] = bf; diag_raw[o] = d; }
-      rz += (double)bf * (double)uf;
-      bb += (double)bf * (double)bf;
-    }
-    if (MODE == MODE_EG) {
-      acc[kTerms] += rz;
-      acc[kTerms + 1] += bb;
     }
   }
 
@@ -410,7 +492,7 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
   if (threadIdx.x == 0) {
     bool finite = true;
     for (int j = 0; j < kTerms; ++j) finite = finite && isfinite(tot[j]);
-    if (MODE == MODE_EG) {
+    if (!TRIAL) {
       for (int j = 0; j < kTerms; ++j) sc->terms0[j] = tot[j];
       sc->gamma = tot[kTerms];
       sc->gamma_prev = 0.0;
@@ -427,15 +509,6 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
   }
 }
 
-// ---------------------------------------------------------------------------
-// matrix-free normal operator w = J^T J u (fp32), frozen at X
-// ---------------------------------------------------------------------------
-// TMA path: a 2-stage pipeline per persistent CTA -- thread 0 issues the
-// three boxes of tile j+2 into the stage tile j just released, all threads
-// wait on that stage's mbarrier; no load instructions in the SM.  The
-// fallback (row widths not 16-byte multiples) stages the same layout with
-// cooperative loads.  Image borders are handled by zero-filled halos and
-// multiplicative 0/1 masks (branch-free stencils).
 // One pixel of w = J^T J u.  IN: interior tile (every stencil neighbour is
 // inside the image) -> no border masks.  Returns the pixel's <w, u>.
 template <int NT, bool IN>
@@ -733,38 +806,53 @@ __global__ void __launch_bounds__(kThreads) k_update(int64_t M, float* __restric
   }
 
 template <int NT>
-static size_t energy_smem(int mode) { return sizeof(float) * tile_floats(NT, mode == MODE_TRIAL); }
+static size_t energy_smem(int mode, bool tma) {
+  const bool trial = mode == MODE_TRIAL;
+  return sizeof(float) * e_stage(NT, trial) * ((tma && !trial) ? 2 : 1);
+}
 template <int NT>
 static size_t apply_smem(bool tma) { return sizeof(float) * tile_floats(NT, true) * (tma ? 2 : 1); }
 
 template <int NT>
 static void prepare_nt() {
-  cudaFuncSetAttribute(k_energy<NT, MODE_EG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)energy_smem<NT>(MODE_EG));
-  cudaFuncSetAttribute(k_energy<NT, MODE_TRIAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)energy_smem<NT>(MODE_TRIAL));
+  cudaFuncSetAttribute(k_energy<NT, MODE_EG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)energy_smem<NT>(MODE_EG, true));
+  cudaFuncSetAttribute(k_energy<NT, MODE_EG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)energy_smem<NT>(MODE_EG, false));
+  cudaFuncSetAttribute(k_energy<NT, MODE_TRIAL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)energy_smem<NT>(MODE_TRIAL, true));
+  cudaFuncSetAttribute(k_energy<NT, MODE_TRIAL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)energy_smem<NT>(MODE_TRIAL, false));
   cudaFuncSetAttribute(k_apply<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem<NT>(true));
   cudaFuncSetAttribute(k_apply<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem<NT>(false));
 }
 
 void prepare_kernels(int NT) { LS_DISPATCH_NT(NT, (prepare_nt<NT_>())); }
 
-template <int NT>
-static void launch_energy_nt(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
-                             const float* dx, float alpha, float* Xout, float* r_out, float* d_out, float* u_out,
-                             float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc) {
-  if (mode == MODE_EG)
-    k_energy<NT, MODE_EG><<<L.grid, kThreads, energy_smem<NT>(MODE_EG), L.stream>>>(
-        f, c, X, dx, alpha, nullptr, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles);
+template <int NT, int MODE>
+static void launch_energy_mt(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* dx,
+                             float alpha, const float* Y, float* Xout, float* r_out, float* d_out, float* u_out,
+                             float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc,
+                             const EnergyMaps* maps) {
+  if (maps)
+    k_energy<NT, MODE, true><<<L.grid, kThreads, energy_smem<NT>(MODE, true), L.stream>>>(
+        f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, *maps);
   else
-    k_energy<NT, MODE_TRIAL><<<L.grid, kThreads, energy_smem<NT>(MODE_TRIAL), L.stream>>>(
-        f, c, X, dx, alpha, nullptr, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles);
+    k_energy<NT, MODE, false><<<L.grid, kThreads, energy_smem<NT>(MODE, false), L.stream>>>(
+        f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, EnergyMaps{});
 }
 
 template <int NT>
-static void launch_energy_ext_nt(const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
-                                 const float* Y, double* part, unsigned* ticket, Scalars* sc) {
-  k_energy<NT, MODE_TRIAL><<<L.grid, kThreads, energy_smem<NT>(MODE_TRIAL), L.stream>>>(
-      f, c, X, nullptr, 0.f, Y, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, part, ticket, sc, L.ntiles);
+static void launch_energy_nt(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
+                             const float* dx, float alpha, const float* Y, float* Xout, float* r_out, float* d_out,
+                             float* u_out, float* b_raw, float* diag_raw, double* part, unsigned* ticket,
+                             Scalars* sc, const EnergyMaps* maps) {
+  if (mode == MODE_EG)
+    launch_energy_mt<NT, MODE_EG>(L, f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket,
+                                  sc, maps);
+  else
+    launch_energy_mt<NT, MODE_TRIAL>(L, f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part,
+                                     ticket, sc, maps);
 }
 
 template <int NT>
@@ -779,15 +867,11 @@ static void launch_apply_nt(const Launch& L, const Frame& f, const Coef<float>& 
 }
 
 void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
-                   const float* dx, float alpha, float* Xout, float* r_out, float* d_out, float* u_out,
-                   float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc) {
-  LS_DISPATCH_NT(f.NT, (launch_energy_nt<NT_>(mode, L, f, c, X, dx, alpha, Xout, r_out, d_out, u_out, b_raw,
-                                              diag_raw, part, ticket, sc)));
-}
-
-void launch_energy_ext(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* Y,
-                       double* part, unsigned* ticket, Scalars* sc) {
-  LS_DISPATCH_NT(f.NT, (launch_energy_ext_nt<NT_>(L, f, c, X, Y, part, ticket, sc)));
+                   const float* dx, float alpha, const float* Y, float* Xout, float* r_out, float* d_out,
+                   float* u_out, float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc,
+                   const EnergyMaps* maps) {
+  LS_DISPATCH_NT(f.NT, (launch_energy_nt<NT_>(mode, L, f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw,
+                                              diag_raw, part, ticket, sc, maps)));
 }
 
 void launch_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* u,
@@ -803,7 +887,8 @@ void launch_update(const Launch& L, int64_t M, float* x, float* r, float* p, flo
 int energy_grid_limit(int NT) {
   int nb = 0;
   LS_DISPATCH_NT(NT, (prepare_nt<NT_>(), cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                                             &nb, k_energy<NT_, MODE_TRIAL>, kThreads, energy_smem<NT_>(MODE_TRIAL))));
+                                             &nb, k_energy<NT_, MODE_TRIAL, true>, kThreads,
+                                             energy_smem<NT_>(MODE_TRIAL, true))));
   return nb;
 }
 int apply_grid_limit(int NT) {
