@@ -232,7 +232,7 @@ def run_reference(args):
 def run_ours(args):
     import numpy as np
     import torch
-    from paper_1908_01961_b200 import synth, _device
+    from paper_1908_01961_b200 import synth, _device, clips
     from paper_1908_01961_b200.energy import EnergyWeights
     from paper_1908_01961_b200.palette import BaseColorPalette
     from paper_1908_01961_b200.pipeline import StreamingDecomposer
@@ -285,11 +285,9 @@ def run_ours(args):
     t_ms = ev0.elapsed_time(ev1)
     prof = solver.profile_read()
     solver.profile(False)
-    if world > 1:
-        tt = torch.tensor([t_ms], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_ms = float(tt.item())
-    value = world * steps / (t_ms / 1e3)
+    th = clips.aggregate(steps, t_ms / 1e3)     # frames summed, time = max over ranks
+    t_ms = th.seconds * 1e3
+    value = th.fps
 
     # --- roofline of the dominant kernel (algorithmic bytes / event time) ---
     N = H * W
@@ -346,11 +344,8 @@ def run_ours(args):
         e1.record()
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1)
-        if world > 1:
-            tt = torch.tensor([e_ms], device=dev)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            e_ms = float(tt.item())
-        e2e = {"value": world * steps / (e_ms / 1e3), "unit": UNIT,
+        eth = clips.aggregate(steps, e_ms / 1e3)
+        e2e = {"value": eth.fps, "unit": UNIT,
                "h2d_bytes_per_step": int(host[0].numel() * 4),
                "d2h_bytes_per_step": int(U * H * W * 4),
                "api": "pipeline.StreamingDecomposer.step (reference decompose_frames loop)"}
