@@ -93,7 +93,7 @@ struct ls_ctx {
   ls_weights w{};
   ls_solve_cfg cfg{};
   cudaStream_t stream = nullptr;
-  int nsm = 0, ntiles = 0, grid_energy = 0, grid_apply = 0, grid_update = 0, grid_dense = 0;
+  int nsm = 0, ntiles = 0, grid_energy = 0, grid_apply = 0, grid_update = 0, grid_dense = 0, grid_pcg = 0;
   // per-frame aux
   float* img = nullptr;
   double* chroma = nullptr;
@@ -246,6 +246,7 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   c->ntiles = ((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH);
   c->grid_energy = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, energy_grid_limit(c->NT)), kMaxBlocks}));
   c->grid_apply = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, apply_grid_limit(c->NT)), kMaxBlocks}));
+  c->grid_pcg = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, pcg_apply_grid_limit(c->NT)), kMaxBlocks}));
   const int64_t upd_blocks = (M / 4 + kThreads - 1) / kThreads;
   c->grid_update = (int)std::max<int64_t>(1, std::min<int64_t>({upd_blocks, (int64_t)c->nsm * std::max(1, update_grid_limit()), (int64_t)kMaxBlocks}));
   c->grid_dense = std::max(1, std::min(c->nsm * 4, (N + 127) / 128));
@@ -684,11 +685,22 @@ int ls_apply_normal(ls_ctx* c, const double* colors, const float* X, const float
   return LS_OK;
 }
 
-// fused energy/gradient + PCG loop; x receives the step
+static bool pcg_maps(ls_ctx* c, const float* X, const float* pprev, PcgMaps* m) {
+  if (!c->use_tma) return false;
+  const int U = c->U, NT = c->NT, W = c->W, H = c->H;
+  const size_t N = (size_t)c->N;
+  return make_map(&m->X, X, W, H, U, tile_box_w(), kTileH + 2) &&
+         make_map(&m->ZT, c->u + 3 * N, W, H, NT, tile_box_w(), kTileH + 2) &&
+         make_map(&m->ZR, c->u, W, H, 3, tile_box_rw(), kTileH + 2 * kHalf) &&
+         make_map(&m->PT, pprev + 3 * N, W, H, NT, tile_box_w(), kTileH + 2) &&
+         make_map(&m->PR, pprev, W, H, 3, tile_box_rw(), kTileH + 2 * kHalf);
+}
+
+// fused energy/gradient + textbook PCG loop (solver.py:79-107); x receives the step.
+// Buffers: r, d = 1/diag, u = z = r/diag, wv = q = A p, p / s = ping-pong p.
 static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, float* x) {
   const Frame f = frame_of(c);
   const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
-  const Coef<float> cf = make_coef<float>(c->w, colors, c->K);
   size_t pi = prof_begin(c);
   EnergyMaps em;
   const bool etma = energy_maps(c, X, nullptr, &em);
@@ -696,17 +708,21 @@ static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, f
                 c->part, c->tickets + 0, c->sc, etma ? &em : nullptr);
   prof_end(c, PC_EG, pi);
   const int64_t M = (int64_t)c->U * c->N;
-  TileMaps maps;
-  const bool tma = tile_maps(c, X, c->u, &maps);
+  float* pbuf[2] = {c->p, c->s};
+  PcgMaps maps[2];
+  const bool tma = pcg_maps(c, X, pbuf[1], &maps[0]) && pcg_maps(c, X, pbuf[0], &maps[1]);
+  const Launch La{c->grid_pcg, c->ntiles, c->stream};
   for (int it = 0; it < iters; ++it) {
     pi = prof_begin(c);
-    launch_apply(L_apply(c), f, cf, X, c->u, c->wv, c->part, c->tickets + 1, c->sc, it, tma ? &maps : nullptr);
+    launch_pcg_apply(La, f, cd, X, c->u, pbuf[(it + 1) & 1], pbuf[it & 1], x, c->wv, c->part, c->tickets + 1,
+                     c->sc, it, tma ? &maps[it & 1] : nullptr);
     prof_end(c, PC_APPLY, pi);
     pi = prof_begin(c);
-    launch_update(L_update(c), M, x, c->r, c->p, c->s, c->wv, c->d, c->u, c->part, c->tickets + 2, c->sc, it);
+    launch_pcg_update(L_update(c), M, c->r, c->wv, c->d, c->u, c->part, c->tickets + 2, c->sc, it);
     prof_end(c, PC_UPDATE, pi);
   }
-  c->launches += 1 + 2LL * iters;
+  launch_pcg_xfinal(c->stream, c->grid_update, M, x, pbuf[0], pbuf[1], c->sc);
+  c->launches += 3 + 2LL * iters;
   LS_CK(cudaGetLastError());
   return LS_OK;
 }

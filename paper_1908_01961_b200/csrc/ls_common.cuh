@@ -64,15 +64,21 @@ struct Frame {
   const float* ent_w;     // per-entry pair weight or nullptr (all 1)
 };
 
-// device-resident PCG / step scalars (Chronopoulos-Gear PCG)
+// device-resident PCG / step scalars (textbook Jacobi PCG of solver.py:79-107
+// with the p-update fused into the operator kernel and a deferred x-update)
 struct Scalars {
-  double gamma, gamma_prev, delta, alpha, alpha_prev, beta;
+  double gamma, gamma_prev;   // rz_i = <r_i, z_i>, rz_{i-1}
+  double delta;               // pAp_i
+  double alpha, alpha_prev, beta;
   double bnorm2, rnorm2;
-  double terms0[kTerms];   // energies at the linearisation point
-  double terms1[kTerms];   // energies at the last trial point
+  double terms0[kTerms];      // energies at the linearisation point
+  double terms1[kTerms];      // energies at the last trial point
   int iterations;
   int stop;
-  int pad[2];
+  int pending;                // x still needs alpha * p_last
+  int xinit;                  // x has been written (else it is zero)
+  int plast;                  // ping-pong index of the last p written
+  int pad[3];
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }

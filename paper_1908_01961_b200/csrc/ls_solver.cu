@@ -354,11 +354,11 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
     g += gcons[ch];
     d += dcons;
     const float bf = -g;
-    const float dd = d > 0.f ? d : 1.f;
-    const float uf = bf / dd;
-    if (r_out) { r_out[ch * N + i] = bf; d_out[ch * N + i] = dd; u_out[ch * N + i] = uf; }
+    const float di = 1.f / (d > 0.f ? d : 1.f);   // Jacobi preconditioner (solver.py:87)
+    const float zf = bf * di;
+    if (r_out) { r_out[ch * N + i] = bf; d_out[ch * N + i] = di; u_out[ch * N + i] = zf; }
     if (b_raw) { b_raw[ch * N + i] = bf; diag_raw[ch * N + i] = d; }
-    rz = fmaf(bf, uf, rz);
+    rz = fmaf(bf, zf, rz);
     bb = fmaf(bf, bf, bb);
   }
 #pragma unroll
@@ -384,12 +384,12 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
     g = fmaf(c.lam_sm, gs, g);
     d = fmaf(c.lam_sm, ds, d);
     const float bf = -g;
-    const float dd = d > 0.f ? d : 1.f;
-    const float uf = bf / dd;
+    const float di = 1.f / (d > 0.f ? d : 1.f);
+    const float zf = bf * di;
     const size_t o = (size_t)(3 + k) * N + i;
-    if (r_out) { r_out[o] = bf; d_out[o] = dd; u_out[o] = uf; }
+    if (r_out) { r_out[o] = bf; d_out[o] = di; u_out[o] = zf; }
     if (b_raw) { b_raw[o] = bf; diag_raw[o] = d; }
-    rz = fmaf(bf, uf, rz);
+    rz = fmaf(bf, zf, rz);
     bb = fmaf(bf, bf, bb);
   }
   acc[kTerms] += (double)rz;
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
   const int ntx = (W + kTileW - 1) / kTileW;
   // the evaluation point: X itself, X + alpha*dx, or an external Y
   const bool ext = TRIAL && Yext != nullptr;
-  const bool step = TRIAL && !ext && dx != nullptr && sc->iterations > 0;
+  const bool step = TRIAL && !ext && dx != nullptr && sc->xinit;
   const bool with_d = ext || step;
   double acc[NV];
 #pragma unroll
@@ -500,6 +500,9 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
       sc->rnorm2 = tot[kTerms + 1];
       sc->alpha = sc->alpha_prev = sc->beta = sc->delta = 0.0;
       sc->iterations = 0;
+      sc->pending = 0;
+      sc->xinit = 0;
+      sc->plast = 0;
       // zero rhs -> x = 0 (solver.py:85-86); non-finite -> host raises
       sc->stop = (!finite || tot[kTerms + 1] == 0.0 || r_out == nullptr) ? 1 : 0;
     } else {
@@ -785,6 +788,227 @@ __global__ void __launch_bounds__(kThreads) k_update(int64_t M, float* __restric
 }
 
 // ---------------------------------------------------------------------------
+// textbook Jacobi PCG (solver.py:79-107), two kernels per iteration:
+//   k_pcg_apply  i: p_i = z_i + beta_i p_{i-1} (formed in shared memory on the
+//                   tile + halo), q_i = J^T J p_i, x_i = x_{i-1} + alpha_{i-1}
+//                   p_{i-1} (deferred update, owned pixels), <p_i, q_i>;
+//                   last CTA: alpha_i = rz_i / pAp_i or break (solver.py:95)
+//   k_pcg_update i: r_{i+1} = r_i - alpha_i q_i, z = r * dinv, <r, z>, |r|^2;
+//                   last CTA: beta, break on rz <= 0 (solver.py:101-103)
+//   k_pcg_xfinal   : applies the last pending alpha p to x
+// HBM words / pixel / iteration: (X + z + p_prev + x) + (p + q + x) +
+// (r + q + dinv) + (r + z) = 12U  (vs 15U for a separate update pass).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int op_floats(int NT) { return pad32(NT * kSP) + pad32(3 * kRP); }
+__host__ __device__ constexpr int pcg_stage(int NT) { return pad32((NT + 3) * kSP) + 2 * op_floats(NT); }
+
+template <int NT>
+__device__ __forceinline__ void tma_issue_pcg(float* stage, const PcgMaps& m, uint64_t* bar, int tx0, int ty0,
+                                              bool with_p) {
+  constexpr uint32_t xb = sizeof(float) * (NT + 3) * kSP;
+  constexpr uint32_t ob = sizeof(float) * (NT * kSP + 3 * kRP);
+  mbar_expect_tx(bar, xb + (with_p ? 2 : 1) * ob);
+  float* z = stage + pad32((NT + 3) * kSP);
+  float* pp = z + op_floats(NT);
+  tma_load_3d(stage, &m.X, bar, tx0 - kSX, ty0 - 1, 0);
+  tma_load_3d(z, &m.ZT, bar, tx0 - kSX, ty0 - 1, 0);
+  tma_load_3d(z + pad32(NT * kSP), &m.ZR, bar, tx0 - kRX, ty0 - kHalf, 0);
+  if (with_p) {
+    tma_load_3d(pp, &m.PT, bar, tx0 - kSX, ty0 - 1, 0);
+    tma_load_3d(pp + pad32(NT * kSP), &m.PR, bar, tx0 - kRX, ty0 - kHalf, 0);
+  }
+}
+
+template <int NT, bool TMA>
+__global__ void __launch_bounds__(kThreads, 3) k_pcg_apply(Frame f, Coef<float> c, const float* __restrict__ X,
+                                                           const float* __restrict__ z,
+                                                           const float* __restrict__ pprev,
+                                                           float* __restrict__ pnew, float* __restrict__ xv,
+                                                           float* __restrict__ q, double* part, unsigned* ticket,
+                                                           Scalars* sc, int iter, int ntiles,
+                                                           const __grid_constant__ PcgMaps maps) {
+  constexpr int U = NT + 3;
+  constexpr int STAGE = pcg_stage(NT);
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t bars[1];
+  if (sc->stop) return;
+  const int W = f.W, H = f.H, N = f.N;
+  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+  const int cx = lx + kSX, cy = ly + 1, rx = lx + kRX, ry = ly + kHalf;
+  const int ntx = (W + kTileW - 1) / kTileW;
+  const bool with_p = iter > 0;
+  const float beta = (float)sc->beta;
+  const float alpha_prev = (float)sc->alpha;
+  const bool do_x = with_p && sc->pending;   // x_i = x_{i-1} + alpha_{i-1} p_{i-1}
+  const bool xzero = !sc->xinit;
+  float* sX = smem;
+  float* sZT = smem + pad32(U * kSP);
+  float* sZR = sZT + pad32(NT * kSP);
+  float* sPT = sZT + op_floats(NT);
+  float* sPR = sPT + pad32(NT * kSP);
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bars[0], 1);
+      fence_barrier_init();
+      if ((int)blockIdx.x < ntiles) {
+        const int t = blockIdx.x;
+        tma_issue_pcg<NT>(smem, maps, &bars[0], (t % ntx) * kTileW, (t / ntx) * kTileH, with_p);
+      }
+    }
+    __syncthreads();
+  }
+  uint32_t phase = 0;
+  float acc = 0.f;
+  double accd = 0.0;
+  for (int j = 0;; ++j) {
+    const int tile = blockIdx.x + j * gridDim.x;
+    if (tile >= ntiles) break;
+    const int tx0 = (tile % ntx) * kTileW, ty0 = (tile / ntx) * kTileH;
+    const int x = tx0 + lx, y = ty0 + ly;
+    const bool own = x < W && y < H;
+    // owned-pixel x values: issued before waiting for the tile (independent)
+    float xo[U];
+    if (do_x && own && !xzero) {
+#pragma unroll
+      for (int pl = 0; pl < U; ++pl) xo[pl] = xv[(size_t)pl * N + y * W + x];
+    } else {
+#pragma unroll
+      for (int pl = 0; pl < U; ++pl) xo[pl] = 0.f;
+    }
+    if (TMA) {
+      mbar_wait(&bars[0], phase);
+      phase ^= 1u;
+    } else {
+      __syncthreads();
+      load_halo1<U>(sX, X, N, W, H, tx0, ty0);
+      load_halo1<NT>(sZT, z + 3 * (size_t)N, N, W, H, tx0, ty0);
+      load_halo7(sZR, z, nullptr, 0.f, N, W, H, tx0, ty0);
+      if (with_p) {
+        load_halo1<NT>(sPT, pprev + 3 * (size_t)N, N, W, H, tx0, ty0);
+        load_halo7(sPR, pprev, nullptr, 0.f, N, W, H, tx0, ty0);
+      }
+      __syncthreads();
+    }
+    if (with_p) {   // operand p_i = z_i + beta_i p_{i-1} on the whole window
+      for (int e = threadIdx.x; e < NT * kSP; e += kThreads) sZT[e] = fmaf(beta, sPT[e], sZT[e]);
+      for (int e = threadIdx.x; e < 3 * kRP; e += kThreads) sZR[e] = fmaf(beta, sPR[e], sZR[e]);
+      __syncthreads();
+    }
+    const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H;
+    if (interior)
+      acc += apply_pixel<NT, true>(f, c, sX, sZT, sZR, q, x, y, cx, cy, rx, ry);
+    else if (own)
+      acc += apply_pixel<NT, false>(f, c, sX, sZT, sZR, q, x, y, cx, cy, rx, ry);
+    if (own) {
+      const int i = y * W + x;
+      const int sc0 = cy * kSW + cx, rc0 = ry * kRW + rx;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const size_t o = (size_t)ch * N + i;
+        pnew[o] = sZR[ch * kRP + rc0];
+        if (do_x) xv[o] = fmaf(alpha_prev, sPR[ch * kRP + rc0], xo[ch]);
+      }
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        const size_t o = (size_t)(3 + k) * N + i;
+        pnew[o] = sZT[k * kSP + sc0];
+        if (do_x) xv[o] = fmaf(alpha_prev, sPT[k * kSP + sc0], xo[3 + k]);
+      }
+    }
+    if (TMA) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int t = blockIdx.x + (j + 1) * gridDim.x;
+        if (t < ntiles) tma_issue_pcg<NT>(smem, maps, &bars[0], (t % ntx) * kTileW, (t / ntx) * kTileH, with_p);
+      }
+    }
+    accd += (double)acc;
+    acc = 0.f;
+  }
+  double accv[1] = {accd};
+  block_reduce_store<1>(accv, part);
+  if (!last_block(ticket)) return;
+  const double pap = sum_partials<1>(part, gridDim.x, 0);
+  if (threadIdx.x == 0) {
+    if (do_x) {
+      sc->xinit = 1;
+      sc->pending = 0;
+    }
+    sc->delta = pap;
+    sc->plast = iter & 1;
+    if (!(pap > 0.0) || !isfinite(pap)) {
+      sc->stop = 1;                       // solver.py:95-96: break before the update
+    } else {
+      sc->alpha_prev = sc->alpha;
+      sc->alpha = sc->gamma / pap;
+      sc->pending = 1;
+    }
+    *ticket = 0u;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __restrict__ r, const float* __restrict__ q,
+                                                         const float* __restrict__ dinv, float* __restrict__ z,
+                                                         double* part, unsigned* ticket, Scalars* sc, int iter) {
+  if (sc->stop) return;
+  const float a = (float)sc->alpha;
+  double acc[2] = {0.0, 0.0};
+  const int64_t M4 = M >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M4; j += stride) {
+    float4 rr = reinterpret_cast<const float4*>(r)[j];
+    const float4 qq = __ldg(reinterpret_cast<const float4*>(q) + j);
+    const float4 di = __ldg(reinterpret_cast<const float4*>(dinv) + j);
+    rr = make_float4(fmaf(-a, qq.x, rr.x), fmaf(-a, qq.y, rr.y), fmaf(-a, qq.z, rr.z), fmaf(-a, qq.w, rr.w));
+    const float4 zz = make_float4(rr.x * di.x, rr.y * di.y, rr.z * di.z, rr.w * di.w);
+    reinterpret_cast<float4*>(r)[j] = rr;
+    reinterpret_cast<float4*>(z)[j] = zz;
+    acc[0] += (double)fmaf(rr.x, zz.x, fmaf(rr.y, zz.y, fmaf(rr.z, zz.z, rr.w * zz.w)));
+    acc[1] += (double)fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, fmaf(rr.z, rr.z, rr.w * rr.w)));
+  }
+  for (int64_t j = (M4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride) {
+    const float rr = fmaf(-a, q[j], r[j]);
+    const float zz = rr * dinv[j];
+    r[j] = rr;
+    z[j] = zz;
+    acc[0] += (double)rr * zz;
+    acc[1] += (double)rr * rr;
+  }
+  block_reduce_store<2>(acc, part);
+  if (!last_block(ticket)) return;
+  const double rz = sum_partials<2>(part, gridDim.x, 0);
+  const double rn = sum_partials<2>(part, gridDim.x, 1);
+  if (threadIdx.x == 0) {
+    sc->iterations = iter + 1;
+    sc->gamma_prev = sc->gamma;
+    sc->gamma = rz;
+    sc->rnorm2 = rn;
+    sc->beta = rz / sc->gamma_prev;
+    if (rz <= 0.0) sc->stop = 1;          // solver.py:101-103
+    *ticket = 0u;
+  }
+}
+
+__global__ void k_pcg_xfinal(int64_t M, float* __restrict__ xv, const float* __restrict__ p0,
+                             const float* __restrict__ p1, Scalars* sc) {
+  if (!sc->pending) return;
+  const float a = (float)sc->alpha;
+  const float* p = sc->plast ? p1 : p0;
+  const bool xzero = !sc->xinit;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x)
+    xv[j] = fmaf(a, p[j], xzero ? 0.f : xv[j]);
+}
+
+// flag update after k_pcg_xfinal (stream-ordered, one thread)
+
+__global__ void k_pcg_xflags(Scalars* sc) {
+  if (sc->pending) {
+    sc->xinit = 1;
+    sc->pending = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host-side launchers (dispatch on NT)
 // ---------------------------------------------------------------------------
 #define LS_DISPATCH_NT(NTV, CALL)                       \
@@ -814,7 +1038,12 @@ template <int NT>
 static size_t apply_smem(bool tma) { return sizeof(float) * tile_floats(NT, true) * (tma ? 2 : 1); }
 
 template <int NT>
+static size_t pcg_smem() { return sizeof(float) * pcg_stage(NT); }
+
+template <int NT>
 static void prepare_nt() {
+  cudaFuncSetAttribute(k_pcg_apply<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcg_smem<NT>());
+  cudaFuncSetAttribute(k_pcg_apply<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcg_smem<NT>());
   cudaFuncSetAttribute(k_energy<NT, MODE_EG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)energy_smem<NT>(MODE_EG, true));
   cudaFuncSetAttribute(k_energy<NT, MODE_EG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -877,6 +1106,42 @@ void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<float>&
 void launch_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* u,
                   float* w, double* part, unsigned* ticket, Scalars* sc, int iter, const TileMaps* maps) {
   LS_DISPATCH_NT(f.NT, (launch_apply_nt<NT_>(L, f, c, X, u, w, part, ticket, sc, iter, maps)));
+}
+
+template <int NT>
+static void launch_pcg_apply_nt(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* z,
+                                const float* pprev, float* pnew, float* xv, float* q, double* part, unsigned* ticket,
+                                Scalars* sc, int iter, const PcgMaps* maps) {
+  if (maps)
+    k_pcg_apply<NT, true><<<L.grid, kThreads, pcg_smem<NT>(), L.stream>>>(f, c, X, z, pprev, pnew, xv, q, part, ticket,
+                                                                         sc, iter, L.ntiles, *maps);
+  else
+    k_pcg_apply<NT, false><<<L.grid, kThreads, pcg_smem<NT>(), L.stream>>>(f, c, X, z, pprev, pnew, xv, q, part,
+                                                                          ticket, sc, iter, L.ntiles, PcgMaps{});
+}
+
+void launch_pcg_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* z,
+                      const float* pprev, float* pnew, float* xv, float* q, double* part, unsigned* ticket,
+                      Scalars* sc, int iter, const PcgMaps* maps) {
+  LS_DISPATCH_NT(f.NT, (launch_pcg_apply_nt<NT_>(L, f, c, X, z, pprev, pnew, xv, q, part, ticket, sc, iter, maps)));
+}
+
+void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
+                       double* part, unsigned* ticket, Scalars* sc, int iter) {
+  k_pcg_update<<<L.grid, kThreads, 0, L.stream>>>(M, r, q, dinv, z, part, ticket, sc, iter);
+}
+
+void launch_pcg_xfinal(cudaStream_t s, int grid, int64_t M, float* xv, const float* p0, const float* p1,
+                       Scalars* sc) {
+  k_pcg_xfinal<<<grid, kThreads, 0, s>>>(M, xv, p0, p1, sc);
+  k_pcg_xflags<<<1, 1, 0, s>>>(sc);
+}
+
+int pcg_apply_grid_limit(int NT) {
+  int nb = 0;
+  LS_DISPATCH_NT(NT, (prepare_nt<NT_>(), cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                             &nb, k_pcg_apply<NT_, true>, kThreads, pcg_smem<NT_>())));
+  return nb;
 }
 
 void launch_update(const Launch& L, int64_t M, float* x, float* r, float* p, float* s, const float* w,
