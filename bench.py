@@ -293,8 +293,10 @@ def run_ours(args):
     N = H * W
     U = K + 4
     ent_per_px = prof["adjacency_entries"] / N
-    bytes_apply = N * (4 * (2 * U + 1) + 4 * U + 8 + 2 * ent_per_px)
-    bytes_update = N * 4 * 12 * U
+    # k_pcg_apply: reads X, z, p_prev (3U), edge, row_ptr, entries; writes p, q (2U)
+    bytes_apply = N * (4 * (5 * U + 2) + 2 * ent_per_px)
+    # k_pcg_update: reads r, q, dinv, p, x (5U); writes r, z, x (3U)
+    bytes_update = N * 4 * 8 * U
     kern = {
         "apply": (prof["apply"], bytes_apply),
         "update": (prof["update"], bytes_update),

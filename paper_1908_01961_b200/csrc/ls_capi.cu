@@ -714,15 +714,14 @@ static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, f
   const Launch La{c->grid_pcg, c->ntiles, c->stream};
   for (int it = 0; it < iters; ++it) {
     pi = prof_begin(c);
-    launch_pcg_apply(La, f, cd, X, c->u, pbuf[(it + 1) & 1], pbuf[it & 1], x, c->wv, c->part, c->tickets + 1,
-                     c->sc, it, tma ? &maps[it & 1] : nullptr);
+    launch_pcg_apply(La, f, cd, X, c->u, pbuf[(it + 1) & 1], pbuf[it & 1], c->wv, c->part, c->tickets + 1, c->sc,
+                     it, tma ? &maps[it & 1] : nullptr);
     prof_end(c, PC_APPLY, pi);
     pi = prof_begin(c);
-    launch_pcg_update(L_update(c), M, c->r, c->wv, c->d, c->u, c->part, c->tickets + 2, c->sc, it);
+    launch_pcg_update(L_update(c), M, c->r, c->wv, c->d, c->u, pbuf[it & 1], x, c->part, c->tickets + 2, c->sc, it);
     prof_end(c, PC_UPDATE, pi);
   }
-  launch_pcg_xfinal(c->stream, c->grid_update, M, x, pbuf[0], pbuf[1], c->sc);
-  c->launches += 3 + 2LL * iters;
+  c->launches += 1 + 2LL * iters;
   LS_CK(cudaGetLastError());
   return LS_OK;
 }

@@ -46,12 +46,10 @@ int tile_box_rw();
 void launch_update(const Launch& L, int64_t M, float* x, float* r, float* p, float* s, const float* w,
                    const float* d, float* u, double* part, unsigned* ticket, Scalars* sc, int iter);
 void launch_pcg_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* z,
-                      const float* pprev, float* pnew, float* xv, float* q, double* part, unsigned* ticket,
-                      Scalars* sc, int iter, const PcgMaps* maps);
+                      const float* pprev, float* pnew, float* q, double* part, unsigned* ticket, Scalars* sc,
+                      int iter, const PcgMaps* maps);
 void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
-                       double* part, unsigned* ticket, Scalars* sc, int iter);
-void launch_pcg_xfinal(cudaStream_t s, int grid, int64_t M, float* xv, const float* p0, const float* p1,
-                       Scalars* sc);
+                       const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter);
 int pcg_apply_grid_limit(int NT);
 int energy_grid_limit(int NT);
 void prepare_kernels(int NT);

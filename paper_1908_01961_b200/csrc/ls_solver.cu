@@ -537,32 +537,32 @@ __device__ __forceinline__ float apply_pixel(const Frame& f, const Coef<float>& 
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) S0[ch] = fmaf(T0[k], c.B[k][ch], S0[ch]);
   }
-  // data rows rho_c = R0 (S0 u_r + sum_k b_kc u_Tk) (energy.py:211-218),
-  // monochrome q_c = w_edge sum_k G_kc u_Tk (energy.py:403-408)
-  float rho[3], q[3], outr[3];
+  // data rows rho_c = R0 (S0 u_r + sum_k b_kc u_Tk) (energy.py:211-218) and
+  // monochrome q_c = w_edge sum_k G_kc u_Tk (energy.py:403-408).  With
+  // G = B - rowmean(B): sum_k G_kc u_k = s_c - mean_c(s) and sum_c q_c = 0,
+  // so the T rows are sum_c B_kc (rho_c + q_c).
+  float rq[3], outr[3], s[3] = {0.f, 0.f, 0.f};
   const float lm = c.lam_m * __ldg(f.edge + i);
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    float s = 0.f, qq = 0.f;
+  for (int k = 0; k < NT; ++k)
 #pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      s = fmaf(uT[k], c.B[k][ch], s);
-      qq = fmaf(uT[k], c.G[k][ch], qq);
-    }
+    for (int ch = 0; ch < 3; ++ch) s[ch] = fmaf(uT[k], c.B[k][ch], s[ch]);
+  const float smean = (s[0] + s[1] + s[2]) * (1.f / 3.f);
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
     const float r0s0 = R0[ch] * S0[ch];
-    const float rr = fmaf(r0s0, ur[ch], R0[ch] * s);
+    const float rr = fmaf(r0s0, ur[ch], R0[ch] * s[ch]);
     outr[ch] = fmaf(c.lam_d * r0s0, rr, c.lam_cl * ur[ch]);
-    q[ch] = qq * lm;
-    rho[ch] = c.lam_d * R0[ch] * rr;
+    rq[ch] = fmaf(c.lam_d * R0[ch], rr, lm * (s[ch] - smean));
   }
   float dot = 0.f;
 #pragma unroll
   for (int k = 0; k < NT; ++k) {
     const float* P = sX + (3 + k) * kSP + sc0;
     const float* Q = sT + k * kSP + sc0;
-    float a = 0.f;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) a = fmaf(c.B[k][ch], rho[ch], fmaf(c.G[k][ch], q[ch], a));
+    float a = c.B[k][0] * rq[0];
+    a = fmaf(c.B[k][1], rq[1], a);
+    a = fmaf(c.B[k][2], rq[2], a);
     const float v = T0[k], uv = uT[k];
     const float wis = (k >= 1) ? c.lam_is * irls1f(v, c) : 0.f;
     const float wnn = c.lam_nn * nonneg_wf(v, c.eps_nn);
@@ -790,14 +790,14 @@ __global__ void __launch_bounds__(kThreads) k_update(int64_t M, float* __restric
 // ---------------------------------------------------------------------------
 // textbook Jacobi PCG (solver.py:79-107), two kernels per iteration:
 //   k_pcg_apply  i: p_i = z_i + beta_i p_{i-1} (formed in shared memory on the
-//                   tile + halo), q_i = J^T J p_i, x_i = x_{i-1} + alpha_{i-1}
-//                   p_{i-1} (deferred update, owned pixels), <p_i, q_i>;
+//                   tile + halo), q_i = J^T J p_i, <p_i, q_i>;
 //                   last CTA: alpha_i = rz_i / pAp_i or break (solver.py:95)
-//   k_pcg_update i: r_{i+1} = r_i - alpha_i q_i, z = r * dinv, <r, z>, |r|^2;
+//   k_pcg_update i: x += alpha_i p_i, r_{i+1} = r_i - alpha_i q_i,
+//                   z = r * dinv, <r, z>, |r|^2;
 //                   last CTA: beta, break on rz <= 0 (solver.py:101-103)
-//   k_pcg_xfinal   : applies the last pending alpha p to x
-// HBM words / pixel / iteration: (X + z + p_prev + x) + (p + q + x) +
-// (r + q + dinv) + (r + z) = 12U  (vs 15U for a separate update pass).
+// HBM words / pixel / iteration: (X + z + p_prev) + (p + q) +
+// (r + q + dinv + p + x) + (r + z + x) = 13U (vs 15U for the CG form with a
+// separate vector update; forming p costs no pass of its own).
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int op_floats(int NT) { return pad32(NT * kSP) + pad32(3 * kRP); }
 __host__ __device__ constexpr int pcg_stage(int NT) { return pad32((NT + 3) * kSP) + 2 * op_floats(NT); }
@@ -823,8 +823,7 @@ template <int NT, bool TMA>
 __global__ void __launch_bounds__(kThreads, 3) k_pcg_apply(Frame f, Coef<float> c, const float* __restrict__ X,
                                                            const float* __restrict__ z,
                                                            const float* __restrict__ pprev,
-                                                           float* __restrict__ pnew, float* __restrict__ xv,
-                                                           float* __restrict__ q, double* part, unsigned* ticket,
+                                                           float* __restrict__ pnew, float* __restrict__ q, double* part, unsigned* ticket,
                                                            Scalars* sc, int iter, int ntiles,
                                                            const __grid_constant__ PcgMaps maps) {
   constexpr int U = NT + 3;
@@ -838,9 +837,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_apply(Frame f, Coef<float> 
   const int ntx = (W + kTileW - 1) / kTileW;
   const bool with_p = iter > 0;
   const float beta = (float)sc->beta;
-  const float alpha_prev = (float)sc->alpha;
-  const bool do_x = with_p && sc->pending;   // x_i = x_{i-1} + alpha_{i-1} p_{i-1}
-  const bool xzero = !sc->xinit;
   float* sX = smem;
   float* sZT = smem + pad32(U * kSP);
   float* sZR = sZT + pad32(NT * kSP);
@@ -866,15 +862,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_apply(Frame f, Coef<float> 
     const int tx0 = (tile % ntx) * kTileW, ty0 = (tile / ntx) * kTileH;
     const int x = tx0 + lx, y = ty0 + ly;
     const bool own = x < W && y < H;
-    // owned-pixel x values: issued before waiting for the tile (independent)
-    float xo[U];
-    if (do_x && own && !xzero) {
-#pragma unroll
-      for (int pl = 0; pl < U; ++pl) xo[pl] = xv[(size_t)pl * N + y * W + x];
-    } else {
-#pragma unroll
-      for (int pl = 0; pl < U; ++pl) xo[pl] = 0.f;
-    }
     if (TMA) {
       mbar_wait(&bars[0], phase);
       phase ^= 1u;
@@ -906,13 +893,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_apply(Frame f, Coef<float> 
       for (int ch = 0; ch < 3; ++ch) {
         const size_t o = (size_t)ch * N + i;
         pnew[o] = sZR[ch * kRP + rc0];
-        if (do_x) xv[o] = fmaf(alpha_prev, sPR[ch * kRP + rc0], xo[ch]);
       }
 #pragma unroll
       for (int k = 0; k < NT; ++k) {
         const size_t o = (size_t)(3 + k) * N + i;
         pnew[o] = sZT[k * kSP + sc0];
-        if (do_x) xv[o] = fmaf(alpha_prev, sPT[k * kSP + sc0], xo[3 + k]);
       }
     }
     if (TMA) {
@@ -930,18 +915,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_apply(Frame f, Coef<float> 
   if (!last_block(ticket)) return;
   const double pap = sum_partials<1>(part, gridDim.x, 0);
   if (threadIdx.x == 0) {
-    if (do_x) {
-      sc->xinit = 1;
-      sc->pending = 0;
-    }
     sc->delta = pap;
-    sc->plast = iter & 1;
     if (!(pap > 0.0) || !isfinite(pap)) {
       sc->stop = 1;                       // solver.py:95-96: break before the update
     } else {
       sc->alpha_prev = sc->alpha;
       sc->alpha = sc->gamma / pap;
-      sc->pending = 1;
     }
     *ticket = 0u;
   }
@@ -949,9 +928,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_apply(Frame f, Coef<float> 
 
 __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __restrict__ r, const float* __restrict__ q,
                                                          const float* __restrict__ dinv, float* __restrict__ z,
+                                                         const float* __restrict__ p, float* __restrict__ xv,
                                                          double* part, unsigned* ticket, Scalars* sc, int iter) {
   if (sc->stop) return;
   const float a = (float)sc->alpha;
+  const bool first = iter == 0;            // x_0 = 0 (solver.py:82)
   double acc[2] = {0.0, 0.0};
   const int64_t M4 = M >> 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -959,14 +940,19 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
     float4 rr = reinterpret_cast<const float4*>(r)[j];
     const float4 qq = __ldg(reinterpret_cast<const float4*>(q) + j);
     const float4 di = __ldg(reinterpret_cast<const float4*>(dinv) + j);
+    const float4 pp = __ldg(reinterpret_cast<const float4*>(p) + j);
+    float4 xx = first ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4*>(xv)[j];
+    xx = make_float4(fmaf(a, pp.x, xx.x), fmaf(a, pp.y, xx.y), fmaf(a, pp.z, xx.z), fmaf(a, pp.w, xx.w));
     rr = make_float4(fmaf(-a, qq.x, rr.x), fmaf(-a, qq.y, rr.y), fmaf(-a, qq.z, rr.z), fmaf(-a, qq.w, rr.w));
     const float4 zz = make_float4(rr.x * di.x, rr.y * di.y, rr.z * di.z, rr.w * di.w);
     reinterpret_cast<float4*>(r)[j] = rr;
     reinterpret_cast<float4*>(z)[j] = zz;
+    reinterpret_cast<float4*>(xv)[j] = xx;
     acc[0] += (double)fmaf(rr.x, zz.x, fmaf(rr.y, zz.y, fmaf(rr.z, zz.z, rr.w * zz.w)));
     acc[1] += (double)fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, fmaf(rr.z, rr.z, rr.w * rr.w)));
   }
   for (int64_t j = (M4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride) {
+    xv[j] = fmaf(a, p[j], first ? 0.f : xv[j]);
     const float rr = fmaf(-a, q[j], r[j]);
     const float zz = rr * dinv[j];
     r[j] = rr;
@@ -980,31 +966,13 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
   const double rn = sum_partials<2>(part, gridDim.x, 1);
   if (threadIdx.x == 0) {
     sc->iterations = iter + 1;
+    sc->xinit = 1;
     sc->gamma_prev = sc->gamma;
     sc->gamma = rz;
     sc->rnorm2 = rn;
     sc->beta = rz / sc->gamma_prev;
     if (rz <= 0.0) sc->stop = 1;          // solver.py:101-103
     *ticket = 0u;
-  }
-}
-
-__global__ void k_pcg_xfinal(int64_t M, float* __restrict__ xv, const float* __restrict__ p0,
-                             const float* __restrict__ p1, Scalars* sc) {
-  if (!sc->pending) return;
-  const float a = (float)sc->alpha;
-  const float* p = sc->plast ? p1 : p0;
-  const bool xzero = !sc->xinit;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x)
-    xv[j] = fmaf(a, p[j], xzero ? 0.f : xv[j]);
-}
-
-// flag update after k_pcg_xfinal (stream-ordered, one thread)
-
-__global__ void k_pcg_xflags(Scalars* sc) {
-  if (sc->pending) {
-    sc->xinit = 1;
-    sc->pending = 0;
   }
 }
 
@@ -1110,31 +1078,25 @@ void launch_apply(const Launch& L, const Frame& f, const Coef<float>& c, const f
 
 template <int NT>
 static void launch_pcg_apply_nt(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* z,
-                                const float* pprev, float* pnew, float* xv, float* q, double* part, unsigned* ticket,
+                                const float* pprev, float* pnew, float* q, double* part, unsigned* ticket,
                                 Scalars* sc, int iter, const PcgMaps* maps) {
   if (maps)
-    k_pcg_apply<NT, true><<<L.grid, kThreads, pcg_smem<NT>(), L.stream>>>(f, c, X, z, pprev, pnew, xv, q, part, ticket,
+    k_pcg_apply<NT, true><<<L.grid, kThreads, pcg_smem<NT>(), L.stream>>>(f, c, X, z, pprev, pnew, q, part, ticket,
                                                                          sc, iter, L.ntiles, *maps);
   else
-    k_pcg_apply<NT, false><<<L.grid, kThreads, pcg_smem<NT>(), L.stream>>>(f, c, X, z, pprev, pnew, xv, q, part,
-                                                                          ticket, sc, iter, L.ntiles, PcgMaps{});
+    k_pcg_apply<NT, false><<<L.grid, kThreads, pcg_smem<NT>(), L.stream>>>(f, c, X, z, pprev, pnew, q, part, ticket,
+                                                                          sc, iter, L.ntiles, PcgMaps{});
 }
 
 void launch_pcg_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* z,
-                      const float* pprev, float* pnew, float* xv, float* q, double* part, unsigned* ticket,
-                      Scalars* sc, int iter, const PcgMaps* maps) {
-  LS_DISPATCH_NT(f.NT, (launch_pcg_apply_nt<NT_>(L, f, c, X, z, pprev, pnew, xv, q, part, ticket, sc, iter, maps)));
+                      const float* pprev, float* pnew, float* q, double* part, unsigned* ticket, Scalars* sc,
+                      int iter, const PcgMaps* maps) {
+  LS_DISPATCH_NT(f.NT, (launch_pcg_apply_nt<NT_>(L, f, c, X, z, pprev, pnew, q, part, ticket, sc, iter, maps)));
 }
 
 void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
-                       double* part, unsigned* ticket, Scalars* sc, int iter) {
-  k_pcg_update<<<L.grid, kThreads, 0, L.stream>>>(M, r, q, dinv, z, part, ticket, sc, iter);
-}
-
-void launch_pcg_xfinal(cudaStream_t s, int grid, int64_t M, float* xv, const float* p0, const float* p1,
-                       Scalars* sc) {
-  k_pcg_xfinal<<<grid, kThreads, 0, s>>>(M, xv, p0, p1, sc);
-  k_pcg_xflags<<<1, 1, 0, s>>>(sc);
+                       const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter) {
+  k_pcg_update<<<L.grid, kThreads, 0, L.stream>>>(M, r, q, dinv, z, p, xv, part, ticket, sc, iter);
 }
 
 int pcg_apply_grid_limit(int NT) {
