@@ -1,0 +1,183 @@
+"""GPU tests at full size and on the less common code paths:
+1080p bit-exact sampler / segmentation vs the oracle, operator symmetry,
+bitwise determinism, TMA vs cooperative-load paths, K = 0 and K = 12
+instantiations, non-default weights (p != 1, identity chroma regulariser)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lumisplit_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _clip(H, W, K, n=2, seed=0):
+    from paper_1908_01961_b200 import synth
+    return synth.make_clip(H, W, K, n, seed=seed, device="cpu")
+
+
+def _state(clip, idx=0, prev=None, weights=None, seed=0):
+    from paper_1908_01961_b200.energy import EnergyWeights
+    from paper_1908_01961_b200.imaging import Frame, chromaticity
+    from paper_1908_01961_b200.palette import BaseColorPalette, segment
+    from paper_1908_01961_b200.solver import SolveConfig, SolverState, build_aux, initialize
+    frame = Frame(clip.frames[idx].cuda())
+    pal = BaseColorPalette(colors=clip.colors)
+    cm = segment(frame, pal)
+    if prev is None:
+        aux = build_aux(frame, cm, seed)
+        layers = initialize(frame, cm, pal)
+    else:
+        pframe, players = prev
+        aux = build_aux(frame, cm, seed, prev_chroma=chromaticity(pframe), prev_r=players.r)
+        layers = players.copy()
+    return SolverState(frame=frame, palette=pal, layers=layers, aux=aux,
+                       weights=weights or EnergyWeights(), config=SolveConfig(tol_rel=0.0))
+
+
+def test_1080p_sampler_and_segment_bit_exact():
+    clip = _clip(1080, 1920, 8, n=2, seed=4)
+    from paper_1908_01961_b200.imaging import Frame, chromaticity
+    from paper_1908_01961_b200.energy import sample_consistency
+    from paper_1908_01961_b200.palette import segment, BaseColorPalette
+    f0, f1 = (Frame(f.cuda()) for f in clip.frames)
+    c0, c1 = chromaticity(f0), chromaticity(f1)
+    s = sample_consistency(c1, c0, 11)
+    img0 = clip.frames[0].double().numpy()
+    img1 = clip.frames[1].double().numpy()
+    ref = O.sample_pairs(O.chromaticity(img1)[0], O.chromaticity(img0)[0], 11)
+    assert np.array_equal(s.src.cpu().numpy(), ref.src)
+    assert np.array_equal(s.dst.cpu().numpy(), ref.dst)
+    assert np.array_equal(s.temporal.cpu().numpy(), ref.temporal)
+    ids = segment(f1, BaseColorPalette(colors=clip.colors)).ids.cpu().numpy()
+    assert np.array_equal(ids, O.segment(img1, clip.colors))
+
+
+def test_1080p_operator_symmetric_and_step_deterministic():
+    from paper_1908_01961_b200.energy import assemble_blocks
+    from paper_1908_01961_b200.solver import gn_step_sparse
+    clip = _clip(1080, 1920, 8, n=1, seed=5)
+    st = _state(clip)
+    blocks = assemble_blocks(st.frame, st.palette, st.layers, st.aux, st.weights)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    p = torch.randn(st.layers.X.shape, device="cuda", generator=g)
+    q = torch.randn(st.layers.X.shape, device="cuda", generator=g)
+    Ap, Aq = blocks.apply_normal(p), blocks.apply_normal(q)
+    a = float((q.double() * Ap.double()).sum())
+    b = float((p.double() * Aq.double()).sum())
+    assert abs(a - b) <= 1e-5 * max(abs(a), abs(b))
+    assert float((p.double() * Ap.double()).sum()) > 0       # J^T J is PSD
+    X0 = st.layers.X.clone()
+    r1 = gn_step_sparse(st)
+    X1 = st.layers.X.clone()
+    st2 = _state(clip)
+    st2.layers.X.copy_(X0)
+    r2 = gn_step_sparse(st2)
+    assert r1["energy_after"] == r2["energy_after"] and r1["accepted"]
+    assert torch.equal(X1, st2.layers.X)
+    assert r1["energy_after"] < r1["energy_before"]
+
+
+def test_tma_and_cooperative_paths_identical():
+    """Same problem through the TMA pipeline and the cooperative-load path
+    (LS_NO_TMA): bitwise identical operator, gradient and GN step."""
+    from paper_1908_01961_b200 import _device
+    from paper_1908_01961_b200.energy import assemble_blocks
+    from paper_1908_01961_b200.solver import gn_step_sparse
+    clip = _clip(72, 136, 5, n=1, seed=6)
+    outs = []
+    for no_tma in (False, True):
+        _device.clear_cache()
+        if no_tma:
+            os.environ["LS_NO_TMA"] = "1"
+        try:
+            st = _state(clip)
+            blocks = assemble_blocks(st.frame, st.palette, st.layers, st.aux, st.weights)
+            p = torch.linspace(-1, 1, st.layers.X.numel(), device="cuda").reshape(st.layers.X.shape)
+            Ap = blocks.apply_normal(p)
+            b, d = blocks.gradient_and_diag()
+            e = blocks.energies()
+            rec = gn_step_sparse(st)
+            outs.append((Ap, b, d, e, rec["energy_after"], st.layers.X.clone()))
+        finally:
+            os.environ.pop("LS_NO_TMA", None)
+            _device.clear_cache()
+    (Ap0, b0, d0, e0, ea0, X0), (Ap1, b1, d1, e1, ea1, X1) = outs
+    assert torch.equal(Ap0, Ap1) and torch.equal(b0, b1) and torch.equal(d0, d1)
+    assert e0 == e1 and ea0 == ea1
+    assert torch.equal(X0, X1)
+
+
+@pytest.mark.parametrize("K", [1, 12])
+def test_extreme_K_gn_step_matches_oracle(K):
+    from paper_1908_01961_b200.solver import gn_step_sparse
+    clip = _clip(40, 52, K, n=1, seed=7)
+    st = _state(clip)
+    r0 = st.layers.r.double().cpu().numpy()
+    T0 = st.layers.T.double().cpu().numpy()
+    rec = gn_step_sparse(st)
+    img = clip.frames[0].double().numpy()
+    ids = st.aux.cluster_ids.cpu().numpy()
+    ost = O.State(image=img, colors=clip.colors, r=r0, T=T0, aux=O.build_aux(img, ids, 0),
+                  weights=O.Weights(), config=O.Config())
+    orec = O.gn_step_sparse(ost)
+    assert rec["accepted"] == orec["accepted"]
+    assert np.isclose(rec["energy_before"], orec["energy_before"], rtol=1e-5)
+    assert np.isclose(rec["energy_after"], orec["energy_after"], rtol=1e-4)
+    assert np.max(np.abs(st.layers.T.double().cpu().numpy() - ost.T)) < 1e-3
+
+
+def test_k0_direct_layer_only():
+    """K = 0 (white illuminant only), as test_solver.py:72-100 uses."""
+    from paper_1908_01961_b200.energy import ConsistencySamples, EnergyAux, EnergyWeights, LayerStack
+    from paper_1908_01961_b200.imaging import Frame, chromaticity
+    from paper_1908_01961_b200.energy import chroma_edge_weights, sample_consistency
+    from paper_1908_01961_b200.palette import BaseColorPalette
+    from paper_1908_01961_b200.solver import SolveConfig, SolverState, gn_step_sparse
+    h = w = 8
+    rng = np.random.default_rng(3)
+    image = np.clip(rng.uniform(0.2, 0.9, size=(h, w, 3)), 0, 1).astype(np.float32)
+    frame = Frame(torch.as_tensor(image, device="cuda"))
+    R = np.full((h, w, 3), 0.7, dtype=np.float32)
+    layers = LayerStack(torch.as_tensor(np.log(R), device="cuda"),
+                        torch.full((h, w, 1), 0.1, device="cuda"))
+    ch = chromaticity(frame)
+    aux = EnergyAux(edge_weights=chroma_edge_weights(ch), samples=sample_consistency(ch, None, 0),
+                    r_cluster_log=torch.as_tensor(np.log(R), device="cuda"))
+    weights = EnergyWeights(lambda_clustering=1e12, lambda_r_sparsity=0, lambda_r_consistency=0,
+                            lambda_monochrome=0, lambda_i_sparsity=0, lambda_smoothness=0, lambda_non_neg=0)
+    st = SolverState(frame=frame, palette=BaseColorPalette(colors=np.zeros((0, 3))), layers=layers,
+                     aux=aux, weights=weights, config=SolveConfig(pcg_iterations=16))
+    gn_step_sparse(st)
+    S0 = 0.1
+    num = (R * (image - R * S0)).sum(axis=2)
+    den = (R ** 2).sum(axis=2)
+    expected = 0.1 + num / den
+    assert np.max(np.abs(st.layers.T[:, :, 0].cpu().numpy() - expected)) < 1e-5
+
+
+def test_nondefault_weights_match_oracle():
+    from paper_1908_01961_b200.energy import EnergyWeights, assemble_blocks, to_reference_vector
+    clip = _clip(36, 44, 3, n=1, seed=8)
+    w = EnergyWeights(p=0.8, chroma_reg="identity", lambda_r_consistency=25.0, eps_irls=0.05)
+    st = _state(clip, weights=w)
+    blocks = assemble_blocks(st.frame, st.palette, st.layers, st.aux, w)
+    img = clip.frames[0].double().numpy()
+    ids = st.aux.cluster_ids.cpu().numpy()
+    ow = O.Weights(p=0.8, chroma_reg="identity", lambda_r_consistency=25.0, eps_irls=0.05)
+    osys = O.FrozenSystem(img, clip.colors, st.layers.r.double().cpu().numpy(),
+                          st.layers.T.double().cpu().numpy(), O.build_aux(img, ids, 0), ow)
+    e = blocks.energies()
+    et = osys.terms(osys.r0, osys.T0)
+    for k in O.TERM_NAMES:
+        assert np.isclose(e[k], et[k], rtol=1e-5, atol=1e-9), k
+    b, d = blocks.gradient_and_diag()
+    ob, od = osys.grad_diag()
+    bv = to_reference_vector(b).cpu().numpy()
+    assert np.max(np.abs(bv - ob)) / np.max(np.abs(ob)) < 1e-5
+    from paper_1908_01961_b200.energy import refine_normal_system
+    A, rhs = refine_normal_system(st.frame, st.layers, st.palette, w, cluster_ids=st.aux.cluster_ids)
+    oA, orhs = O.refine_normal_system(img, osys.r0, osys.T0, clip.colors, ow, ids)
+    assert np.max(np.abs(A - oA)) / np.max(np.abs(oA)) < 1e-9
