@@ -119,6 +119,10 @@ LS_API int ls_set_image(ls_ctx* ctx, const float* image_hwc);
 LS_API int ls_sample_consistency(ls_ctx* ctx, const double* chroma_planes, const double* prev_chroma_planes,
                           uint64_t state_hi, uint64_t state_lo,
                           uint64_t inc_hi, uint64_t inc_lo, int64_t* n_pairs_out);
+/* Counts of the installed partner rows (synchronises the stream): pairs,
+ * temporal pairs, adjacency entries.  ls_sample_consistency itself does not
+ * synchronise and reports n_pairs_out = -1. */
+LS_API int ls_pair_count(ls_ctx* ctx, int64_t* n_pairs, int64_t* n_temporal, int64_t* n_entries);
 /* Explicit partner rows (ConsistencySamples, energy.py:139-151); src/dst
  * flat pixel indices (int64), temporal as uint8, weight may be NULL (all 1).
  * Partners must lie in the 15x15 window (|dx|,|dy| <= 7) -> else LS_ERR_ARG. */

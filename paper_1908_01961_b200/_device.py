@@ -125,6 +125,12 @@ class DeviceSolver:
         self._chk(self.lib.ls_get_chroma(self.ctx, L.dptr(out)))
         return out
 
+    def pair_count(self) -> int:
+        n, t, e = C.c_int64(), C.c_int64(), C.c_int64()
+        self._enter()
+        self._chk(self.lib.ls_pair_count(self.ctx, C.byref(n), C.byref(t), C.byref(e)))
+        return int(n.value)
+
     def sample(self, seed: int, chroma_planes=None, prev_chroma_planes=None) -> int:
         st = np.random.PCG64(int(seed)).state["state"]
         s, inc = int(st["state"]), int(st["inc"])
@@ -138,7 +144,9 @@ class DeviceSolver:
         self.sample_gen += 1
         return int(n.value)
 
-    def get_pairs(self, n: int):
+    def get_pairs(self, n: int | None = None):
+        if n is None or n < 0:
+            n = self.pair_count()
         src = torch.empty(n, dtype=torch.int64, device=self.device)
         dst = torch.empty(n, dtype=torch.int64, device=self.device)
         tmp = torch.empty(n, dtype=torch.uint8, device=self.device)

@@ -66,6 +66,7 @@ SIGNATURES = {
     "ls_set_image": [P, P],
     "ls_sample_consistency": [P, P, P, U64, U64, U64, U64, C.POINTER(I64)],
     "ls_set_pairs": [P, I64, P, P, P, P],
+    "ls_pair_count": [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)],
     "ls_get_pairs": [P, P, P, P],
     "ls_set_edge": [P, P],
     "ls_set_prev_r": [P, P],

@@ -71,17 +71,17 @@ struct U32Stream {
   }
 };
 
-__device__ __forceinline__ unsigned long long shifted_pos(const SampleParams& P, unsigned long long j) {
+__device__ __forceinline__ unsigned long long shifted_pos(const SampleState* S, int nz, unsigned long long j) {
   unsigned long long s = j;
-  for (int t = 0; t < P.nz; ++t)
-    if ((unsigned long long)P.z[t] < s) ++s;
+  for (int t = 0; t < nz; ++t)
+    if ((unsigned long long)S->z[t] < s) ++s;
     else break;
   return s;
 }
 
-__device__ __forceinline__ bool known_zero(const SampleParams& P, unsigned long long pos) {
-  for (int t = 0; t < P.nz; ++t)
-    if ((unsigned long long)P.z[t] == pos) return true;
+__device__ __forceinline__ bool known_zero(const SampleState* S, int nz, unsigned long long pos) {
+  for (int t = 0; t < nz; ++t)
+    if ((unsigned long long)S->z[t] == pos) return true;
   return false;
 }
 
@@ -143,57 +143,126 @@ __global__ void k_edge(const double* __restrict__ ch, int H, int W, float* __res
 }
 
 // ---- consistency sampler (energy.py:154-187) --------------------------------
-// codes[4p+s] = -1 (dropped) or offset code | temporal<<8 for pixel p, slot s.
-__global__ void k_sample(SampleParams P, const double* __restrict__ ch, const double* __restrict__ pch, int H,
-                         int W, int16_t* __restrict__ codes, int32_t* __restrict__ out_cnt,
-                         int32_t* __restrict__ in_cnt, unsigned long long* new_zero) {
+// codes[4p+s] = -1 (dropped) or make_ent(...) for pixel p, slot s.
+// Each thread draws kSamplePix consecutive pixels: one PCG64 jump per
+// section (dx, dy, temporal) then sequential u32 reads, so the 128-bit
+// jump-ahead is amortised over 4*kSamplePix draws.  Draws are kept packed
+// (4-bit dx/dy, 1-bit temporal) until the gate.
+// Lemire rejections (u32 == 0 in the range-15 sections) shift the rest of the
+// stream by one word: positions already known are in S.z; a new one is
+// reported through S.new_zero and the pass is repeated on the device
+// (k_sample_fix / redo) -- no host round trip.
+constexpr int kSamplePix = 8;
+
+__global__ void k_sample(SampleParams P, const SampleState* __restrict__ Sg, const double* __restrict__ ch,
+                         const double* __restrict__ pch, int H, int W, int16_t* __restrict__ codes,
+                         int32_t* __restrict__ out_cnt, int32_t* __restrict__ in_cnt, SampleState* Sw) {
+  if (!Sg->redo) return;
+  const int nz = Sg->nz;
   const int N = H * W;
   const u128 s0 = mk128(P.st_hi, P.st_lo), inc = mk128(P.inc_hi, P.inc_lo);
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
-    const int x = p % W, y = p / W;
-    int dxv[4], dyv[4], tv[4] = {0, 0, 0, 0};
+  const int nthreads = (N + kSamplePix - 1) / kSamplePix;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nthreads; t += gridDim.x * blockDim.x) {
+    const int p0 = t * kSamplePix;
+    const int np = min(kSamplePix, N - p0);
+    uint32_t dxp[kSamplePix / 2], dyp[kSamplePix / 2], tp = 0;   // 8 nibbles per word
+#pragma unroll
+    for (int w = 0; w < kSamplePix / 2; ++w) dxp[w] = dyp[w] = 0u;
     U32Stream st;
     // dx then dy: rng.integers(-7, 8, size=(n, 4)) -> Lemire on range 15,
     // reject iff (u * 15) mod 2^32 < (2^32 mod 15) = 1, i.e. u == 0
     for (int sec = 0; sec < 2; ++sec) {
-      unsigned long long pos = shifted_pos(P, (unsigned long long)sec * 4ULL * N + 4ULL * p);
+      unsigned long long pos = shifted_pos(Sg, nz, (unsigned long long)sec * 4ULL * N + 4ULL * p0);
       st.seek(s0, inc, pos);
-      int got = 0;
-      while (got < 4) {
-        const unsigned u = st.next();
-        if (u == 0u) {
-          if (!known_zero(P, pos)) atomicMin(new_zero, pos);
+#pragma unroll
+      for (int d = 0; d < 4 * kSamplePix; ++d) {
+        if (d >= 4 * np) break;
+        unsigned u = st.next();
+        while (u == 0u) {
+          if (!known_zero(Sg, nz, pos)) atomicMin(&Sw->new_zero, pos);
           ++pos;
-          continue;
+          u = st.next();
         }
         ++pos;
-        const int v = (int)(((unsigned long long)u * 15ULL) >> 32) - kHalf;
-        if (sec == 0) dxv[got] = v; else dyv[got] = v;
-        ++got;
+        const uint32_t v = (uint32_t)(((unsigned long long)u * 15ULL) >> 32);   // 0..14 = offset + 7
+        if (sec == 0) dxp[d >> 3] |= v << (4 * (d & 7));
+        else dyp[d >> 3] |= v << (4 * (d & 7));
       }
     }
     if (P.has_prev) {   // rng.integers(0, 2): Lemire threshold 0, no rejection
-      st.seek(s0, inc, shifted_pos(P, 8ULL * N + 4ULL * p));
-      for (int k = 0; k < 4; ++k) tv[k] = (int)(((unsigned long long)st.next() * 2ULL) >> 32);
-    }
-    const double c0 = ch[p], c1 = ch[N + p];
-    int cnt = 0;
-    for (int k = 0; k < 4; ++k) {
-      const int px = clampi(x + dxv[k], 0, W - 1), py = clampi(y + dyv[k], 0, H - 1);
-      const int q = py * W + px;
-      const double* src = tv[k] ? pch : ch;
-      const double dist = norm2d(__dsub_rn(c0, src[q]), __dsub_rn(c1, src[N + q]));
-      const bool keep = (dist < 0.05) && (tv[k] || q != p);
-      int16_t code = -1;
-      if (keep) {
-        code = (int16_t)make_ent(py - y, px - x, tv[k] != 0, false);
-        ++cnt;
-        if (!tv[k]) atomicAdd(in_cnt + q, 1);
+      st.seek(s0, inc, shifted_pos(Sg, nz, 8ULL * N + 4ULL * p0));
+#pragma unroll
+      for (int d = 0; d < 4 * kSamplePix; ++d) {
+        if (d >= 4 * np) break;
+        tp |= (uint32_t)(((unsigned long long)st.next() * 2ULL) >> 32) << d;
       }
-      codes[4 * p + k] = code;
     }
-    out_cnt[p] = cnt;
+#pragma unroll
+    for (int pp = 0; pp < kSamplePix; ++pp) {
+      if (pp >= np) break;
+      const int p = p0 + pp;
+      const int x = p % W, y = p / W;
+      const double c0 = ch[p], c1 = ch[N + p];
+      int cnt = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int d = 4 * pp + k;
+        const int dx = (int)((dxp[d >> 3] >> (4 * (d & 7))) & 15u) - kHalf;
+        const int dy = (int)((dyp[d >> 3] >> (4 * (d & 7))) & 15u) - kHalf;
+        const bool tk = (tp >> d) & 1u;
+        const int px = clampi(x + dx, 0, W - 1), py = clampi(y + dy, 0, H - 1);
+        const int q = py * W + px;
+        const double* src = tk ? pch : ch;
+        const double dist = norm2d(__dsub_rn(c0, src[q]), __dsub_rn(c1, src[N + q]));
+        const bool keep = (dist < 0.05) && (tk || q != p);
+        int16_t code = -1;
+        if (keep) {
+          code = (int16_t)make_ent(py - y, px - x, tk, false);
+          ++cnt;
+          if (!tk) atomicAdd(in_cnt + q, 1);
+        }
+        codes[4 * p + k] = code;
+      }
+      out_cnt[p] = cnt;
+    }
   }
+}
+
+__global__ void k_sample_init(SampleState* S) {
+  S->nz = 0;
+  S->redo = 1;
+  S->error = 0;
+  S->new_zero = ~0ULL;
+}
+
+// clears the adjacency counters before a (re)draw pass
+__global__ void k_sample_zero(const SampleState* S, int n, int32_t* a, int32_t* b) {
+  if (!S->redo) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = b[i] = 0;
+}
+
+// after a pass: record a newly found rejection (sorted) and request a redo,
+// or finish
+__global__ void k_sample_fix(SampleState* S, int last_pass) {
+  if (!S->redo) return;
+  const unsigned long long z = S->new_zero;
+  if (z == ~0ULL) {
+    S->redo = 0;
+    return;
+  }
+  if (last_pass || S->nz >= kMaxRejections) {
+    S->error = 1;
+    S->redo = 0;
+    return;
+  }
+  int at = S->nz;
+  while (at > 0 && (unsigned long long)S->z[at - 1] > z) {
+    S->z[at] = S->z[at - 1];
+    --at;
+  }
+  S->z[at] = (long long)z;
+  S->nz += 1;
+  S->new_zero = ~0ULL;
 }
 
 __global__ void k_degree(int N, const int32_t* a, const int32_t* b, int32_t* deg) {
@@ -301,13 +370,13 @@ __global__ void k_pairs_from_samples(const int16_t* __restrict__ codes, int H, i
 
 // ---- segmentation (palette.py:195-224) --------------------------------------
 __global__ void k_segment_raw(const float* __restrict__ img, const double* __restrict__ ch, int N, int K,
-                              const double* __restrict__ pal, int32_t* ids_raw, int32_t* key, int* first_valid) {
+                              const PalChroma pal, int32_t* ids_raw, int32_t* key, int* first_valid) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     const double c0 = ch[i], c1 = ch[N + i];
     int best = 0;
     double bd = 0.0;
     for (int k = 0; k < K; ++k) {
-      const double d = norm2d(__dsub_rn(c0, pal[2 * k]), __dsub_rn(c1, pal[2 * k + 1]));
+      const double d = norm2d(__dsub_rn(c0, pal.c[2 * k]), __dsub_rn(c1, pal.c[2 * k + 1]));
       if (k == 0 || d < bd) { bd = d; best = k; }    // argmin: first minimum wins
     }
     ids_raw[i] = best + 1;
@@ -331,12 +400,12 @@ __global__ void k_segment_final(int N, const int32_t* __restrict__ ids_raw, cons
 
 // ---- first-frame initialisation (solver.py:295-308) ------------------------
 __global__ void k_initialize(const float* __restrict__ img, const int32_t* __restrict__ ids, int N, int NT,
-                             const double* __restrict__ colors, float* __restrict__ X) {
+                             const PalColors colors, float* __restrict__ X) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     const int id = ids[i] - 1;
     double ratio_sum = 0.0;
     for (int c = 0; c < 3; ++c) {
-      const double rc = colors[3 * id + c];
+      const double rc = colors.c[3 * id + c];
       const double fl = rc > 1e-4 ? rc : 1e-4;
       X[(size_t)c * N + i] = (float)log(fl);
       ratio_sum += (double)img[(size_t)c * N + i] / fl;
@@ -372,10 +441,17 @@ void launch_image(cudaStream_t s, const float* hwc, int N, float* img, double* c
 void launch_edge(cudaStream_t s, const double* chroma, int H, int W, float* edge) {
   k_edge<<<grid_for((int64_t)H * W), 256, 0, s>>>(chroma, H, W, edge);
 }
-void launch_sample(cudaStream_t s, const SampleParams& P, const double* chroma, const double* prev_chroma, int H,
-                   int W, int16_t* codes, int32_t* out_cnt, int32_t* in_cnt, unsigned long long* new_zero) {
-  k_sample<<<grid_for((int64_t)H * W, 128), 128, 0, s>>>(P, chroma, prev_chroma, H, W, codes, out_cnt, in_cnt,
-                                                        new_zero);
+void launch_sample(cudaStream_t s, const SampleParams& P, SampleState* S, const double* chroma,
+                   const double* prev_chroma, int H, int W, int16_t* codes, int32_t* out_cnt, int32_t* in_cnt,
+                   int passes) {
+  const int N = H * W;
+  const int nthreads = (N + kSamplePix - 1) / kSamplePix;
+  k_sample_init<<<1, 1, 0, s>>>(S);
+  for (int pass = 0; pass < passes; ++pass) {
+    k_sample_zero<<<grid_for(N + 1), 256, 0, s>>>(S, N + 1, out_cnt, in_cnt);
+    k_sample<<<grid_for(nthreads, 128), 128, 0, s>>>(P, S, chroma, prev_chroma, H, W, codes, out_cnt, in_cnt, S);
+    k_sample_fix<<<1, 1, 0, s>>>(S, pass == passes - 1);
+  }
 }
 void launch_pairs_count(cudaStream_t s, int64_t n, const int64_t* src, const int64_t* dst, const uint8_t* temporal,
                         int H, int W, int32_t* out_cnt, int32_t* in_cnt, int* bad) {
@@ -400,7 +476,7 @@ void launch_pairs_from_samples(cudaStream_t s, const int16_t* codes, int H, int 
                                int64_t* dst, uint8_t* temporal) {
   k_pairs_from_samples<<<grid_for((int64_t)H * W), 256, 0, s>>>(codes, H, W, off, src, dst, temporal);
 }
-void launch_segment_raw(cudaStream_t s, const float* img, const double* chroma, int N, int K, const double* pal,
+void launch_segment_raw(cudaStream_t s, const float* img, const double* chroma, int N, int K, const PalChroma& pal,
                         int32_t* ids_raw, int32_t* key, int* first_valid) {
   k_segment_raw<<<grid_for(N), 256, 0, s>>>(img, chroma, N, K, pal, ids_raw, key, first_valid);
 }
@@ -408,7 +484,7 @@ void launch_segment_final(cudaStream_t s, int N, const int32_t* ids_raw, const i
                           int32_t* ids) {
   k_segment_final<<<grid_for(N), 256, 0, s>>>(N, ids_raw, last, first_valid, ids);
 }
-void launch_initialize(cudaStream_t s, const float* img, const int32_t* ids, int N, int NT, const double* colors,
+void launch_initialize(cudaStream_t s, const float* img, const int32_t* ids, int N, int NT, const PalColors& colors,
                        float* X) {
   k_initialize<<<grid_for(N), 256, 0, s>>>(img, ids, N, NT, colors, X);
 }

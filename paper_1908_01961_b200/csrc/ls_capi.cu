@@ -117,7 +117,8 @@ struct ls_ctx {
   int16_t* codes = nullptr;
   int32_t *out_cnt = nullptr, *in_cnt = nullptr, *deg = nullptr, *fill = nullptr, *pair_off = nullptr;
   int* small_i = nullptr;                     // [0] bad flag, [1] temporal count, [2] first_valid
-  unsigned long long* zero_flag = nullptr;
+  SampleState* sstate = nullptr;          // device-side sampler rejection bookkeeping
+  bool sampled_counts_known = true;
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   int32_t *seg_raw = nullptr, *seg_key = nullptr, *seg_last = nullptr;
@@ -194,12 +195,20 @@ static Frame frame_of(const ls_ctx* c) {
   return f;
 }
 
+extern "C" int ls_pair_count(ls_ctx* c, int64_t* n_pairs, int64_t* n_temporal, int64_t* n_entries);
+
 static int check_ready(ls_ctx* c) {
   LS_ARG(c != nullptr, "null context");
   LS_ARG(c->has_image, "no frame image set (ls_set_image)");
   LS_ARG(c->has_pairs, "no consistency partners (ls_sample_consistency / ls_set_pairs)");
   LS_ARG(c->has_ids || c->has_anchor, "EnergyAux needs cluster_ids or r_cluster_log");
-  LS_ARG(c->n_temporal == 0 || c->has_prev_r, "temporal partners need the previous frame's reflectance");
+  if (c->n_temporal != 0 && !c->has_prev_r) {
+    if (c->n_temporal < 0) {
+      int rc = ls_pair_count(c, nullptr, nullptr, nullptr);
+      if (rc) return rc;
+    }
+    LS_ARG(c->n_temporal == 0, "temporal partners need the previous frame's reflectance");
+  }
   return LS_OK;
 }
 
@@ -274,7 +283,7 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   A_(dalloc(c, &c->fill, (size_t)N + 1));
   A_(dalloc(c, &c->pair_off, (size_t)N + 1));
   A_(dalloc(c, &c->small_i, 8));
-  A_(dalloc(c, &c->zero_flag, 1));
+  A_(dalloc(c, &c->sstate, 1));
   A_(dalloc(c, &c->seg_raw, (size_t)N));
   A_(dalloc(c, &c->seg_key, (size_t)N));
   A_(dalloc(c, &c->seg_last, (size_t)N));
@@ -332,6 +341,10 @@ int ls_profile_read(ls_ctx* c, double* out) {
     out[2 * i + 1] = c->prof.ms[i];
   }
   out[2 * PC_N] = (double)c->launches;
+  if (c->has_pairs && !c->sampled_counts_known) {
+    const int rc = ls_pair_count(c, nullptr, nullptr, nullptr);
+    if (rc) return rc;
+  }
   out[2 * PC_N + 1] = (double)c->n_entries;
   out[2 * PC_N + 2] = (double)c->n_pairs;
   return LS_OK;
@@ -450,8 +463,8 @@ int ls_edge_from_chroma(const double* chroma, int H, int W, float* edge, void* s
   return LS_OK;
 }
 
-int ls_sample_consistency(ls_ctx* c, const double* chroma, const double* prev_chroma, uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi,
-                          uint64_t inc_lo, int64_t* n_pairs_out) {
+int ls_sample_consistency(ls_ctx* c, const double* chroma, const double* prev_chroma, uint64_t st_hi, uint64_t st_lo,
+                          uint64_t inc_hi, uint64_t inc_lo, int64_t* n_pairs_out) {
   LS_ARG(c && (chroma || c->has_image), "ls_set_image first");
   LS_CK(cudaSetDevice(c->dev));
   const int N = c->N;
@@ -463,49 +476,54 @@ int ls_sample_consistency(ls_ctx* c, const double* chroma, const double* prev_ch
   P.inc_hi = inc_hi;
   P.inc_lo = inc_lo;
   P.has_prev = prev_chroma ? 1 : 0;
-  for (;;) {
-    LS_CK(cudaMemsetAsync(c->out_cnt, 0, sizeof(int32_t) * (N + 1), c->stream));
-    LS_CK(cudaMemsetAsync(c->in_cnt, 0, sizeof(int32_t) * (N + 1), c->stream));
-    LS_CK(cudaMemsetAsync(c->zero_flag, 0xff, sizeof(unsigned long long), c->stream));
-    launch_sample(c->stream, P, cur, prev_chroma, c->H, c->W, c->codes, c->out_cnt, c->in_cnt,
-                  c->zero_flag);
-    c->launches += 1;
-    LS_CK(cudaGetLastError());
-    unsigned long long z = 0;
-    LS_CK(cudaMemcpyAsync(&z, c->zero_flag, sizeof(z), cudaMemcpyDeviceToHost, c->stream));
-    LS_CK(cudaStreamSynchronize(c->stream));
-    if (z == ~0ULL) break;
-    // a Lemire rejection (u32 == 0, p = 2^-32 per draw) shifts the stream
-    LS_ARG(P.nz < 8, "too many PCG64 rejections in one frame");
-    int at = P.nz;
-    while (at > 0 && (unsigned long long)P.z[at - 1] > z) {
-      P.z[at] = P.z[at - 1];
-      --at;
-    }
-    P.z[at] = (long long)z;
-    ++P.nz;
-  }
-  int64_t total = 0;
-  int rc = build_rows(c, &total);
-  if (rc != LS_OK) return rc;
+  // draws + device-side rejection re-passes: no host synchronisation
+  launch_sample(c->stream, P, c->sstate, cur, prev_chroma, c->H, c->W, c->codes, c->out_cnt, c->in_cnt,
+                kSamplePasses);
+  launch_degree(c->stream, N, c->out_cnt, c->in_cnt, c->deg);
+  LS_CK(cudaMemsetAsync(c->deg + N, 0, sizeof(int32_t), c->stream));
+  size_t bytes = c->cub_bytes;
+  LS_CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->deg, c->row_ptr, N + 1, c->stream));
   LS_CK(cudaMemsetAsync(c->fill, 0, sizeof(int32_t) * N, c->stream));
   launch_fill_from_samples(c->stream, c->codes, c->H, c->W, c->row_ptr, c->fill, c->ent, c->key);
   launch_sort_rows(c->stream, N, c->row_ptr, c->ent, c->key, nullptr);
-  c->launches += 6;   // degree, 2 scans, fill, sort (+ scan kernels counted as 1 each)
-  // pair offsets (src-major, slot order) for ls_get_pairs and the pair count
-  size_t bytes = c->cub_bytes;
+  // pair offsets (src-major, slot order) for ls_get_pairs / ls_pair_count
+  bytes = c->cub_bytes;
   LS_CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->out_cnt, c->pair_off, N + 1, c->stream));
-  int32_t np = 0;
-  LS_CK(cudaMemcpyAsync(&np, c->pair_off + N, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
-  LS_CK(cudaStreamSynchronize(c->stream));
   LS_CK(cudaGetLastError());
-  c->n_pairs = np;
-  c->n_entries = total;
-  c->n_temporal = P.has_prev ? (int)(np - (total - np)) : 0;   // out entries minus spatial incoming ones
+  c->launches += 1 + 3 * kSamplePasses + 6;
+  c->n_pairs = -1;                       // resolved lazily by ls_pair_count
+  c->n_entries = -1;
+  c->n_temporal = P.has_prev ? -1 : 0;
+  c->sampled_counts_known = false;
   c->has_ent_w = false;
   c->has_pairs = true;
   c->pairs_from_sampler = true;
-  if (n_pairs_out) *n_pairs_out = np;
+  if (n_pairs_out) *n_pairs_out = -1;
+  return LS_OK;
+}
+
+// pair / entry / temporal counts of the sampled adjacency (synchronises)
+int ls_pair_count(ls_ctx* c, int64_t* n_pairs, int64_t* n_temporal, int64_t* n_entries) {
+  LS_ARG(c && c->has_pairs, "no consistency partners");
+  if (!c->sampled_counts_known) {
+    int32_t v[2] = {0, 0};
+    int err = 0;
+    LS_CK(cudaMemcpyAsync(&v[0], c->pair_off + c->N, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    LS_CK(cudaMemcpyAsync(&v[1], c->row_ptr + c->N, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    LS_CK(cudaMemcpyAsync(&err, &c->sstate->error, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    LS_CK(cudaStreamSynchronize(c->stream));
+    if (err) {
+      g_err = "consistency sampler: too many PCG64 rejections in one frame";
+      return LS_ERR_CUDA;
+    }
+    c->n_pairs = v[0];
+    c->n_entries = v[1];
+    c->n_temporal = (c->n_temporal != 0) ? (int)(v[0] - (v[1] - v[0])) : 0;
+    c->sampled_counts_known = true;
+  }
+  if (n_pairs) *n_pairs = c->n_pairs;
+  if (n_temporal) *n_temporal = c->n_temporal;
+  if (n_entries) *n_entries = c->n_entries;
   return LS_OK;
 }
 
@@ -549,6 +567,7 @@ int ls_set_pairs(ls_ctx* c, int64_t n, const int64_t* src, const int64_t* dst, c
   launch_sort_rows(c->stream, N, c->row_ptr, c->ent, c->key, weight ? c->ent_w : nullptr);
   LS_CK(cudaGetLastError());
   c->n_pairs = n;
+  c->sampled_counts_known = true;
   c->n_entries = total;
   c->n_temporal = (int)(n - (total - n));
   c->has_ent_w = weight != nullptr;
@@ -561,31 +580,31 @@ int ls_segment(ls_ctx* c, const double* colors, int32_t* ids_out) {
   LS_ARG(c && c->has_image && colors && ids_out, "bad arguments");
   LS_ARG(c->K >= 1, "segment needs K >= 1");
   const int N = c->N, K = c->K;
-  double pc[2 * LS_MAX_K];
+  PalChroma pc;
+  std::memset(&pc, 0, sizeof(pc));
   for (int k = 0; k < K; ++k) {   // chroma_of_color (imaging.py:174-180)
     const double s = (colors[3 * k] + colors[3 * k + 1]) + colors[3 * k + 2];
-    pc[2 * k] = s > 1e-12 ? colors[3 * k] / s : 1.0 / 3.0;
-    pc[2 * k + 1] = s > 1e-12 ? colors[3 * k + 1] / s : 1.0 / 3.0;
+    pc.c[2 * k] = s > 1e-12 ? colors[3 * k] / s : 1.0 / 3.0;
+    pc.c[2 * k + 1] = s > 1e-12 ? colors[3 * k + 1] / s : 1.0 / 3.0;
   }
-  LS_CK(cudaMemcpyAsync(c->pal_chroma, pc, sizeof(double) * 2 * K, cudaMemcpyHostToDevice, c->stream));
   launch_set_i32(c->stream, c->small_i + 2, 1, N);
-  launch_segment_raw(c->stream, c->img, c->chroma, N, K, c->pal_chroma, c->seg_raw, c->seg_key, c->small_i + 2);
+  launch_segment_raw(c->stream, c->img, c->chroma, N, K, pc, c->seg_raw, c->seg_key, c->small_i + 2);
   size_t bytes = c->cub_bytes;
   LS_CK(cub::DeviceScan::InclusiveScan(c->cub_tmp, bytes, c->seg_key, c->seg_last, MaxOp(), N, c->stream));
   launch_segment_final(c->stream, N, c->seg_raw, c->seg_last, c->small_i + 2, ids_out);
   c->launches += 4;
   LS_CK(cudaGetLastError());
-  // pageable source: wait before the host array goes out of scope
-  LS_CK(cudaStreamSynchronize(c->stream));
   return LS_OK;
 }
 
 int ls_initialize(ls_ctx* c, const double* colors, const int32_t* ids, float* X) {
   LS_ARG(c && c->has_image && colors && ids && X, "bad arguments");
-  LS_CK(cudaMemcpyAsync(c->colors_dev, colors, sizeof(double) * 3 * c->K, cudaMemcpyHostToDevice, c->stream));
-  launch_initialize(c->stream, c->img, ids, c->N, c->NT, c->colors_dev, X);
+  PalColors pc;
+  std::memset(&pc, 0, sizeof(pc));
+  for (int i = 0; i < 3 * c->K; ++i) pc.c[i] = colors[i];
+  launch_initialize(c->stream, c->img, ids, c->N, c->NT, pc, X);
+  c->launches += 1;
   LS_CK(cudaGetLastError());
-  LS_CK(cudaStreamSynchronize(c->stream));
   return LS_OK;
 }
 
@@ -771,8 +790,14 @@ int ls_gn_step(ls_ctx* c, const double* colors, const float* X, float* X_out, ls
     c->launches += 1;
     LS_CK(cudaGetLastError());
     LS_CK(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
+    if (h == 0 && !c->sampled_counts_known)
+      LS_CK(cudaMemcpyAsync(c->host_buf, &c->sstate->error, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     LS_CK(cudaStreamSynchronize(c->stream));
     prof_harvest(c);
+    if (h == 0 && !c->sampled_counts_known && *reinterpret_cast<int*>(c->host_buf)) {
+      g_err = "consistency sampler: too many PCG64 rejections in one frame";
+      return LS_ERR_CUDA;
+    }
     const Scalars& s = *c->sc_host;
     if (h == 0) {
       std::memcpy(rec->terms_before, s.terms0, sizeof(rec->terms_before));

@@ -60,16 +60,22 @@ int update_grid_limit();
 struct SampleParams {
   unsigned long long st_hi, st_lo, inc_hi, inc_lo;
   int has_prev;
-  int nz;                       // known rejected stream positions
-  long long z[8];
 };
+constexpr int kMaxRejections = 16;
+// device-resident rejection bookkeeping of the partner sampler
+struct SampleState {
+  int nz, redo, error, pad;
+  unsigned long long new_zero;
+  long long z[kMaxRejections];   // rejected u32 stream positions, ascending
+};
+constexpr int kSamplePasses = 4;
 void launch_pack_hwc(cudaStream_t s, const float* hwc, int C, int N, float* planes);
 void launch_unpack_hwc(cudaStream_t s, const float* planes, int C, int N, float* hwc);
 void launch_image(cudaStream_t s, const float* hwc, int N, float* img_planes, double* chroma);
 void launch_edge(cudaStream_t s, const double* chroma, int H, int W, float* edge);
-void launch_sample(cudaStream_t s, const SampleParams& P, const double* chroma, const double* prev_chroma,
-                   int H, int W, int16_t* codes, int32_t* out_cnt, int32_t* in_cnt,
-                   unsigned long long* new_zero);
+void launch_sample(cudaStream_t s, const SampleParams& P, SampleState* S, const double* chroma,
+                   const double* prev_chroma, int H, int W, int16_t* codes, int32_t* out_cnt, int32_t* in_cnt,
+                   int passes);
 void launch_pairs_count(cudaStream_t s, int64_t n, const int64_t* src, const int64_t* dst,
                         const uint8_t* temporal, int H, int W, int32_t* out_cnt, int32_t* in_cnt, int* bad);
 void launch_degree(cudaStream_t s, int N, const int32_t* out_cnt, const int32_t* in_cnt, int32_t* deg);
@@ -82,13 +88,14 @@ void launch_sort_rows(cudaStream_t s, int N, const int32_t* row_ptr, uint16_t* e
                       float* ent_w);
 void launch_pairs_from_samples(cudaStream_t s, const int16_t* codes, int H, int W, const int32_t* pair_off,
                                int64_t* src, int64_t* dst, uint8_t* temporal);
+struct PalChroma { double c[2 * (kMaxNT - 1)]; };   // palette chromas, by value
+struct PalColors { double c[3 * (kMaxNT - 1)]; };   // palette colors, by value
 void launch_segment_raw(cudaStream_t s, const float* img, const double* chroma, int N, int K,
-                        const double* pal_chroma /*device K*2*/, int32_t* ids_raw, int32_t* key,
-                        int* first_valid);
+                        const PalChroma& pal, int32_t* ids_raw, int32_t* key, int* first_valid);
 void launch_segment_final(cudaStream_t s, int N, const int32_t* ids_raw, const int32_t* last,
                           const int* first_valid, int32_t* ids);
 void launch_initialize(cudaStream_t s, const float* img, const int32_t* ids, int N, int NT,
-                       const double* colors /*device K*3*/, float* X);
+                       const PalColors& colors, float* X);
 void launch_set_i32(cudaStream_t s, int32_t* p, int n, int32_t v);
 
 // ls_dense.cu

@@ -188,9 +188,12 @@ class ConsistencySamples:
         if self._gen != self._solver.sample_gen:
             raise RuntimeError("consistency samples were overwritten before being read")
         self._src, self._dst, self._temporal = self._solver.get_pairs(self._n)
+        self._n = int(self._src.numel())
         self._weight = torch.ones(self._n, dtype=torch.float64, device=self._src.device)
 
     def __len__(self):
+        if self._src is None and self._n < 0 and self._solver is not None:
+            self._n = self._solver.pair_count()
         return self._n if self._src is None else int(self._src.numel())
 
     @property
