@@ -176,6 +176,17 @@ LS_API int ls_pcg(ls_ctx* ctx, const double* colors_host, const float* X, int it
  * starting energy (solver.py:153-157). */
 LS_API int ls_gn_step(ls_ctx* ctx, const double* colors_host, const float* X, float* X_out,
                ls_gn_record* rec);
+/* Streaming flip-flop (solver.py:311-338 with refine = False), enqueued
+ * without host round trips: line search, acceptance, state selection and the
+ * relative-decrease convergence test run on the device; one synchronisation
+ * at the end.  The state starts in X0; X1 / X2 are ping-pong buffers;
+ * *final_buffer (0/1/2) says which holds the result.  out (host, outer *
+ * gn_steps records) receives *n_records executed steps; *status: 0
+ * max_outer, 1 stalled, 2 converged.  A non-finite starting energy returns
+ * LS_ERR_NONFINITE with *fault_step the faulting record (solver.py:153-157). */
+LS_API int ls_flip_flop_stream(ls_ctx* ctx, const double* colors_host, float* X0, float* X1, float* X2, int outer,
+                               int gn_steps, double tol_rel, ls_gn_record* out, int* n_records, int* status,
+                               int* final_buffer, int* fault_step);
 /* Dense 3K x 3K refinement normal system at delta_b = 0 (energy.py:563-610);
  * uses the cluster ids set by ls_set_anchor when use_ids != 0.  Host outputs. */
 LS_API int ls_dense_normal(ls_ctx* ctx, const double* colors_host, const float* X, int use_ids,

@@ -239,6 +239,23 @@ class DeviceSolver:
             self._chk(rc)
         return rc, rec
 
+    def flip_flop_stream(self, colors, X0, outer: int, gn_steps: int, tol_rel: float):
+        """Device-resident streaming flip-flop; returns (rc, records, status,
+        final state tensor, fault step)."""
+        a, pa = L.dbl_array(colors)
+        X1 = torch.empty_like(X0)
+        X2 = torch.empty_like(X0)
+        n = max(1, outer * gn_steps)
+        recs = (L.GNRecord * n)()
+        nrec, status, final, fault = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        self._enter()
+        rc = self.lib.ls_flip_flop_stream(self.ctx, pa, L.dptr(X0), L.dptr(X1), L.dptr(X2), int(outer),
+                                          int(gn_steps), float(tol_rel), recs, C.byref(nrec), C.byref(status),
+                                          C.byref(final), C.byref(fault))
+        if rc not in (L.LS_OK, L.LS_ERR_NONFINITE):
+            self._chk(rc)
+        return rc, [recs[i] for i in range(nrec.value)], status.value, (X0, X1, X2)[final.value], fault.value
+
     def dense_normal(self, colors, X, use_ids: bool):
         a, pa = L.dbl_array(colors)
         n = 3 * self.K

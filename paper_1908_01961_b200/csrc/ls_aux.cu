@@ -327,24 +327,56 @@ __global__ void k_fill_pairs(int64_t n, const int64_t* src, const int64_t* dst, 
   }
 }
 
-// deterministic order inside each adjacency row (insertion sort by key)
-__global__ void k_sort_rows(int N, const int32_t* __restrict__ row_ptr, uint16_t* ent, uint32_t* key, float* ent_w) {
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
-    const int a = row_ptr[p], b = row_ptr[p + 1];
-    for (int i = a + 1; i < b; ++i) {
-      const uint32_t k = key[i];
-      const uint16_t e = ent[i];
-      const float w = ent_w ? ent_w[i] : 0.f;
-      int j = i - 1;
-      while (j >= a && key[j] > k) {
-        key[j + 1] = key[j];
-        ent[j + 1] = ent[j];
-        if (ent_w) ent_w[j + 1] = ent_w[j];
-        --j;
+// deterministic order inside each adjacency row (insertion sort by key).
+// Rows are short (~8 entries): each thread sorts its row in shared memory
+// (column-major per block -> conflict-free); longer rows sort in place.
+constexpr int kSortThreads = 128, kSortCap = 24;
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_rows(int N, const int32_t* __restrict__ row_ptr, uint16_t* ent,
+                                                            uint32_t* key, float* ent_w) {
+  __shared__ uint32_t sk[kSortCap][kSortThreads];
+  __shared__ uint16_t se[kSortCap][kSortThreads];
+  __shared__ float sw[kSortCap][kSortThreads];
+  const int t = threadIdx.x;
+  for (int p = blockIdx.x * blockDim.x + t; p < N; p += gridDim.x * blockDim.x) {
+    const int a = row_ptr[p], n = row_ptr[p + 1] - a;
+    if (n <= kSortCap) {
+      for (int i = 0; i < n; ++i) {
+        const uint32_t k = key[a + i];
+        const uint16_t e = ent[a + i];
+        const float w = ent_w ? ent_w[a + i] : 0.f;
+        int j = i - 1;
+        while (j >= 0 && sk[j][t] > k) {
+          sk[j + 1][t] = sk[j][t];
+          se[j + 1][t] = se[j][t];
+          sw[j + 1][t] = sw[j][t];
+          --j;
+        }
+        sk[j + 1][t] = k;
+        se[j + 1][t] = e;
+        sw[j + 1][t] = w;
       }
-      key[j + 1] = k;
-      ent[j + 1] = e;
-      if (ent_w) ent_w[j + 1] = w;
+      for (int i = 0; i < n; ++i) {
+        key[a + i] = sk[i][t];
+        ent[a + i] = se[i][t];
+        if (ent_w) ent_w[a + i] = sw[i][t];
+      }
+    } else {
+      for (int i = a + 1; i < a + n; ++i) {
+        const uint32_t k = key[i];
+        const uint16_t e = ent[i];
+        const float w = ent_w ? ent_w[i] : 0.f;
+        int j = i - 1;
+        while (j >= a && key[j] > k) {
+          key[j + 1] = key[j];
+          ent[j + 1] = ent[j];
+          if (ent_w) ent_w[j + 1] = ent_w[j];
+          --j;
+        }
+        key[j + 1] = k;
+        ent[j + 1] = e;
+        if (ent_w) ent_w[j + 1] = w;
+      }
     }
   }
 }
@@ -470,7 +502,7 @@ void launch_fill_from_pairs(cudaStream_t s, int64_t n, const int64_t* src, const
   if (n > 0) k_fill_pairs<<<grid_for(n), 256, 0, s>>>(n, src, dst, temporal, weight, W, row_ptr, fill, ent, key, ent_w);
 }
 void launch_sort_rows(cudaStream_t s, int N, const int32_t* row_ptr, uint16_t* ent, uint32_t* key, float* ent_w) {
-  k_sort_rows<<<grid_for(N), 256, 0, s>>>(N, row_ptr, ent, key, ent_w);
+  k_sort_rows<<<grid_for(N, kSortThreads), kSortThreads, 0, s>>>(N, row_ptr, ent, key, ent_w);
 }
 void launch_pairs_from_samples(cudaStream_t s, const int16_t* codes, int H, int W, const int32_t* off, int64_t* src,
                                int64_t* dst, uint8_t* temporal) {

@@ -134,6 +134,10 @@ struct ls_ctx {
   double *dense_sums = nullptr, *colors_dev = nullptr, *dense_A = nullptr, *dense_rhs = nullptr,
          *dense_x = nullptr;
   double* host_buf = nullptr;   // pinned, 2 * 36 * 36 + 64 doubles
+  FrameCtl* ctl = nullptr;       // device-resident flip-flop control
+  StepRecord* recs = nullptr;    // device step records
+  StepRecord* recs_host = nullptr;
+  FrameCtl* ctl_host = nullptr;
   std::vector<void*> allocs;
 };
 
@@ -299,6 +303,10 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   A_(dalloc(c, &c->dense_rhs, 36));
   A_(dalloc(c, &c->dense_x, 36));
   A_(cudaMallocHost((void**)&c->sc_host, sizeof(Scalars)));
+  A_(dalloc(c, &c->ctl, 1));
+  A_(dalloc(c, &c->recs, kMaxStepRecords));
+  A_(cudaMallocHost((void**)&c->recs_host, sizeof(StepRecord) * kMaxStepRecords));
+  A_(cudaMallocHost((void**)&c->ctl_host, sizeof(FrameCtl)));
   A_(cudaMallocHost((void**)&c->host_buf, sizeof(double) * (2 * 36 * 36 + 64)));
   A_(cudaMemset(c->tickets, 0, 8 * sizeof(unsigned)));
   A_(cudaMemset(c->sc, 0, sizeof(Scalars)));
@@ -360,6 +368,8 @@ int ls_ctx_destroy(ls_ctx* c) {
   cudaFree(c->ent_w);
   cudaFree(c->key);
   if (c->sc_host) cudaFreeHost(c->sc_host);
+  if (c->recs_host) cudaFreeHost(c->recs_host);
+  if (c->ctl_host) cudaFreeHost(c->ctl_host);
   if (c->host_buf) cudaFreeHost(c->host_buf);
   delete c;
   return LS_OK;
@@ -717,14 +727,15 @@ static bool pcg_maps(ls_ctx* c, const float* X, const float* pprev, PcgMaps* m) 
 
 // fused energy/gradient + textbook PCG loop (solver.py:79-107); x receives the step.
 // Buffers: r, d = 1/diag, u = z = r/diag, wv = q = A p, p / s = ping-pong p.
-static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, float* x) {
+static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, float* x,
+                   const FrameCtl* ctl = nullptr) {
   const Frame f = frame_of(c);
   const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
   size_t pi = prof_begin(c);
   EnergyMaps em;
   const bool etma = energy_maps(c, X, nullptr, &em);
   launch_energy(0, L_energy(c), f, cd, X, nullptr, 0.f, nullptr, nullptr, c->r, c->d, c->u, nullptr, nullptr,
-                c->part, c->tickets + 0, c->sc, etma ? &em : nullptr);
+                c->part, c->tickets + 0, c->sc, etma ? &em : nullptr, ctl);
   prof_end(c, PC_EG, pi);
   const int64_t M = (int64_t)c->U * c->N;
   float* pbuf[2] = {c->p, c->s};
@@ -825,6 +836,79 @@ int ls_gn_step(ls_ctx* c, const double* colors, const float* X, float* X_out, ls
   rec->energy_after = accepted ? e1 : e0;
   if (!accepted) std::memcpy(rec->terms, rec->terms_before, sizeof(rec->terms));
   return LS_OK;
+}
+
+// Whole streaming flip-flop (solver.py:311-338 with refine = False) enqueued
+// without host round trips: per GN step the EG kernel, the PCG, up to
+// max_halvings+1 trial kernels deciding accept / halve on the device, and a
+// step-end kernel; per outer iteration the convergence test.  One host
+// synchronisation at the end to read the records.
+extern "C" int ls_flip_flop_stream(ls_ctx* c, const double* colors, float* X0, float* X1, float* X2, int outer,
+                                   int gn_steps, double tol_rel, ls_gn_record* out, int* n_records, int* status,
+                                   int* final_buffer, int* fault_step) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  LS_ARG(X0 && X1 && X2 && out && n_records && status && final_buffer && fault_step, "bad arguments");
+  LS_ARG(outer >= 0 && gn_steps >= 0 && (int64_t)outer * gn_steps <= kMaxStepRecords, "too many GN steps");
+  LS_CK(cudaSetDevice(c->dev));
+  const Frame f = frame_of(c);
+  const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
+  const int64_t M = (int64_t)c->U * c->N;
+  float* bufs[3] = {X0, X1, X2};
+  launch_frame_init(c->stream, c->ctl);
+  int k = 0;
+  for (int o = 0; o < outer; ++o) {
+    for (int g = 0; g < gn_steps; ++g, ++k) {
+      const int in_id = (k == 0) ? 0 : 1 + ((k - 1) & 1), out_id = 1 + (k & 1);
+      rc = run_pcg(c, colors, bufs[in_id], c->cfg.pcg_iterations, c->x, c->ctl);
+      if (rc) return rc;
+      EnergyMaps em;
+      const bool etma = energy_maps(c, bufs[in_id], c->x, &em);
+      double alpha = 1.0;
+      for (int h = 0; h <= c->cfg.max_halvings; ++h, alpha *= 0.5) {
+        const size_t pi = prof_begin(c);
+        launch_energy(1, L_energy(c), f, cd, bufs[in_id], c->x, (float)alpha, nullptr, bufs[out_id], nullptr, nullptr,
+                      nullptr, nullptr, nullptr, c->part, c->tickets + 0, c->sc, etma ? &em : nullptr, c->ctl, 1,
+                      h == c->cfg.max_halvings);
+        prof_end(c, PC_TRIAL, pi);
+      }
+      launch_step_end(c->stream, c->grid_update, c->ctl, c->sc, bufs[in_id], bufs[out_id], M, out_id, c->recs);
+      c->launches += 2 + c->cfg.max_halvings;
+    }
+    launch_outer_end(c->stream, c->ctl, tol_rel);
+    c->launches += 1;
+  }
+  LS_CK(cudaGetLastError());
+  LS_CK(cudaMemcpyAsync(c->ctl_host, c->ctl, sizeof(FrameCtl), cudaMemcpyDeviceToHost, c->stream));
+  if (k > 0)
+    LS_CK(cudaMemcpyAsync(c->recs_host, c->recs, sizeof(StepRecord) * k, cudaMemcpyDeviceToHost, c->stream));
+  if (!c->sampled_counts_known)
+    LS_CK(cudaMemcpyAsync(c->host_buf, &c->sstate->error, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaStreamSynchronize(c->stream));
+  prof_harvest(c);
+  if (!c->sampled_counts_known && *reinterpret_cast<int*>(c->host_buf)) {
+    g_err = "consistency sampler: too many PCG64 rejections in one frame";
+    return LS_ERR_CUDA;
+  }
+  const FrameCtl& ctl = *c->ctl_host;
+  for (int i = 0; i < ctl.n_exec; ++i) {
+    const StepRecord& R = c->recs_host[i];
+    ls_gn_record& o = out[i];
+    o.energy_before = R.e0;
+    o.energy_after = R.e1;
+    o.alpha = R.alpha;
+    o.accepted = R.accepted;
+    o.pcg_iterations = R.iterations;
+    o.initial_residual = std::sqrt(R.bnorm2);
+    o.final_residual = std::sqrt(R.rnorm2);
+    std::memcpy(o.terms_before, R.terms0, sizeof(o.terms_before));
+    std::memcpy(o.terms, R.terms1, sizeof(o.terms));
+  }
+  *n_records = ctl.n_exec;
+  *status = ctl.converged ? 2 : (ctl.stalled ? 1 : 0);
+  *final_buffer = ctl.cur;
+  *fault_step = ctl.fault_step;
+  return ctl.fault_step >= 0 ? LS_ERR_NONFINITE : LS_OK;
 }
 
 static int dense_system(ls_ctx* c, const double* colors, const float* X, int use_ids) {

@@ -75,10 +75,34 @@ struct Scalars {
   double terms1[kTerms];      // energies at the last trial point
   int iterations;
   int stop;
-  int pending;                // x still needs alpha * p_last
+  int pending;                // (unused; kept for layout stability)
   int xinit;                  // x has been written (else it is zero)
-  int plast;                  // ping-pong index of the last p written
-  int pad[3];
+  int plast;
+  int ls_done;                // device line search: decided
+  int accepted;
+  int fault;                  // non-finite energy at the linearisation point
+  double alpha_ls;            // accepted step length
+  double e0, e1;              // Python-sum order of terms0 / terms1 (solver.py:139-140)
+};
+
+// device-resident flip-flop of a streaming frame (solver.py:311-338 with
+// refine = False): convergence test and step bookkeeping on the GPU
+struct FrameCtl {
+  int done;                   // converged or faulted: later kernels are no-ops
+  int converged;
+  int stalled;
+  int has_hist;               // energy_history non-empty
+  int e_prev_valid;
+  int n_exec;                 // GN steps executed (records written)
+  int cur;                    // which of the two state buffers holds the state
+  int fault_step;             // index of a faulting step, -1 if none
+  double e_last, e_prev;
+};
+
+struct StepRecord {
+  double e0, e1, alpha, bnorm2, rnorm2;
+  double terms0[kTerms], terms1[kTerms];
+  int accepted, iterations, fault, pad;
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }

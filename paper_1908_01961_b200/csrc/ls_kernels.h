@@ -38,7 +38,11 @@ struct Launch {
 void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
                    const float* dx, float alpha, const float* Y, float* Xout, float* r_out, float* d_out,
                    float* u_out, float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc,
-                   const EnergyMaps* maps);
+                   const EnergyMaps* maps, const FrameCtl* ctl = nullptr, int dev_ls = 0, int last_trial = 0);
+void launch_frame_init(cudaStream_t s, FrameCtl* ctl);
+void launch_step_end(cudaStream_t s, int grid, FrameCtl* ctl, const Scalars* sc, const float* Xin, float* Xout,
+                     int64_t M, int out_id, StepRecord* recs);
+void launch_outer_end(cudaStream_t s, FrameCtl* ctl, double tol_rel);
 void launch_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* u,
                   float* w, double* part, unsigned* ticket, Scalars* sc, int iter, const TileMaps* maps);
 int tile_box_w();
@@ -69,6 +73,7 @@ struct SampleState {
   long long z[kMaxRejections];   // rejected u32 stream positions, ascending
 };
 constexpr int kSamplePasses = 4;
+constexpr int kMaxStepRecords = 256;
 void launch_pack_hwc(cudaStream_t s, const float* hwc, int C, int N, float* planes);
 void launch_unpack_hwc(cudaStream_t s, const float* planes, int C, int N, float* hwc);
 void launch_image(cudaStream_t s, const float* hwc, int N, float* img_planes, double* chroma);

@@ -404,9 +404,16 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
                                                      float* __restrict__ u_out, float* __restrict__ b_raw,
                                                      float* __restrict__ diag_raw, double* part,
                                                      unsigned* ticket, Scalars* sc, int ntiles,
+                                                     const FrameCtl* ctl, int dev_ls, int last_trial,
                                                      const __grid_constant__ EnergyMaps maps) {
   constexpr int U = NT + 3;
   constexpr bool TRIAL = MODE == MODE_TRIAL;
+  // device-resident flip-flop: skip finished frames / decided line searches
+  if (ctl && ctl->done) {
+    if (!TRIAL && blockIdx.x == 0 && threadIdx.x == 0) sc->stop = 1;
+    return;
+  }
+  if (TRIAL && dev_ls && sc->ls_done) return;
   constexpr int NST = (TMA && !TRIAL) ? 2 : 1;
   constexpr int STAGE = e_stage(NT, TRIAL);
   constexpr int NV = TRIAL ? kTerms : kTerms + 2;
@@ -493,6 +500,14 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
     bool finite = true;
     for (int j = 0; j < kTerms; ++j) finite = finite && isfinite(tot[j]);
     if (!TRIAL) {
+      double e0 = 0.0;   // Python sum() order over the blocks (solver.py:139-140)
+      for (int j = 0; j < kTerms; ++j) e0 += tot[j];
+      sc->e0 = e0;
+      sc->ls_done = 0;
+      sc->accepted = 0;
+      sc->fault = 0;
+      sc->alpha_ls = 0.0;
+      sc->e1 = e0;
       for (int j = 0; j < kTerms; ++j) sc->terms0[j] = tot[j];
       sc->gamma = tot[kTerms];
       sc->gamma_prev = 0.0;
@@ -507,6 +522,21 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
       sc->stop = (!finite || tot[kTerms + 1] == 0.0 || r_out == nullptr) ? 1 : 0;
     } else {
       for (int j = 0; j < kTerms; ++j) sc->terms1[j] = tot[j];
+      if (dev_ls) {   // accept / halve decision of solver.py:169-178 on the device
+        double e1 = 0.0;
+        for (int j = 0; j < kTerms; ++j) e1 += tot[j];
+        if (!isfinite(sc->e0)) {
+          sc->fault = 1;
+          sc->ls_done = 1;
+        } else if (isfinite(e1) && e1 <= sc->e0) {
+          sc->ls_done = 1;
+          sc->accepted = 1;
+          sc->alpha_ls = (double)alpha;
+          sc->e1 = e1;
+        } else if (last_trial) {
+          sc->ls_done = 1;
+        }
+      }
     }
     *ticket = 0u;
   }
@@ -1030,26 +1060,28 @@ template <int NT, int MODE>
 static void launch_energy_mt(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* dx,
                              float alpha, const float* Y, float* Xout, float* r_out, float* d_out, float* u_out,
                              float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc,
-                             const EnergyMaps* maps) {
+                             const EnergyMaps* maps, const FrameCtl* ctl, int dev_ls, int last_trial) {
   if (maps)
     k_energy<NT, MODE, true><<<L.grid, kThreads, energy_smem<NT>(MODE, true), L.stream>>>(
-        f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, *maps);
+        f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, ctl, dev_ls,
+        last_trial, *maps);
   else
     k_energy<NT, MODE, false><<<L.grid, kThreads, energy_smem<NT>(MODE, false), L.stream>>>(
-        f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, EnergyMaps{});
+        f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, ctl, dev_ls,
+        last_trial, EnergyMaps{});
 }
 
 template <int NT>
 static void launch_energy_nt(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
                              const float* dx, float alpha, const float* Y, float* Xout, float* r_out, float* d_out,
                              float* u_out, float* b_raw, float* diag_raw, double* part, unsigned* ticket,
-                             Scalars* sc, const EnergyMaps* maps) {
+                             Scalars* sc, const EnergyMaps* maps, const FrameCtl* ctl, int dev_ls, int last_trial) {
   if (mode == MODE_EG)
     launch_energy_mt<NT, MODE_EG>(L, f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket,
-                                  sc, maps);
+                                  sc, maps, ctl, dev_ls, last_trial);
   else
     launch_energy_mt<NT, MODE_TRIAL>(L, f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part,
-                                     ticket, sc, maps);
+                                     ticket, sc, maps, ctl, dev_ls, last_trial);
 }
 
 template <int NT>
@@ -1066,10 +1098,84 @@ static void launch_apply_nt(const Launch& L, const Frame& f, const Coef<float>& 
 void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
                    const float* dx, float alpha, const float* Y, float* Xout, float* r_out, float* d_out,
                    float* u_out, float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc,
-                   const EnergyMaps* maps) {
+                   const EnergyMaps* maps, const FrameCtl* ctl, int dev_ls, int last_trial) {
   LS_DISPATCH_NT(f.NT, (launch_energy_nt<NT_>(mode, L, f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw,
-                                              diag_raw, part, ticket, sc, maps)));
+                                              diag_raw, part, ticket, sc, maps, ctl, dev_ls, last_trial)));
 }
+
+// ---------------------------------------------------------------------------
+// device-resident flip-flop bookkeeping (solver.py:311-338, refine = False)
+// ---------------------------------------------------------------------------
+__global__ void k_frame_init(FrameCtl* ctl) {
+  ctl->done = ctl->converged = ctl->stalled = ctl->has_hist = ctl->e_prev_valid = 0;
+  ctl->n_exec = 0;
+  ctl->cur = 0;
+  ctl->fault_step = -1;
+  ctl->e_last = ctl->e_prev = 0.0;
+}
+
+// end of one GN step: the state moves to buffer `out_id` (copied through on a
+// rejected step, solver.py:169-178 leaves it unchanged); record + bookkeeping
+__global__ void k_step_end(FrameCtl* ctl, const Scalars* sc, const float* __restrict__ Xin, float* __restrict__ Xout,
+                           int64_t M, int out_id, StepRecord* recs) {
+  if (ctl->done) return;
+  const bool fault = sc->fault;
+  const bool acc = sc->accepted && !fault;
+  if (!acc && !fault)
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x)
+      Xout[j] = Xin[j];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    StepRecord& R = recs[ctl->n_exec];
+    R.e0 = sc->e0;
+    R.e1 = acc ? sc->e1 : sc->e0;
+    R.alpha = acc ? sc->alpha_ls : 0.0;
+    R.bnorm2 = sc->bnorm2;
+    R.rnorm2 = sc->rnorm2;
+    for (int j = 0; j < kTerms; ++j) {
+      R.terms0[j] = sc->terms0[j];
+      R.terms1[j] = acc ? sc->terms1[j] : sc->terms0[j];
+    }
+    R.accepted = acc;
+    R.iterations = sc->iterations;
+    R.fault = fault;
+    if (fault) {
+      ctl->done = 1;
+      ctl->fault_step = ctl->n_exec;
+    } else {
+      ctl->cur = out_id;
+      if (acc) {
+        ctl->e_last = sc->e1;
+        ctl->has_hist = 1;
+      } else {
+        ctl->stalled = 1;
+      }
+    }
+    ctl->n_exec += 1;
+  }
+}
+
+// end of one outer iteration: relative-decrease convergence (solver.py:328-336)
+__global__ void k_outer_end(FrameCtl* ctl, double tol_rel) {
+  if (ctl->done || !ctl->has_hist) return;
+  const double e_now = ctl->e_last;
+  if (ctl->e_prev_valid && ctl->e_prev > 0.0) {
+    const double rel = (ctl->e_prev - e_now) / ctl->e_prev;
+    if (0.0 <= rel && rel < tol_rel) {
+      ctl->converged = 1;
+      ctl->done = 1;
+      return;
+    }
+  }
+  ctl->e_prev = e_now;
+  ctl->e_prev_valid = 1;
+}
+
+void launch_frame_init(cudaStream_t s, FrameCtl* ctl) { k_frame_init<<<1, 1, 0, s>>>(ctl); }
+void launch_step_end(cudaStream_t s, int grid, FrameCtl* ctl, const Scalars* sc, const float* Xin, float* Xout,
+                     int64_t M, int out_id, StepRecord* recs) {
+  k_step_end<<<grid, kThreads, 0, s>>>(ctl, sc, Xin, Xout, M, out_id, recs);
+}
+void launch_outer_end(cudaStream_t s, FrameCtl* ctl, double tol_rel) { k_outer_end<<<1, 1, 0, s>>>(ctl, tol_rel); }
 
 void launch_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* u,
                   float* w, double* part, unsigned* ticket, Scalars* sc, int iter, const TileMaps* maps) {

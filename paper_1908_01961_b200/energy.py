@@ -171,11 +171,12 @@ class ConsistencySamples:
         self._solver = None
         self._gen = -1
         self._n = 0
+        self._recipe = None     # (frame, seed, prev_chroma): the draws are deterministic
 
     @classmethod
-    def _device_backed(cls, solver, n: int, shape):
+    def _device_backed(cls, solver, n: int, shape, recipe=None):
         s = cls(shape=shape)
-        s._solver, s._gen, s._n = solver, solver.sample_gen, n
+        s._solver, s._gen, s._n, s._recipe = solver, solver.sample_gen, n, recipe
         solver.csr_owner = s
         return s
 
@@ -183,17 +184,28 @@ class ConsistencySamples:
         return self._solver is solver and self._gen == solver.sample_gen
 
     def _materialize(self):
-        if self._src is not None or self._solver is None:
+        if self._src is not None:
             return
-        if self._gen != self._solver.sample_gen:
+        if self._solver is not None and self._gen == self._solver.sample_gen:
+            self._src, self._dst, self._temporal = self._solver.get_pairs(self._n)
+        elif self._recipe is not None:
+            # the adjacency was rebuilt since: redraw (bit-identical) in a scratch context
+            from .imaging import chromaticity
+            frame, seed, prev = self._recipe
+            again = sample_consistency(chromaticity(frame), prev, seed)
+            self._src, self._dst, self._temporal = again.src, again.dst, again.temporal
+        else:
             raise RuntimeError("consistency samples were overwritten before being read")
-        self._src, self._dst, self._temporal = self._solver.get_pairs(self._n)
+        self._solver = None
         self._n = int(self._src.numel())
         self._weight = torch.ones(self._n, dtype=torch.float64, device=self._src.device)
 
     def __len__(self):
-        if self._src is None and self._n < 0 and self._solver is not None:
-            self._n = self._solver.pair_count()
+        if self._src is None and self._n < 0:
+            if self._solver is not None and self._gen == self._solver.sample_gen:
+                self._n = self._solver.pair_count()
+            else:
+                self._materialize()
         return self._n if self._src is None else int(self._src.numel())
 
     @property
@@ -218,10 +230,14 @@ class ConsistencySamples:
 
 
 def _guard_csr(solver):
-    """Copy out device-backed samples before the adjacency is rebuilt."""
+    """Before the adjacency is rebuilt: device-backed samples that can be
+    redrawn (a recipe) are just detached; others are copied out."""
     owner = getattr(solver, "csr_owner", None)
     if owner is not None and owner._src is None and owner.backed_by(solver):
-        owner._materialize()
+        if owner._recipe is not None:
+            owner._solver = None
+        else:
+            owner._materialize()
     solver.csr_owner = None
 
 
@@ -300,7 +316,8 @@ def install(solver, frame: Frame, aux: EnergyAux):
         _guard_csr(solver)
         _, seed, prev = aux._recipe
         n = solver.sample(seed, None, None if prev is None else prev.planes)
-        aux._samples = ConsistencySamples._device_backed(solver, n, (solver.H, solver.W))
+        aux._samples = ConsistencySamples._device_backed(solver, n, (solver.H, solver.W),
+                                                         recipe=(frame, seed, prev))
         if aux._edge is None:
             aux._edge = solver.get_edge()
     else:

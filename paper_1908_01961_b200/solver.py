@@ -125,6 +125,25 @@ def pcg(apply_A: Callable, b, diag, iterations: int):
     return (x.numpy() if is_np else x), info
 
 
+# streaming flip-flops (refine = False) run device-resident (ls_flip_flop_stream)
+DEVICE_FLIP_FLOP = True
+
+
+def _record_from(rec) -> dict:
+    accepted = bool(rec.accepted)
+    return {
+        "phase": "sparse",
+        "energy_before": float(rec.energy_before),
+        "energy_after": float(rec.energy_after),
+        "accepted": accepted,
+        "alpha": float(rec.alpha) if accepted else 0.0,
+        "pcg": {"iterations": int(rec.pcg_iterations),
+                "initial_residual": float(rec.initial_residual),
+                "final_residual": float(rec.final_residual)},
+        "terms": {k: float(v) for k, v in zip(TERM_NAMES, rec.terms)},
+    }
+
+
 def gn_step_sparse(state: SolverState) -> dict:
     """solver.py:143-192: one device Gauss-Newton step on the per-pixel unknowns."""
     solver = _solver_for(state)
@@ -138,17 +157,7 @@ def gn_step_sparse(state: SolverState) -> dict:
     accepted = bool(rec.accepted)
     if accepted:
         state.layers = LayerStack(planes=X_out)
-    record = {
-        "phase": "sparse",
-        "energy_before": float(rec.energy_before),
-        "energy_after": float(rec.energy_after),
-        "accepted": accepted,
-        "alpha": float(rec.alpha) if accepted else 0.0,
-        "pcg": {"iterations": int(rec.pcg_iterations),
-                "initial_residual": float(rec.initial_residual),
-                "final_residual": float(rec.final_residual)},
-        "terms": {k: float(v) for k, v in zip(TERM_NAMES, rec.terms)},
-    }
+    record = _record_from(rec)
     state.records.append(record)
     if accepted:
         state.energy_history.append(record["energy_after"])
@@ -247,9 +256,33 @@ def initialize(frame: Frame, cluster_map: ClusterMap | None, palette: BaseColorP
     return LayerStack(planes=X)
 
 
+def _flip_flop_device(state: SolverState) -> SolverState:
+    """solver.py:311-338 with refine = False, decided on the device (the
+    same accept / halve / convergence rules, one host synchronisation)."""
+    cfg = state.config
+    solver = _solver_for(state)
+    rc, recs, status, X_final, fault = solver.flip_flop_stream(
+        state.palette.colors, state.layers.X, cfg.outer_iterations, cfg.gn_steps, cfg.tol_rel)
+    for i, rec in enumerate(recs):
+        if rc == L.LS_ERR_NONFINITE and i == fault:
+            state.layers = LayerStack(planes=X_final)
+            terms = {k: float(v) for k, v in zip(TERM_NAMES, rec.terms_before)}
+            raise NumericalFaultError("non-finite residuals in sparse phase",
+                                      dump={"iteration": len(state.records), "terms": terms})
+        d = _record_from(rec)
+        state.records.append(d)
+        if d["accepted"]:
+            state.energy_history.append(d["energy_after"])
+    state.layers = LayerStack(planes=X_final)
+    state.status = ("max_outer", "stalled", "converged")[status]
+    return state
+
+
 def flip_flop(state: SolverState) -> SolverState:
     """solver.py:311-338."""
     cfg = state.config
+    if not cfg.refine and DEVICE_FLIP_FLOP:
+        return _flip_flop_device(state)
     e_prev = None
     stalled = False
     for outer in range(cfg.outer_iterations):

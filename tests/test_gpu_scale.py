@@ -181,3 +181,30 @@ def test_nondefault_weights_match_oracle():
     A, rhs = refine_normal_system(st.frame, st.layers, st.palette, w, cluster_ids=st.aux.cluster_ids)
     oA, orhs = O.refine_normal_system(img, osys.r0, osys.T0, clip.colors, ow, ids)
     assert np.max(np.abs(A - oA)) / np.max(np.abs(oA)) < 1e-9
+
+
+def test_device_flip_flop_equals_host_loop():
+    """The device-resident streaming flip-flop makes the same decisions and
+    produces the same state (bitwise) as the host-driven loop of
+    solver.py:311-338, including the convergence test."""
+    from dataclasses import replace
+    from paper_1908_01961_b200 import solver as S
+    clip = _clip(64, 96, 4, n=2, seed=9)
+    outs = []
+    for dev in (True, False):
+        S.DEVICE_FLIP_FLOP = dev
+        try:
+            st0 = _state(clip)
+            st0.config = replace(st0.config, refine=False, outer_iterations=2)
+            S.flip_flop(st0)
+            st = _state(clip, idx=1, prev=(st0.frame, st0.layers), seed=1)
+            st.config = replace(st.config, refine=False, outer_iterations=6, tol_rel=2e-3)
+            S.flip_flop(st)
+            outs.append((st.records, st.status, st.layers.X.clone(), st.energy_history))
+        finally:
+            S.DEVICE_FLIP_FLOP = True
+    (r0, s0, X0, h0), (r1, s1, X1, h1) = outs
+    assert s0 == s1 and len(r0) == len(r1) and h0 == h1
+    for a, b in zip(r0, r1):
+        assert a == b
+    assert torch.equal(X0, X1)
