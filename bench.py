@@ -301,6 +301,7 @@ def run_ours(args):
         "apply": (prof["apply"], bytes_apply),
         "update": (prof["update"], bytes_update),
     }
+    kname = {"apply": "k_pcg_apply", "update": "k_pcg_update"}
     dom = max(kern, key=lambda k: kern[k][0]["ms"])
     pst, bpl = kern[dom]
     avg_ms = pst["ms"] / max(pst["count"], 1)
@@ -316,10 +317,15 @@ def run_ours(args):
         per_kernel[k] = {"launches": prof[k]["count"],
                          "avg_us": 1e3 * prof[k]["ms"] / max(prof[k]["count"], 1)}
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic_from_profiles(f"k_{dom}"),
-                "kernel": f"k_{dom}", "peak_source": peak_src,
+                "frac": achieved / peak, "traffic": traffic_from_profiles(kname[dom]),
+                "kernel": kname[dom], "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bpl, "avg_launch_us": avg_ms * 1e3,
-                "per_kernel": per_kernel}
+                "per_kernel": per_kernel,
+                # SURVEY.md 8(d) compulsory-traffic model of a whole streaming
+                # frame, B_frame = 4 N (860 U + 298) bytes, over the measured frame time
+                "frame_model": {"bytes": 4 * N * (860 * U + 298),
+                                "achieved_gbs": 4 * N * (860 * U + 298) / (t_ms / steps / 1e3) / 1e9,
+                                "frac": 4 * N * (860 * U + 298) / (t_ms / steps / 1e3) / 1e9 / peak}}
 
     # --- e2e through the public API with host buffers ---
     e2e = None

@@ -9,10 +9,12 @@ the CPU test suite can check the ABI without a GPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "liblumisplit_b200.so"
+# LS_LIB_PATH selects another build of the same library (tools/ablate.py)
+LIB_PATH = Path(os.environ.get("LS_LIB_PATH") or Path(__file__).resolve().parent / "liblumisplit_b200.so")
 
 LS_OK, LS_ERR_NONFINITE, LS_ERR_ARG, LS_ERR_CUDA = 0, 1, 2, 3
 NUM_TERMS = 8

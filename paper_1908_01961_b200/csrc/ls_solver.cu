@@ -25,6 +25,11 @@
 #include "ls_common.cuh"
 #include "ls_kernels.h"
 
+// timing ablations of k_pcg_apply (tools/ablate.py only; 0 in every product build)
+#ifndef LS_ABLATE
+#define LS_ABLATE 0
+#endif
+
 namespace ls {
 
 enum { MODE_EG = 0, MODE_TRIAL = 1 };
@@ -544,10 +549,27 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
 
 // One pixel of w = J^T J u.  IN: interior tile (every stencil neighbour is
 // inside the image) -> no border masks.  Returns the pixel's <w, u>.
+// Per-pixel global reads of the operator (CSR row bounds, edge gate), issued
+// before the tile's TMA wait so their latency overlaps it.
+struct PixPre {
+  int e0, e1;
+  float edge;
+};
+__device__ __forceinline__ PixPre pix_prefetch(const Frame& f, int x, int y, bool own) {
+  PixPre p{0, 0, 0.f};
+  if (own) {
+    const int i = y * f.W + x;
+    p.e0 = __ldg(f.row_ptr + i);
+    p.e1 = __ldg(f.row_ptr + i + 1);
+    p.edge = __ldg(f.edge + i);
+  }
+  return p;
+}
+
 template <int NT, bool IN>
 __device__ __forceinline__ float apply_pixel(const Frame& f, const Coef<float>& c, const float* sX, const float* sT,
                                              const float* sR, float* __restrict__ w, int x, int y, int cx, int cy,
-                                             int rx, int ry) {
+                                             int rx, int ry, const PixPre& pre) {
   const int W = f.W, H = f.H, N = f.N;
   const int i = y * W + x;
   const bool hx = IN || x < W - 1, hy = IN || y < H - 1, hl = IN || x > 0, hu = IN || y > 0;
@@ -572,7 +594,7 @@ __device__ __forceinline__ float apply_pixel(const Frame& f, const Coef<float>& 
   // G = B - rowmean(B): sum_k G_kc u_k = s_c - mean_c(s) and sum_c q_c = 0,
   // so the T rows are sum_c B_kc (rho_c + q_c).
   float rq[3], outr[3], s[3] = {0.f, 0.f, 0.f};
-  const float lm = c.lam_m * __ldg(f.edge + i);
+  const float lm = c.lam_m * pre.edge;
 #pragma unroll
   for (int k = 0; k < NT; ++k)
 #pragma unroll
@@ -599,16 +621,18 @@ __device__ __forceinline__ float apply_pixel(const Frame& f, const Coef<float>& 
     a = fmaf(wis + wnn, uv, a);
     // smoothness D^T W_k D u_Tk (energy.py:272-282), weights from X
     float sm = 0.f;
+    if (LS_ABLATE != 3) {
     if (hx) sm = fmaf(irls1f(P[1] - v, c), uv - Q[1], sm);
     if (hl) sm = fmaf(irls1f(v - P[-1], c), uv - Q[-1], sm);
     if (hy) sm = fmaf(irls1f(P[kSW] - v, c), uv - Q[kSW], sm);
     if (hu) sm = fmaf(irls1f(v - P[-kSW], c), uv - Q[-kSW], sm);
+    }
     a = fmaf(c.lam_sm, sm, a);
     w[(size_t)(3 + k) * N + i] = a;
     dot = fmaf(a, uv, dot);
   }
   // r-sparsity D^T W D u_r, one weight per pixel shared by the channels
-  {
+  if (LS_ABLATE != 4) {
     const float wc = wrs_s(sX, cx, cy, hx, hy, c);
     const float wl = hl ? wrs_s(sX, cx - 1, cy, true, hy, c) : 0.f;
     const float wu = hu ? wrs_s(sX, cx, cy - 1, hx, true, c) : 0.f;
@@ -628,29 +652,44 @@ __device__ __forceinline__ float apply_pixel(const Frame& f, const Coef<float>& 
   // u(x) - u(q); temporal partners are constant (energy.py:356).  Entries
   // carry the partner's offset in this smem window.
   {
-    const int e0 = __ldg(f.row_ptr + i), e1 = __ldg(f.row_ptr + i + 1);
+    const int e0 = pre.e0, e1 = pre.e1;
     float a0 = 0.f, a1 = 0.f, a2 = 0.f;
     const float* R0p = sR + rc0;
-    if (f.ent_w == nullptr) {
-      for (int e = e0; e < e1; ++e) {
-        const uint16_t ent = __ldg(f.ent + e);
+    // entries are fetched four at a time so their load latencies overlap;
+    // the accumulation order is the CSR order either way
+    if (LS_ABLATE == 1) {
+    } else if (f.ent_w == nullptr) {
+      auto one = [&](uint16_t ent) {
         const int o = ent_soff(ent);
         const bool tmp = ent & kEntTemporal;
         a0 += ur[0] - (tmp ? 0.f : R0p[o]);
         a1 += ur[1] - (tmp ? 0.f : R0p[kRP + o]);
         a2 += ur[2] - (tmp ? 0.f : R0p[2 * kRP + o]);
+      };
+      int e = e0;
+      for (; e + 4 <= e1; e += 4) {
+        const uint16_t q0 = __ldg(f.ent + e), q1 = __ldg(f.ent + e + 1);
+        const uint16_t q2 = __ldg(f.ent + e + 2), q3 = __ldg(f.ent + e + 3);
+        one(q0); one(q1); one(q2); one(q3);
       }
+      for (; e < e1; ++e) one(__ldg(f.ent + e));
       a0 *= c.lam_rc; a1 *= c.lam_rc; a2 *= c.lam_rc;
     } else {
-      for (int e = e0; e < e1; ++e) {
-        const uint16_t ent = __ldg(f.ent + e);
-        const float we = c.lam_rc * __ldg(f.ent_w + e);
+      auto one = [&](uint16_t ent, float wgt) {
+        const float we = c.lam_rc * wgt;
         const int o = ent_soff(ent);
         const bool tmp = ent & kEntTemporal;
         a0 = fmaf(we, ur[0] - (tmp ? 0.f : R0p[o]), a0);
         a1 = fmaf(we, ur[1] - (tmp ? 0.f : R0p[kRP + o]), a1);
         a2 = fmaf(we, ur[2] - (tmp ? 0.f : R0p[2 * kRP + o]), a2);
+      };
+      int e = e0;
+      for (; e + 2 <= e1; e += 2) {
+        const uint16_t q0 = __ldg(f.ent + e), q1 = __ldg(f.ent + e + 1);
+        const float w0 = __ldg(f.ent_w + e), w1 = __ldg(f.ent_w + e + 1);
+        one(q0, w0); one(q1, w1);
       }
+      for (; e < e1; ++e) one(__ldg(f.ent + e), __ldg(f.ent_w + e));
     }
     outr[0] += a0; outr[1] += a1; outr[2] += a2;
   }
@@ -703,6 +742,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_apply(Frame f, Coef<float> c, c
     float* sX = smem + st * STAGE;
     float* sT = sX + off_T(NT);
     float* sR = sX + off_R(NT, true);
+    const PixPre pre = pix_prefetch(f, tx0 + lx, ty0 + ly, tx0 + lx < W && ty0 + ly < H);
     if (TMA) {
       mbar_wait(&bars[st], (phase >> st) & 1u);
       phase ^= 1u << st;
@@ -715,9 +755,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_apply(Frame f, Coef<float> c, c
     }
     const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H;
     if (interior)
-      acc += apply_pixel<NT, true>(f, c, sX, sT, sR, w, tx0 + lx, ty0 + ly, cx, cy, rx, ry);
+      acc += apply_pixel<NT, true>(f, c, sX, sT, sR, w, tx0 + lx, ty0 + ly, cx, cy, rx, ry, pre);
     else if (tx0 + lx < W && ty0 + ly < H)
-      acc += apply_pixel<NT, false>(f, c, sX, sT, sR, w, tx0 + lx, ty0 + ly, cx, cy, rx, ry);
+      acc += apply_pixel<NT, false>(f, c, sX, sT, sR, w, tx0 + lx, ty0 + ly, cx, cy, rx, ry, pre);
     if (TMA) {
       __syncthreads();   // every thread is done with this stage
       if (threadIdx.x == 0) {
@@ -830,7 +870,8 @@ __global__ void __launch_bounds__(kThreads) k_update(int64_t M, float* __restric
 // separate vector update; forming p costs no pass of its own).
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int op_floats(int NT) { return pad32(NT * kSP) + pad32(3 * kRP); }
-__host__ __device__ constexpr int pcg_stage(int NT) { return pad32((NT + 3) * kSP) + 2 * op_floats(NT); }
+// X, z and p_{i-1} windows (p_i = z_i + beta p_{i-1} is formed in place over z)
+__host__ __device__ constexpr int pcg_stage(int NT, bool) { return pad32((NT + 3) * kSP) + 2 * op_floats(NT); }
 
 template <int NT>
 __device__ __forceinline__ void tma_issue_pcg(float* stage, const PcgMaps& m, uint64_t* bar, int tx0, int ty0,
@@ -849,15 +890,18 @@ __device__ __forceinline__ void tma_issue_pcg(float* stage, const PcgMaps& m, ui
   }
 }
 
+
 template <int NT, bool TMA>
-__global__ void __launch_bounds__(kThreads, 3) k_pcg_apply(Frame f, Coef<float> c, const float* __restrict__ X,
+#ifndef LS_PCG_MINB
+#define LS_PCG_MINB 3
+#endif
+__global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Coef<float> c, const float* __restrict__ X,
                                                            const float* __restrict__ z,
                                                            const float* __restrict__ pprev,
                                                            float* __restrict__ pnew, float* __restrict__ q, double* part, unsigned* ticket,
                                                            Scalars* sc, int iter, int ntiles,
                                                            const __grid_constant__ PcgMaps maps) {
   constexpr int U = NT + 3;
-  constexpr int STAGE = pcg_stage(NT);
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bars[1];
   if (sc->stop) return;
@@ -865,7 +909,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_apply(Frame f, Coef<float> 
   const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
   const int cx = lx + kSX, cy = ly + 1, rx = lx + kRX, ry = ly + kHalf;
   const int ntx = (W + kTileW - 1) / kTileW;
-  const bool with_p = iter > 0;
+  const bool with_p = LS_ABLATE != 2 && iter > 0;
   const float beta = (float)sc->beta;
   float* sX = smem;
   float* sZT = smem + pad32(U * kSP);
@@ -892,6 +936,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_apply(Frame f, Coef<float> 
     const int tx0 = (tile % ntx) * kTileW, ty0 = (tile / ntx) * kTileH;
     const int x = tx0 + lx, y = ty0 + ly;
     const bool own = x < W && y < H;
+    const PixPre pre = pix_prefetch(f, x, y, own);
     if (TMA) {
       mbar_wait(&bars[0], phase);
       phase ^= 1u;
@@ -907,15 +952,28 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_apply(Frame f, Coef<float> 
       __syncthreads();
     }
     if (with_p) {   // operand p_i = z_i + beta_i p_{i-1} on the whole window
-      for (int e = threadIdx.x; e < NT * kSP; e += kThreads) sZT[e] = fmaf(beta, sPT[e], sZT[e]);
-      for (int e = threadIdx.x; e < 3 * kRP; e += kThreads) sZR[e] = fmaf(beta, sPR[e], sZR[e]);
+      // float4 over both regions (sizes and offsets are multiples of 4 words)
+      static_assert((NT * kSP) % 4 == 0 && (3 * kRP) % 4 == 0, "float4 operand formation");
+      auto form = [beta](float* zz, const float* pp, int n4) {
+        float4* z4 = reinterpret_cast<float4*>(zz);
+        const float4* p4 = reinterpret_cast<const float4*>(pp);
+        for (int e = threadIdx.x; e < n4; e += kThreads) {
+          float4 a = z4[e];
+          const float4 b = p4[e];
+          a.x = fmaf(beta, b.x, a.x); a.y = fmaf(beta, b.y, a.y);
+          a.z = fmaf(beta, b.z, a.z); a.w = fmaf(beta, b.w, a.w);
+          z4[e] = a;
+        }
+      };
+      form(sZT, sPT, NT * kSP / 4);
+      form(sZR, sPR, 3 * kRP / 4);
       __syncthreads();
     }
     const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H;
     if (interior)
-      acc += apply_pixel<NT, true>(f, c, sX, sZT, sZR, q, x, y, cx, cy, rx, ry);
+      acc += apply_pixel<NT, true>(f, c, sX, sZT, sZR, q, x, y, cx, cy, rx, ry, pre);
     else if (own)
-      acc += apply_pixel<NT, false>(f, c, sX, sZT, sZR, q, x, y, cx, cy, rx, ry);
+      acc += apply_pixel<NT, false>(f, c, sX, sZT, sZR, q, x, y, cx, cy, rx, ry, pre);
     if (own) {
       const int i = y * W + x;
       const int sc0 = cy * kSW + cx, rc0 = ry * kRW + rx;
@@ -1036,12 +1094,12 @@ template <int NT>
 static size_t apply_smem(bool tma) { return sizeof(float) * tile_floats(NT, true) * (tma ? 2 : 1); }
 
 template <int NT>
-static size_t pcg_smem() { return sizeof(float) * pcg_stage(NT); }
+static size_t pcg_smem(bool tma) { return sizeof(float) * pcg_stage(NT, tma); }
 
 template <int NT>
 static void prepare_nt() {
-  cudaFuncSetAttribute(k_pcg_apply<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcg_smem<NT>());
-  cudaFuncSetAttribute(k_pcg_apply<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcg_smem<NT>());
+  cudaFuncSetAttribute(k_pcg_apply<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcg_smem<NT>(true));
+  cudaFuncSetAttribute(k_pcg_apply<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcg_smem<NT>(false));
   cudaFuncSetAttribute(k_energy<NT, MODE_EG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)energy_smem<NT>(MODE_EG, true));
   cudaFuncSetAttribute(k_energy<NT, MODE_EG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1187,10 +1245,10 @@ static void launch_pcg_apply_nt(const Launch& L, const Frame& f, const Coef<floa
                                 const float* pprev, float* pnew, float* q, double* part, unsigned* ticket,
                                 Scalars* sc, int iter, const PcgMaps* maps) {
   if (maps)
-    k_pcg_apply<NT, true><<<L.grid, kThreads, pcg_smem<NT>(), L.stream>>>(f, c, X, z, pprev, pnew, q, part, ticket,
+    k_pcg_apply<NT, true><<<L.grid, kThreads, pcg_smem<NT>(true), L.stream>>>(f, c, X, z, pprev, pnew, q, part, ticket,
                                                                          sc, iter, L.ntiles, *maps);
   else
-    k_pcg_apply<NT, false><<<L.grid, kThreads, pcg_smem<NT>(), L.stream>>>(f, c, X, z, pprev, pnew, q, part, ticket,
+    k_pcg_apply<NT, false><<<L.grid, kThreads, pcg_smem<NT>(false), L.stream>>>(f, c, X, z, pprev, pnew, q, part, ticket,
                                                                           sc, iter, L.ntiles, PcgMaps{});
 }
 
@@ -1208,7 +1266,7 @@ void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, con
 int pcg_apply_grid_limit(int NT) {
   int nb = 0;
   LS_DISPATCH_NT(NT, (prepare_nt<NT_>(), cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                                             &nb, k_pcg_apply<NT_, true>, kThreads, pcg_smem<NT_>())));
+                                             &nb, k_pcg_apply<NT_, true>, kThreads, pcg_smem<NT_>(true))));
   return nb;
 }
 

@@ -1,0 +1,43 @@
+"""Timing ablations of k_pcg_apply: builds liblumisplit_b200 variants with
+-DLS_ABLATE=n into tools/_ablate/ (1: no consistency term, 2: no p formation,
+3: no smoothness, 4: no r-sparsity; n+100: the same with 4 CTAs/SM) and, with --run, times each through
+bench.py --profile-only.  Results are wrong by construction; timing only."""
+import json, os, subprocess, sys
+from pathlib import Path
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_1908_01961_b200 import build as B
+
+OUT = ROOT / "tools" / "_ablate"
+
+def build_variant(n, extra=()):
+    OUT.mkdir(exist_ok=True)
+    objs = []
+    procs = []
+    for src in B.SRC:
+        obj = OUT / f"{src.stem}_{n}.o"
+        cmd = [B.NVCC, *B.ARCH, *B.FLAGS, f"-DLS_ABLATE={n % 100}", *extra, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
+        procs.append(subprocess.Popen(cmd)); objs.append(str(obj))
+    assert all(p.wait() == 0 for p in procs)
+    so = OUT / f"lib_{n}.so"
+    subprocess.check_call([B.NVCC, *B.ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fPIC", *objs, "-o", str(so)])
+    return so
+
+if __name__ == "__main__":
+    variants = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 and sys.argv[1] != "--run" else [1, 2, 3, 4]
+    if "--run" not in sys.argv:
+        for n in variants:
+            build_variant(n, ["-DLS_PCG_MINB=4"] if n >= 100 else [])
+    else:
+        for n in [0] + variants:
+            env = dict(os.environ)
+            if n:
+                env["LS_LIB_PATH"] = str(OUT / f"lib_{n}.so")
+            r = subprocess.run([sys.executable, "bench.py", "--profile-only", "--steps", "5", "--warmup", "3"],
+                               env=env, capture_output=True, text=True, cwd=ROOT)
+            try:
+                d = json.loads(r.stdout.strip().splitlines()[-1])
+                pk = d["roofline"]["per_kernel"]
+                print(n, {k: round(v["avg_us"], 1) for k, v in pk.items()}, flush=True)
+            except Exception as e:
+                print(n, "failed", r.stderr[-800:], flush=True)

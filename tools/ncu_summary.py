@@ -89,7 +89,7 @@ def main():
     (prof / f"{tag}_ncu_summary.json").write_text(json.dumps(out, indent=1))
     traffic = {}
     for name, avg in summary.items():
-        base = name.split("<")[0]
+        base = name.split("<")[0].split("::")[-1]
         traffic[base] = avg["dram_bytes_per_launch"]
     (prof / "traffic.json").write_text(json.dumps(traffic, indent=1))
     md = [f"# ncu summary {tag}", "", f"report: `{rep}` (ncu --set full, --clock-control none)", "",
