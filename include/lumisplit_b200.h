@@ -201,6 +201,59 @@ LS_API int ls_svd_solve(ls_ctx* ctx, int n, const double* A_host, const double* 
 LS_API int ls_dense_step(ls_ctx* ctx, double* colors_inout_host, const float* X, double* applied_host,
                   ls_dense_record* rec);
 
+/* ---- Row bands (SURVEY.md 8(e), configs[3]: >= 4K frames split spatially) --
+ * One context per band of rows.  The context is created with the band's
+ * LOCAL frame: global rows [gy0, gy0 + H) of a GH-row frame, i.e. the band's
+ * own rows [y_lo, y_hi) plus up to 8 halo rows on each side that the caller
+ * keeps equal to the neighbouring bands' rows.  In band mode every reduction
+ * is written as this band's partial sum (ls_band_buffers()[0]); the caller
+ * gathers all bands' partials in band order ([nbands][nv] doubles, device)
+ * and ls_band_finalize runs the same finalisation the whole-frame kernels
+ * run, so every band takes identical scalar decisions.  The whole-frame entry
+ * points refuse a band context.  The orchestration (one GN step = EG, 16 x
+ * (apply, update), trials; halo refresh between phases) is
+ * paper_1908_01961_b200/bands.py.  Replaces no single reference function:
+ * the reference solves the frame as one problem (solver.py:143-192); the
+ * bands reproduce that problem's arithmetic up to the summation grouping. */
+enum { LS_BAND_EG = 0, LS_BAND_APPLY = 1, LS_BAND_UPDATE = 2, LS_BAND_TRIAL = 3 };
+LS_API int ls_band_set(ls_ctx* ctx, int gy0, int GH, int y_lo, int y_hi);
+LS_API int ls_band_clear(ls_ctx* ctx);
+/* out[6] = {partials (512 doubles), z, p_even, p_odd, x, r}: the PCG vectors
+ * (U planes of H*W floats each) whose halo rows the caller refreshes. */
+LS_API int ls_band_buffers(ls_ctx* ctx, void** out);
+/* Raw PCG64 u32 zeros (the Lemire rejections of energy.py:162-171) at stream
+ * positions [begin, end): list (device, 17 int64) = {count, positions...}.
+ * The bands split [0, 12*GH*W + 64) and gather their lists; the gathered
+ * lists (device, n_lists x 17) are handed to ls_band_set_zeros before the
+ * band's ls_sample_consistency, which then draws with global pixel indices. */
+LS_API int ls_band_zero_scan(ls_ctx* ctx, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                             uint64_t inc_lo, uint64_t begin, uint64_t end, int64_t* list);
+LS_API int ls_band_set_zeros(ls_ctx* ctx, const int64_t* lists, int n_lists);
+/* Phases of one GN step (solver.py:143-192), each writing its band partial:
+ * EG (energies at X, b, diag, PCG init; nv = 10), apply (iteration iter,
+ * p-update + J^T J p; nv = 1), update (nv = 2), trial (energies at
+ * X + alpha*x into X_out, or at X itself when X_out is NULL; nv = 8). */
+LS_API int ls_band_eg(ls_ctx* ctx, const double* colors_host, const float* X);
+LS_API int ls_band_pcg_apply(ls_ctx* ctx, const double* colors_host, const float* X, int iter);
+LS_API int ls_band_pcg_update(ls_ctx* ctx, int iter);
+LS_API int ls_band_trial(ls_ctx* ctx, const double* colors_host, const float* X, double alpha, float* X_out);
+LS_API int ls_band_finalize(ls_ctx* ctx, int phase, const double* gathered, int nbands, int iter, double alpha);
+/* host out[21]: terms0[8], terms1[8], |b|^2, |r|^2, iterations, stop, xinit */
+LS_API int ls_band_read(ls_ctx* ctx, double* out_host);
+/* Dense system (energy.py:563-610) of the band's own pixels as partial sums
+ * (ls_band_dense_nsums() doubles); ls_band_dense_solve sums the gathered
+ * partials in band order, assembles and solves (solver.py:195-204). */
+LS_API int ls_band_dense_accum(ls_ctx* ctx, const double* colors_host, const float* X, int use_ids);
+LS_API int ls_band_dense_nsums(ls_ctx* ctx);
+LS_API int ls_band_dense_solve(ls_ctx* ctx, const double* colors_host, const double* gathered, int nbands,
+                               int use_ids, double* dx_host);
+/* segment (palette.py:195-224) per band: summary (device, 3 int32) = {has a
+ * non-dark own pixel, first id, last id}; with every band's summary gathered
+ * (device, nbands x 3) the final ids of the own rows follow the reference's
+ * raster-order dark-pixel inheritance across band boundaries. */
+LS_API int ls_band_segment(ls_ctx* ctx, const double* colors_host, int32_t* summary);
+LS_API int ls_band_segment_final(ls_ctx* ctx, const int32_t* summaries, int nbands, int band, int32_t* ids_out);
+
 #ifdef __cplusplus
 }
 #endif

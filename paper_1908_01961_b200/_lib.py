@@ -89,7 +89,26 @@ SIGNATURES = {
     "ls_dense_normal": [P, DBL_P, P, C.c_int, DBL_P, DBL_P],
     "ls_svd_solve": [P, C.c_int, DBL_P, DBL_P, C.c_double, DBL_P],
     "ls_dense_step": [P, DBL_P, P, DBL_P, C.POINTER(DenseRecord)],
+    # row bands
+    "ls_band_set": [P, C.c_int, C.c_int, C.c_int, C.c_int],
+    "ls_band_clear": [P],
+    "ls_band_buffers": [P, C.POINTER(C.c_void_p)],
+    "ls_band_zero_scan": [P, U64, U64, U64, U64, U64, U64, P],
+    "ls_band_set_zeros": [P, P, C.c_int],
+    "ls_band_eg": [P, DBL_P, P],
+    "ls_band_pcg_apply": [P, DBL_P, P, C.c_int],
+    "ls_band_pcg_update": [P, C.c_int],
+    "ls_band_trial": [P, DBL_P, P, C.c_double, P],
+    "ls_band_finalize": [P, C.c_int, P, C.c_int, C.c_int, C.c_double],
+    "ls_band_read": [P, DBL_P],
+    "ls_band_dense_accum": [P, DBL_P, P, C.c_int],
+    "ls_band_dense_nsums": [P],
+    "ls_band_dense_solve": [P, DBL_P, P, C.c_int, C.c_int, DBL_P],
+    "ls_band_segment": [P, DBL_P, P],
+    "ls_band_segment_final": [P, P, C.c_int, C.c_int, P],
 }
+BAND_EG, BAND_APPLY, BAND_UPDATE, BAND_TRIAL = 0, 1, 2, 3
+ZERO_LIST = 17          # 1 + kMaxRejections
 STRING_FUNCS = ("ls_version", "ls_last_error")
 
 _lib = None

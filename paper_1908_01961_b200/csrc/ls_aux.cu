@@ -160,6 +160,7 @@ __global__ void k_sample(SampleParams P, const SampleState* __restrict__ Sg, con
   if (!Sg->redo) return;
   const int nz = Sg->nz;
   const int N = H * W;
+  const unsigned long long Ng = (unsigned long long)P.Ng, goff = (unsigned long long)P.goff;
   const u128 s0 = mk128(P.st_hi, P.st_lo), inc = mk128(P.inc_hi, P.inc_lo);
   const int nthreads = (N + kSamplePix - 1) / kSamplePix;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nthreads; t += gridDim.x * blockDim.x) {
@@ -172,7 +173,7 @@ __global__ void k_sample(SampleParams P, const SampleState* __restrict__ Sg, con
     // dx then dy: rng.integers(-7, 8, size=(n, 4)) -> Lemire on range 15,
     // reject iff (u * 15) mod 2^32 < (2^32 mod 15) = 1, i.e. u == 0
     for (int sec = 0; sec < 2; ++sec) {
-      unsigned long long pos = shifted_pos(Sg, nz, (unsigned long long)sec * 4ULL * N + 4ULL * p0);
+      unsigned long long pos = shifted_pos(Sg, nz, (unsigned long long)sec * 4ULL * Ng + 4ULL * (goff + p0));
       st.seek(s0, inc, pos);
 #pragma unroll
       for (int d = 0; d < 4 * kSamplePix; ++d) {
@@ -190,7 +191,7 @@ __global__ void k_sample(SampleParams P, const SampleState* __restrict__ Sg, con
       }
     }
     if (P.has_prev) {   // rng.integers(0, 2): Lemire threshold 0, no rejection
-      st.seek(s0, inc, shifted_pos(Sg, nz, 8ULL * N + 4ULL * p0));
+      st.seek(s0, inc, shifted_pos(Sg, nz, 8ULL * Ng + 4ULL * (goff + p0)));
 #pragma unroll
       for (int d = 0; d < 4 * kSamplePix; ++d) {
         if (d >= 4 * np) break;
@@ -210,11 +211,15 @@ __global__ void k_sample(SampleParams P, const SampleState* __restrict__ Sg, con
         const int dx = (int)((dxp[d >> 3] >> (4 * (d & 7))) & 15u) - kHalf;
         const int dy = (int)((dyp[d >> 3] >> (4 * (d & 7))) & 15u) - kHalf;
         const bool tk = (tp >> d) & 1u;
-        const int px = clampi(x + dx, 0, W - 1), py = clampi(y + dy, 0, H - 1);
-        const int q = py * W + px;
+        // partners are clipped to the global frame; in a row band a halo
+        // pixel's partner may fall outside the local rows (the pair touches
+        // no row of this band and is dropped)
+        const int px = clampi(x + dx, 0, W - 1), py = clampi(P.gy0 + y + dy, 0, P.GH - 1) - P.gy0;
+        const bool inside = py >= 0 && py < H;
+        const int q = inside ? py * W + px : p;
         const double* src = tk ? pch : ch;
         const double dist = norm2d(__dsub_rn(c0, src[q]), __dsub_rn(c1, src[N + q]));
-        const bool keep = (dist < 0.05) && (tk || q != p);
+        const bool keep = inside && (dist < 0.05) && (tk || q != p);
         int16_t code = -1;
         if (keep) {
           code = (int16_t)make_ent(py - y, px - x, tk, false);
@@ -233,6 +238,49 @@ __global__ void k_sample_init(SampleState* S) {
   S->redo = 1;
   S->error = 0;
   S->new_zero = ~0ULL;
+}
+
+// row bands: every rejection position of the stream is known up front (the
+// bands' zero scans, gathered): load them sorted; the draw pass then finds no
+// new ones.  lists: n_lists x kZeroList (count, positions...)
+__global__ void k_sample_init_known(SampleState* S, const long long* lists, int n_lists) {
+  S->nz = 0;
+  S->redo = 1;
+  S->error = 0;
+  S->new_zero = ~0ULL;
+  for (int l = 0; l < n_lists; ++l) {
+    const long long cnt = lists[(size_t)l * kZeroList];
+    if (cnt > kMaxRejections) S->error = 1;
+    for (int i = 0; i < cnt && i < kMaxRejections; ++i) {
+      const long long z = lists[(size_t)l * kZeroList + 1 + i];
+      if (S->nz >= kMaxRejections) { S->error = 1; break; }
+      int at = S->nz;
+      while (at > 0 && S->z[at - 1] > z) { S->z[at] = S->z[at - 1]; --at; }
+      S->z[at] = z;
+      S->nz += 1;
+    }
+  }
+}
+
+constexpr int kScanPerThread = 256;
+__global__ void k_zero_scan(SampleParams P, unsigned long long begin, unsigned long long end, long long* list) {
+  const u128 s0 = mk128(P.st_hi, P.st_lo), inc = mk128(P.inc_hi, P.inc_lo);
+  const unsigned long long n = end > begin ? end - begin : 0;
+  const unsigned long long nth = (n + kScanPerThread - 1) / kScanPerThread;
+  for (unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; t < nth;
+       t += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long p0 = begin + t * kScanPerThread;
+    U32Stream st;
+    st.seek(s0, inc, p0);
+    for (int d = 0; d < kScanPerThread; ++d) {
+      const unsigned long long pos = p0 + d;
+      if (pos >= end) break;
+      if (st.next() == 0u) {
+        const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(list), 1ULL);
+        if (k < kMaxRejections) list[1 + k] = (long long)pos;
+      }
+    }
+  }
 }
 
 // clears the adjacency counters before a (re)draw pass
@@ -401,8 +449,12 @@ __global__ void k_pairs_from_samples(const int16_t* __restrict__ codes, int H, i
 }
 
 // ---- segmentation (palette.py:195-224) --------------------------------------
+// own_lo/own_hi: flat index range of the pixels whose ids are produced (a
+// row band's own rows); pixels before it do not take part in the dark-pixel
+// scan (palette.py:209-219), the band's carry-in id stands in for them
 __global__ void k_segment_raw(const float* __restrict__ img, const double* __restrict__ ch, int N, int K,
-                              const PalChroma pal, int32_t* ids_raw, int32_t* key, int* first_valid) {
+                              const PalChroma pal, int32_t* ids_raw, int32_t* key, int* first_valid, int own_lo,
+                              int own_hi) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     const double c0 = ch[i], c1 = ch[N + i];
     int best = 0;
@@ -414,8 +466,43 @@ __global__ void k_segment_raw(const float* __restrict__ img, const double* __res
     ids_raw[i] = best + 1;
     const double s = __dadd_rn(__dadd_rn((double)img[i], (double)img[N + i]), (double)img[2 * N + i]);
     const bool dark = s < 0.02;
-    key[i] = dark ? -1 : i;
-    if (!dark) atomicMin(first_valid, i);
+    const bool own = i >= own_lo && i < own_hi;
+    key[i] = (dark || i < own_lo) ? -1 : i;
+    if (!dark && own) atomicMin(first_valid, i);
+  }
+}
+
+// band summary of its own rows: {has a non-dark pixel, id of the first, id of
+// the last}
+__global__ void k_segment_summary(const int32_t* __restrict__ ids_raw, const int32_t* __restrict__ last,
+                                  const int* first_valid, int own_hi, int* summary) {
+  const int fv = *first_valid;
+  const bool has = fv < own_hi;
+  summary[0] = has ? 1 : 0;
+  summary[1] = has ? ids_raw[fv] : 0;
+  summary[2] = has ? ids_raw[last[own_hi - 1]] : 0;
+}
+
+// ids of a band's own rows given every band's summary (band order): a dark
+// pixel with no non-dark pixel before it in the band takes the last non-dark
+// id of an earlier band, else the frame's first non-dark id, else 1
+__global__ void k_segment_band_final(int N, const int32_t* __restrict__ ids_raw, const int32_t* __restrict__ last,
+                                     const int* __restrict__ summaries, int nbands, int band, int own_lo, int own_hi,
+                                     int32_t* ids) {
+  __shared__ int carry;
+  if (threadIdx.x == 0) {
+    int cval = -1;
+    for (int b = band - 1; b >= 0 && cval < 0; --b)
+      if (summaries[3 * b]) cval = summaries[3 * b + 2];
+    for (int b = 0; b < nbands && cval < 0; ++b)
+      if (summaries[3 * b]) cval = summaries[3 * b + 1];
+    carry = cval < 0 ? 1 : cval;
+  }
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    if (i < own_lo || i >= own_hi) { ids[i] = ids_raw[i]; continue; }   // halo rows: unused
+    const int l = last[i];
+    ids[i] = l >= 0 ? ids_raw[l] : carry;
   }
 }
 
@@ -475,15 +562,22 @@ void launch_edge(cudaStream_t s, const double* chroma, int H, int W, float* edge
 }
 void launch_sample(cudaStream_t s, const SampleParams& P, SampleState* S, const double* chroma,
                    const double* prev_chroma, int H, int W, int16_t* codes, int32_t* out_cnt, int32_t* in_cnt,
-                   int passes) {
+                   int passes, const long long* known, int n_known_lists) {
   const int N = H * W;
   const int nthreads = (N + kSamplePix - 1) / kSamplePix;
-  k_sample_init<<<1, 1, 0, s>>>(S);
+  if (known) k_sample_init_known<<<1, 1, 0, s>>>(S, known, n_known_lists);
+  else k_sample_init<<<1, 1, 0, s>>>(S);
   for (int pass = 0; pass < passes; ++pass) {
     k_sample_zero<<<grid_for(N + 1), 256, 0, s>>>(S, N + 1, out_cnt, in_cnt);
     k_sample<<<grid_for(nthreads, 128), 128, 0, s>>>(P, S, chroma, prev_chroma, H, W, codes, out_cnt, in_cnt, S);
     k_sample_fix<<<1, 1, 0, s>>>(S, pass == passes - 1);
   }
+}
+void launch_zero_scan(cudaStream_t s, const SampleParams& P, unsigned long long begin, unsigned long long end,
+                      long long* list) {
+  cudaMemsetAsync(list, 0, sizeof(long long) * kZeroList, s);
+  const unsigned long long nth = ((end > begin ? end - begin : 0) + kScanPerThread - 1) / kScanPerThread;
+  if (nth) k_zero_scan<<<grid_for((int64_t)nth, 128), 128, 0, s>>>(P, begin, end, list);
 }
 void launch_pairs_count(cudaStream_t s, int64_t n, const int64_t* src, const int64_t* dst, const uint8_t* temporal,
                         int H, int W, int32_t* out_cnt, int32_t* in_cnt, int* bad) {
@@ -510,7 +604,19 @@ void launch_pairs_from_samples(cudaStream_t s, const int16_t* codes, int H, int 
 }
 void launch_segment_raw(cudaStream_t s, const float* img, const double* chroma, int N, int K, const PalChroma& pal,
                         int32_t* ids_raw, int32_t* key, int* first_valid) {
-  k_segment_raw<<<grid_for(N), 256, 0, s>>>(img, chroma, N, K, pal, ids_raw, key, first_valid);
+  k_segment_raw<<<grid_for(N), 256, 0, s>>>(img, chroma, N, K, pal, ids_raw, key, first_valid, 0, N);
+}
+void launch_segment_band(cudaStream_t s, const float* img, const double* chroma, int N, int K, const PalChroma& pal,
+                         int32_t* ids_raw, int32_t* key, int* first_valid, int own_lo, int own_hi) {
+  k_segment_raw<<<grid_for(N), 256, 0, s>>>(img, chroma, N, K, pal, ids_raw, key, first_valid, own_lo, own_hi);
+}
+void launch_segment_summary(cudaStream_t s, const int32_t* ids_raw, const int32_t* last, const int* first_valid,
+                            int own_hi, int* summary) {
+  k_segment_summary<<<1, 1, 0, s>>>(ids_raw, last, first_valid, own_hi, summary);
+}
+void launch_segment_band_final(cudaStream_t s, int N, const int32_t* ids_raw, const int32_t* last,
+                               const int* summaries, int nbands, int band, int own_lo, int own_hi, int32_t* ids) {
+  k_segment_band_final<<<grid_for(N), 256, 0, s>>>(N, ids_raw, last, summaries, nbands, band, own_lo, own_hi, ids);
 }
 void launch_segment_final(cudaStream_t s, int N, const int32_t* ids_raw, const int32_t* last, const int* first_valid,
                           int32_t* ids) {

@@ -138,6 +138,16 @@ struct ls_ctx {
   StepRecord* recs = nullptr;    // device step records
   StepRecord* recs_host = nullptr;
   FrameCtl* ctl_host = nullptr;
+  // row band: this context holds local rows
+  // [0, H) = global rows [gy0, gy0 + H) of a GH-row frame and produces rows
+  // [y_lo, y_hi); kernels then write partial sums to bsum (band_partial)
+  int gy0 = 0, GH = 0, y_lo = 0, y_hi = 0;
+  bool band_partial = false;
+  double* bsum = nullptr;        // 512 doubles
+  long long* zlist = nullptr;    // kZeroList
+  int* seg_sum = nullptr;        // 4 ints
+  const long long* band_zeros = nullptr;   // gathered zero lists (caller memory) for the next draw
+  int band_zero_lists = 0;
   std::vector<void*> allocs;
 };
 
@@ -196,7 +206,29 @@ static Frame frame_of(const ls_ctx* c) {
   f.row_ptr = c->row_ptr;
   f.ent = c->ent;
   f.ent_w = c->has_ent_w ? c->ent_w : nullptr;
+  f.y_lo = c->y_lo;
+  f.y_hi = c->y_hi;
+  f.bsum = c->band_partial ? c->bsum : nullptr;
   return f;
+}
+
+// tile / grid geometry of the produced rows [y_lo, y_hi)
+static void set_geometry(ls_ctx* c) {
+  const int rows = c->y_hi - c->y_lo;
+  c->ntiles = ((c->W + kTileW - 1) / kTileW) * ((rows + kTileH - 1) / kTileH);
+  c->grid_energy = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, energy_grid_limit(c->NT)), kMaxBlocks}));
+  c->grid_apply = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, apply_grid_limit(c->NT)), kMaxBlocks}));
+  c->grid_pcg = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, pcg_apply_grid_limit(c->NT)), kMaxBlocks}));
+  const int64_t M = (int64_t)c->U * rows * c->W;
+  const int64_t upd_blocks = (M / 4 + kThreads - 1) / kThreads;
+  c->grid_update = (int)std::max<int64_t>(1, std::min<int64_t>({upd_blocks, (int64_t)c->nsm * std::max(1, update_grid_limit()), (int64_t)kMaxBlocks}));
+  c->grid_dense = std::max(1, std::min(c->nsm * 4, (rows * c->W + 127) / 128));
+}
+
+// the whole-frame entry points finalise inside their kernels
+static int whole_frame_only(ls_ctx* c) {
+  LS_ARG(c && !c->band_partial, "context is a row band: use the ls_band_* entry points");
+  return LS_OK;
 }
 
 extern "C" int ls_pair_count(ls_ctx* c, int64_t* n_pairs, int64_t* n_temporal, int64_t* n_entries);
@@ -256,13 +288,9 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   c->nsm = prop.multiProcessorCount;
   const int N = c->N, U = c->U;
   const int64_t M = (int64_t)U * N;
-  c->ntiles = ((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH);
-  c->grid_energy = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, energy_grid_limit(c->NT)), kMaxBlocks}));
-  c->grid_apply = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, apply_grid_limit(c->NT)), kMaxBlocks}));
-  c->grid_pcg = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, pcg_apply_grid_limit(c->NT)), kMaxBlocks}));
-  const int64_t upd_blocks = (M / 4 + kThreads - 1) / kThreads;
-  c->grid_update = (int)std::max<int64_t>(1, std::min<int64_t>({upd_blocks, (int64_t)c->nsm * std::max(1, update_grid_limit()), (int64_t)kMaxBlocks}));
-  c->grid_dense = std::max(1, std::min(c->nsm * 4, (N + 127) / 128));
+  c->GH = H;
+  c->y_hi = H;
+  set_geometry(c);
   c->use_tma = (W % 4 == 0) && tma_encode_fn() != nullptr && std::getenv("LS_NO_TMA") == nullptr;
   cudaError_t e = cudaSuccess;
 #define A_(expr) \
@@ -302,6 +330,9 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   A_(dalloc(c, &c->dense_A, 36 * 36));
   A_(dalloc(c, &c->dense_rhs, 36));
   A_(dalloc(c, &c->dense_x, 36));
+  A_(dalloc(c, &c->bsum, 512));
+  A_(dalloc(c, &c->zlist, kZeroList));
+  A_(dalloc(c, &c->seg_sum, 4));
   A_(cudaMallocHost((void**)&c->sc_host, sizeof(Scalars)));
   A_(dalloc(c, &c->ctl, 1));
   A_(dalloc(c, &c->recs, kMaxStepRecords));
@@ -486,9 +517,16 @@ int ls_sample_consistency(ls_ctx* c, const double* chroma, const double* prev_ch
   P.inc_hi = inc_hi;
   P.inc_lo = inc_lo;
   P.has_prev = prev_chroma ? 1 : 0;
-  // draws + device-side rejection re-passes: no host synchronisation
+  P.gy0 = c->gy0;
+  P.GH = c->GH;
+  P.goff = (long long)c->gy0 * c->W;
+  P.Ng = (long long)c->GH * c->W;
+  // draws + device-side rejection re-passes: no host synchronisation.  A row
+  // band gets every rejection of the stream up front (ls_band_set_zeros).
   launch_sample(c->stream, P, c->sstate, cur, prev_chroma, c->H, c->W, c->codes, c->out_cnt, c->in_cnt,
-                kSamplePasses);
+                kSamplePasses, c->band_zeros, c->band_zero_lists);
+  c->band_zeros = nullptr;
+  c->band_zero_lists = 0;
   launch_degree(c->stream, N, c->out_cnt, c->in_cnt, c->deg);
   LS_CK(cudaMemsetAsync(c->deg + N, 0, sizeof(int32_t), c->stream));
   size_t bytes = c->cub_bytes;
@@ -670,7 +708,8 @@ static Launch L_apply(ls_ctx* c) { return Launch{c->grid_apply, c->ntiles, c->st
 static Launch L_update(ls_ctx* c) { return Launch{c->grid_update, 0, c->stream}; }
 
 int ls_energy_terms(ls_ctx* c, const double* colors, const float* X, const float* Y, double* terms) {
-  int rc = check_ready(c);
+  int rc = whole_frame_only(c);
+  if (!rc) rc = check_ready(c);
   if (rc) return rc;
   LS_ARG(colors || c->K == 0, "null palette");
   LS_ARG(X && Y && terms, "bad arguments");
@@ -757,7 +796,8 @@ static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, f
 }
 
 int ls_pcg(ls_ctx* c, const double* colors, const float* X, int iterations, float* x, double* info) {
-  int rc = check_ready(c);
+  int rc = whole_frame_only(c);
+  if (!rc) rc = check_ready(c);
   if (rc) return rc;
   LS_ARG(X && x && info && iterations >= 0, "bad arguments");
   LS_CK(cudaSetDevice(c->dev));
@@ -779,7 +819,8 @@ static double sum_terms(const double* t) {
 }
 
 int ls_gn_step(ls_ctx* c, const double* colors, const float* X, float* X_out, ls_gn_record* rec) {
-  int rc = check_ready(c);
+  int rc = whole_frame_only(c);
+  if (!rc) rc = check_ready(c);
   if (rc) return rc;
   LS_ARG(X && X_out && rec && X != X_out, "bad arguments");
   LS_CK(cudaSetDevice(c->dev));
@@ -846,7 +887,8 @@ int ls_gn_step(ls_ctx* c, const double* colors, const float* X, float* X_out, ls
 extern "C" int ls_flip_flop_stream(ls_ctx* c, const double* colors, float* X0, float* X1, float* X2, int outer,
                                    int gn_steps, double tol_rel, ls_gn_record* out, int* n_records, int* status,
                                    int* final_buffer, int* fault_step) {
-  int rc = check_ready(c);
+  int rc = whole_frame_only(c);
+  if (!rc) rc = check_ready(c);
   if (rc) return rc;
   LS_ARG(X0 && X1 && X2 && out && n_records && status && final_buffer && fault_step, "bad arguments");
   LS_ARG(outer >= 0 && gn_steps >= 0 && (int64_t)outer * gn_steps <= kMaxStepRecords, "too many GN steps");
@@ -957,7 +999,8 @@ int ls_svd_solve(ls_ctx* c, int n, const double* A, const double* rhs, double tr
 }
 
 int ls_dense_step(ls_ctx* c, double* colors, const float* X, double* applied, ls_dense_record* rec) {
-  int rc = check_ready(c);
+  int rc = whole_frame_only(c);
+  if (!rc) rc = check_ready(c);
   if (rc) return rc;
   LS_ARG(colors && X && applied && rec, "bad arguments");
   LS_ARG(c->K >= 1, "dense step needs K >= 1");
@@ -1022,6 +1065,241 @@ int ls_dense_step(ls_ctx* c, double* colors, const float* X, double* applied, ls
   rec->energy_after = accepted ? e1 : e0;
   rec->accepted = accepted ? 1 : 0;
   rec->alpha = accepted ? alpha : 0.0;
+  return LS_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// Row bands: one context per band of
+// rows, every reduction written as a band partial and finalised from the
+// band-ordered sum of all bands' partials (gathered by the host: a local
+// copy on one GPU, an NCCL all-gather across GPUs).  Halo rows are refreshed
+// by the host between the calls (ls_band_buffers).
+// ---------------------------------------------------------------------------
+static int band_ready(ls_ctx* c) {
+  LS_ARG(c && c->band_partial, "not a row band (ls_band_set first)");
+  return check_ready(c);
+}
+
+int ls_band_set(ls_ctx* c, int gy0, int GH, int y_lo, int y_hi) {
+  LS_ARG(c, "null context");
+  LS_ARG(0 <= y_lo && y_lo < y_hi && y_hi <= c->H, "band rows must satisfy 0 <= y_lo < y_hi <= H");
+  LS_ARG(gy0 >= 0 && (int64_t)gy0 + c->H <= GH, "band outside the frame");
+  LS_ARG(c->W % 4 == 0, "row bands need W % 4 == 0");
+  c->gy0 = gy0;
+  c->GH = GH;
+  c->y_lo = y_lo;
+  c->y_hi = y_hi;
+  c->band_partial = true;
+  set_geometry(c);
+  return LS_OK;
+}
+
+int ls_band_clear(ls_ctx* c) {
+  LS_ARG(c, "null context");
+  c->gy0 = 0;
+  c->GH = c->H;
+  c->y_lo = 0;
+  c->y_hi = c->H;
+  c->band_partial = false;
+  set_geometry(c);
+  return LS_OK;
+}
+
+int ls_band_buffers(ls_ctx* c, void** out) {
+  LS_ARG(c && out, "bad arguments");
+  out[0] = c->bsum;
+  out[1] = c->u;
+  out[2] = c->p;
+  out[3] = c->s;
+  out[4] = c->x;
+  out[5] = c->r;
+  return LS_OK;
+}
+
+int ls_band_zero_scan(ls_ctx* c, uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t begin,
+                      uint64_t end, int64_t* list) {
+  LS_ARG(c && list && end >= begin, "bad arguments");
+  LS_CK(cudaSetDevice(c->dev));
+  SampleParams P;
+  std::memset(&P, 0, sizeof(P));
+  P.st_hi = st_hi;
+  P.st_lo = st_lo;
+  P.inc_hi = inc_hi;
+  P.inc_lo = inc_lo;
+  launch_zero_scan(c->stream, P, begin, end, reinterpret_cast<long long*>(list));
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_set_zeros(ls_ctx* c, const int64_t* lists, int n_lists) {
+  LS_ARG(c && lists && n_lists >= 1, "bad arguments");
+  c->band_zeros = reinterpret_cast<const long long*>(lists);
+  c->band_zero_lists = n_lists;
+  return LS_OK;
+}
+
+int ls_band_eg(ls_ctx* c, const double* colors, const float* X) {
+  int rc = band_ready(c);
+  if (rc) return rc;
+  LS_ARG(X, "bad arguments");
+  const Frame f = frame_of(c);
+  const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
+  EnergyMaps em;
+  const bool etma = energy_maps(c, X, nullptr, &em);
+  const size_t pi = prof_begin(c);
+  launch_energy(0, L_energy(c), f, cd, X, nullptr, 0.f, nullptr, nullptr, c->r, c->d, c->u, nullptr, nullptr,
+                c->part, c->tickets + 0, c->sc, etma ? &em : nullptr);
+  prof_end(c, PC_EG, pi);
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_pcg_apply(ls_ctx* c, const double* colors, const float* X, int iter) {
+  int rc = band_ready(c);
+  if (rc) return rc;
+  LS_ARG(X && iter >= 0, "bad arguments");
+  const Frame f = frame_of(c);
+  const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
+  float* pbuf[2] = {c->p, c->s};
+  PcgMaps maps;
+  const bool tma = pcg_maps(c, X, pbuf[(iter + 1) & 1], &maps);
+  const Launch La{c->grid_pcg, c->ntiles, c->stream};
+  const size_t pi = prof_begin(c);
+  launch_pcg_apply(La, f, cd, X, c->u, pbuf[(iter + 1) & 1], pbuf[iter & 1], c->wv, c->part, c->tickets + 1, c->sc,
+                   iter, tma ? &maps : nullptr);
+  prof_end(c, PC_APPLY, pi);
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_pcg_update(ls_ctx* c, int iter) {
+  int rc = band_ready(c);
+  if (rc) return rc;
+  LS_ARG(iter >= 0, "bad arguments");
+  const Frame f = frame_of(c);
+  float* pbuf[2] = {c->p, c->s};
+  const int64_t M = (int64_t)c->U * c->N;
+  const size_t pi = prof_begin(c);
+  launch_pcg_update(L_update(c), M, c->r, c->wv, c->d, c->u, pbuf[iter & 1], c->x, c->part, c->tickets + 2, c->sc,
+                    iter, &f);
+  prof_end(c, PC_UPDATE, pi);
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_trial(ls_ctx* c, const double* colors, const float* X, double alpha, float* X_out) {
+  int rc = band_ready(c);
+  if (rc) return rc;
+  LS_ARG(X, "bad arguments");
+  const Frame f = frame_of(c);
+  const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
+  EnergyMaps em;
+  const float* dx = X_out ? c->x : nullptr;   // X_out == NULL: energies at X itself
+  const bool etma = energy_maps(c, X, dx, &em);
+  const size_t pi = prof_begin(c);
+  launch_energy(1, L_energy(c), f, cd, X, dx, (float)alpha, nullptr, X_out, nullptr, nullptr, nullptr, nullptr,
+                nullptr, c->part, c->tickets + 0, c->sc, etma ? &em : nullptr);
+  prof_end(c, PC_TRIAL, pi);
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_finalize(ls_ctx* c, int phase, const double* gathered, int nbands, int iter, double alpha) {
+  LS_ARG(c && c->band_partial && gathered && nbands >= 1, "bad arguments");
+  LS_ARG(phase >= BAND_EG && phase <= BAND_TRIAL, "bad band phase");
+  const int nv = phase == BAND_EG ? kTerms + 2 : phase == BAND_APPLY ? 1 : phase == BAND_UPDATE ? 2 : kTerms;
+  launch_band_finalize(c->stream, phase, gathered, nbands, nv, c->sc, iter, (float)alpha, 0, 0);
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_read(ls_ctx* c, double* out) {
+  LS_ARG(c && out, "bad arguments");
+  LS_CK(cudaMemcpyAsync(c->sc_host, c->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaStreamSynchronize(c->stream));
+  prof_harvest(c);
+  const Scalars& s = *c->sc_host;
+  for (int j = 0; j < kTerms; ++j) {
+    out[j] = s.terms0[j];
+    out[kTerms + j] = s.terms1[j];
+  }
+  out[16] = s.bnorm2;
+  out[17] = s.rnorm2;
+  out[18] = s.iterations;
+  out[19] = s.stop;
+  out[20] = s.xinit;
+  return LS_OK;
+}
+
+int ls_band_dense_accum(ls_ctx* c, const double* colors, const float* X, int use_ids) {
+  LS_ARG(c && c->band_partial && c->has_image && colors && X, "bad arguments");
+  LS_ARG(c->K >= 1, "dense system needs K >= 1");
+  LS_ARG(!use_ids || c->has_ids, "no cluster ids set");
+  LS_CK(cudaMemcpyAsync(c->colors_dev, colors, sizeof(double) * 3 * c->K, cudaMemcpyHostToDevice, c->stream));
+  const size_t pi = prof_begin(c);
+  launch_dense_accum(c->stream, c->grid_dense, frame_of(c), c->colors_dev, c->K, X, use_ids, c->part,
+                     c->tickets + 3, c->bsum);
+  prof_end(c, PC_DENSE, pi);
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_dense_nsums(ls_ctx* c) { return c ? dense_nsums(c->K) : 0; }
+
+int ls_band_dense_solve(ls_ctx* c, const double* colors, const double* gathered, int nbands, int use_ids,
+                        double* dx) {
+  LS_ARG(c && colors && gathered && dx && nbands >= 1, "bad arguments");
+  LS_ARG(c->K >= 1, "dense system needs K >= 1");
+  const int n = 3 * c->K;
+  LS_CK(cudaMemcpyAsync(c->colors_dev, colors, sizeof(double) * 3 * c->K, cudaMemcpyHostToDevice, c->stream));
+  launch_band_sum(c->stream, gathered, nbands, dense_nsums(c->K), c->dense_sums);
+  launch_dense_assemble_solve(c->stream, c->dense_sums, c->K, c->colors_dev, use_ids, c->w.lambda_data,
+                              c->w.lambda_clustering, c->w.lambda_ir, c->w.lambda_cr, c->w.chroma_reg,
+                              c->cfg.svd_truncation, c->dense_A, c->dense_rhs, c->dense_x);
+  c->launches += 2;
+  LS_CK(cudaGetLastError());
+  LS_CK(cudaMemcpyAsync(c->host_buf, c->dense_x, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaStreamSynchronize(c->stream));
+  std::memcpy(dx, c->host_buf, sizeof(double) * n);
+  return LS_OK;
+}
+
+int ls_band_segment(ls_ctx* c, const double* colors, int32_t* summary) {
+  LS_ARG(c && c->has_image && colors && summary, "bad arguments");
+  LS_ARG(c->K >= 1, "segment needs K >= 1");
+  const int N = c->N, K = c->K;
+  PalChroma pc;
+  std::memset(&pc, 0, sizeof(pc));
+  for (int k = 0; k < K; ++k) {   // chroma_of_color (imaging.py:174-180)
+    const double s = (colors[3 * k] + colors[3 * k + 1]) + colors[3 * k + 2];
+    pc.c[2 * k] = s > 1e-12 ? colors[3 * k] / s : 1.0 / 3.0;
+    pc.c[2 * k + 1] = s > 1e-12 ? colors[3 * k + 1] / s : 1.0 / 3.0;
+  }
+  const int own_lo = c->y_lo * c->W, own_hi = c->y_hi * c->W;
+  launch_set_i32(c->stream, c->small_i + 2, 1, N);
+  launch_segment_band(c->stream, c->img, c->chroma, N, K, pc, c->seg_raw, c->seg_key, c->small_i + 2, own_lo, own_hi);
+  size_t bytes = c->cub_bytes;
+  LS_CK(cub::DeviceScan::InclusiveScan(c->cub_tmp, bytes, c->seg_key, c->seg_last, MaxOp(), N, c->stream));
+  launch_segment_summary(c->stream, c->seg_raw, c->seg_last, c->small_i + 2, own_hi, summary);
+  c->launches += 4;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_segment_final(ls_ctx* c, const int32_t* summaries, int nbands, int band, int32_t* ids_out) {
+  LS_ARG(c && summaries && ids_out && nbands >= 1 && band >= 0 && band < nbands, "bad arguments");
+  launch_segment_band_final(c->stream, c->N, c->seg_raw, c->seg_last, summaries, nbands, band, c->y_lo * c->W,
+                            c->y_hi * c->W, ids_out);
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
   return LS_OK;
 }
 

@@ -62,6 +62,13 @@ struct Frame {
   const int32_t* row_ptr; // N + 1
   const uint16_t* ent;    // adjacency entries
   const float* ent_w;     // per-entry pair weight or nullptr (all 1)
+  // row band: the kernels produce rows [y_lo, y_hi)
+  // of this H x W local frame; rows outside are halo copies of the
+  // neighbouring bands.  A whole frame is y_lo = 0, y_hi = H.
+  int y_lo, y_hi;
+  // band partial mode: the last CTA writes its reduced sums here instead of
+  // finalising the scalars (ls_band_finalize sums the bands in band order)
+  double* bsum;
 };
 
 // device-resident PCG / step scalars (textbook Jacobi PCG of solver.py:79-107

@@ -54,11 +54,13 @@ __global__ void __launch_bounds__(128) k_dense_accum(Frame f, const double* __re
   double acc[kDensePerLane];
 #pragma unroll
   for (int m = 0; m < kDensePerLane; ++m) acc[m] = 0.0;
-  const int nchunks = (N + 31) / 32;
+  // row bands: only the band's own rows [y_lo, y_hi)
+  const int i0 = f.y_lo * f.W, npx = (f.y_hi - f.y_lo) * f.W;
+  const int nchunks = (npx + 31) / 32;
   for (int chunk = blockIdx.x * 4 + wid; chunk < nchunks; chunk += gridDim.x * 4) {
-    const int i = chunk * 32 + lane;
+    const int i = i0 + chunk * 32 + lane;
     double* pv = pix[wid][lane];
-    if (i < N) {
+    if (chunk * 32 + lane < npx) {
       double S[3] = {0.0, 0.0, 0.0};
       for (int k = 0; k < NT; ++k) {
         const double t = (double)X[(size_t)(3 + k) * N + i];
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(128) k_dense_accum(Frame f, const double* __re
       for (int v = 0; v < 10 + K; ++v) pv[v] = 0.0;
     }
     __syncwarp();
-    const int np = min(32, N - chunk * 32);
+    const int np = min(32, npx - chunk * 32);
 #pragma unroll
     for (int m = 0; m < kDensePerLane; ++m) {
       const int e = lane + 32 * m;
@@ -122,6 +124,18 @@ __global__ void __launch_bounds__(128) k_dense_accum(Frame f, const double* __re
     sums[e] = s;
   }
   if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// band-ordered sum of gathered per-band partial sums [nbands][nv]
+__global__ void k_band_sum(const double* __restrict__ g, int nbands, int nv, double* out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nv; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nbands; ++b) s += g[(size_t)b * nv + j];
+    out[j] = s;
+  }
+}
+void launch_band_sum(cudaStream_t s, const double* gathered, int nbands, int nv, double* out) {
+  k_band_sum<<<1, 256, 0, s>>>(gathered, nbands, nv, out);
 }
 
 // ---- one-sided Jacobi SVD truncated solve, single CTA ---------------------

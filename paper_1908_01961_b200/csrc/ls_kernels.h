@@ -53,7 +53,13 @@ void launch_pcg_apply(const Launch& L, const Frame& f, const Coef<float>& c, con
                       const float* pprev, float* pnew, float* q, double* part, unsigned* ticket, Scalars* sc,
                       int iter, const PcgMaps* maps);
 void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
-                       const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter);
+                       const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter,
+                       const Frame* band = nullptr);
+// row bands: phases whose partial sums are gathered across bands
+enum BandPhase { BAND_EG = 0, BAND_APPLY = 1, BAND_UPDATE = 2, BAND_TRIAL = 3, BAND_DENSE = 4 };
+void launch_band_sum(cudaStream_t s, const double* gathered, int nbands, int nv, double* out);
+void launch_band_finalize(cudaStream_t s, int phase, const double* gathered, int nbands, int nv, Scalars* sc,
+                          int iter, float alpha, int dev_ls, int last_trial);
 int pcg_apply_grid_limit(int NT);
 int energy_grid_limit(int NT);
 void prepare_kernels(int NT);
@@ -64,6 +70,10 @@ int update_grid_limit();
 struct SampleParams {
   unsigned long long st_hi, st_lo, inc_hi, inc_lo;
   int has_prev;
+  // row bands: local pixel 0 is global flat pixel goff of a GH x W frame
+  // with Ng pixels (the PCG64 stream is indexed by global pixel)
+  int gy0, GH;
+  long long goff, Ng;
 };
 constexpr int kMaxRejections = 16;
 // device-resident rejection bookkeeping of the partner sampler
@@ -80,7 +90,12 @@ void launch_image(cudaStream_t s, const float* hwc, int N, float* img_planes, do
 void launch_edge(cudaStream_t s, const double* chroma, int H, int W, float* edge);
 void launch_sample(cudaStream_t s, const SampleParams& P, SampleState* S, const double* chroma,
                    const double* prev_chroma, int H, int W, int16_t* codes, int32_t* out_cnt, int32_t* in_cnt,
-                   int passes);
+                   int passes, const long long* known = nullptr, int n_known_lists = 0);
+// row bands: raw PCG64 u32 zeros (Lemire rejections) at stream positions
+// [begin, end) -> list[0] = count, list[1..] = positions (unsorted)
+constexpr int kZeroList = 1 + kMaxRejections;
+void launch_zero_scan(cudaStream_t s, const SampleParams& P, unsigned long long begin, unsigned long long end,
+                      long long* list);
 void launch_pairs_count(cudaStream_t s, int64_t n, const int64_t* src, const int64_t* dst,
                         const uint8_t* temporal, int H, int W, int32_t* out_cnt, int32_t* in_cnt, int* bad);
 void launch_degree(cudaStream_t s, int N, const int32_t* out_cnt, const int32_t* in_cnt, int32_t* deg);
@@ -97,6 +112,12 @@ struct PalChroma { double c[2 * (kMaxNT - 1)]; };   // palette chromas, by value
 struct PalColors { double c[3 * (kMaxNT - 1)]; };   // palette colors, by value
 void launch_segment_raw(cudaStream_t s, const float* img, const double* chroma, int N, int K,
                         const PalChroma& pal, int32_t* ids_raw, int32_t* key, int* first_valid);
+void launch_segment_band(cudaStream_t s, const float* img, const double* chroma, int N, int K, const PalChroma& pal,
+                         int32_t* ids_raw, int32_t* key, int* first_valid, int own_lo, int own_hi);
+void launch_segment_summary(cudaStream_t s, const int32_t* ids_raw, const int32_t* last, const int* first_valid,
+                            int own_hi, int* summary);
+void launch_segment_band_final(cudaStream_t s, int N, const int32_t* ids_raw, const int32_t* last,
+                               const int* summaries, int nbands, int band, int own_lo, int own_hi, int32_t* ids);
 void launch_segment_final(cudaStream_t s, int N, const int32_t* ids_raw, const int32_t* last,
                           const int* first_valid, int32_t* ids);
 void launch_initialize(cudaStream_t s, const float* img, const int32_t* ids, int N, int NT,

@@ -50,12 +50,6 @@ __host__ __device__ constexpr int off_T(int NT) { return pad32((NT + 3) * kSP); 
 __host__ __device__ constexpr int off_R(int NT, bool has_T) { return off_T(NT) + (has_T ? pad32(NT * kSP) : 0); }
 __host__ __device__ constexpr int tile_floats(int NT, bool has_T) { return off_R(NT, has_T) + pad32(3 * kRP); }
 
-__device__ __forceinline__ void tile_coords(int tile, int W, int& tx0, int& ty0) {
-  const int ntx = (W + kTileW - 1) / kTileW;
-  tx0 = (tile % ntx) * kTileW;
-  ty0 = (tile / ntx) * kTileH;
-}
-
 // MUFU reciprocal / rsqrt (one instruction).  The IRLS weights only have to
 // be the same deterministic function in every kernel; 1-ulp differences to
 // the fp64 reference are far below the solver's tolerance.
@@ -401,6 +395,75 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
   acc[kTerms + 1] += (double)bb;
 }
 
+
+// ---------------------------------------------------------------------------
+// finalisation of reduced sums: run by the last CTA of a kernel, or, for row
+// bands, by k_band_finalize on the band-ordered sum of every band's partials
+// ---------------------------------------------------------------------------
+__device__ void fin_energy_eg(const double* tot, Scalars* sc, bool pcg_init) {
+  bool finite = true;
+  for (int j = 0; j < kTerms; ++j) finite = finite && isfinite(tot[j]);
+  double e0 = 0.0;   // Python sum() order over the blocks (solver.py:139-140)
+  for (int j = 0; j < kTerms; ++j) e0 += tot[j];
+  sc->e0 = e0;
+  sc->ls_done = 0;
+  sc->accepted = 0;
+  sc->fault = 0;
+  sc->alpha_ls = 0.0;
+  sc->e1 = e0;
+  for (int j = 0; j < kTerms; ++j) sc->terms0[j] = tot[j];
+  sc->gamma = tot[kTerms];
+  sc->gamma_prev = 0.0;
+  sc->bnorm2 = tot[kTerms + 1];
+  sc->rnorm2 = tot[kTerms + 1];
+  sc->alpha = sc->alpha_prev = sc->beta = sc->delta = 0.0;
+  sc->iterations = 0;
+  sc->pending = 0;
+  sc->xinit = 0;
+  sc->plast = 0;
+  // zero rhs -> x = 0 (solver.py:85-86); non-finite -> host raises
+  sc->stop = (!finite || tot[kTerms + 1] == 0.0 || !pcg_init) ? 1 : 0;
+}
+
+__device__ void fin_energy_trial(const double* tot, Scalars* sc, float alpha, int dev_ls, int last_trial) {
+  for (int j = 0; j < kTerms; ++j) sc->terms1[j] = tot[j];
+  if (dev_ls) {   // accept / halve decision of solver.py:169-178 on the device
+    double e1 = 0.0;
+    for (int j = 0; j < kTerms; ++j) e1 += tot[j];
+    if (!isfinite(sc->e0)) {
+      sc->fault = 1;
+      sc->ls_done = 1;
+    } else if (isfinite(e1) && e1 <= sc->e0) {
+      sc->ls_done = 1;
+      sc->accepted = 1;
+      sc->alpha_ls = (double)alpha;
+      sc->e1 = e1;
+    } else if (last_trial) {
+      sc->ls_done = 1;
+    }
+  }
+}
+
+__device__ void fin_pcg_apply(double pap, Scalars* sc) {
+  sc->delta = pap;
+  if (!(pap > 0.0) || !isfinite(pap)) {
+    sc->stop = 1;                       // solver.py:95-96: break before the update
+  } else {
+    sc->alpha_prev = sc->alpha;
+    sc->alpha = sc->gamma / pap;
+  }
+}
+
+__device__ void fin_pcg_update(double rz, double rn, Scalars* sc, int iter) {
+  sc->iterations = iter + 1;
+  sc->xinit = 1;
+  sc->gamma_prev = sc->gamma;
+  sc->gamma = rz;
+  sc->rnorm2 = rn;
+  sc->beta = rz / sc->gamma_prev;
+  if (rz <= 0.0) sc->stop = 1;          // solver.py:101-103
+}
+
 template <int NT, int MODE, bool TMA>
 __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, const float* __restrict__ X,
                                                      const float* __restrict__ dx, float alpha,
@@ -443,7 +506,7 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
       for (int j = 0; j < NST; ++j) {
         const int t = blockIdx.x + j * gridDim.x;
         if (t < ntiles) tma_issue_energy<NT>(smem + j * STAGE, maps, &bars[j], (t % ntx) * kTileW,
-                                             (t / ntx) * kTileH, with_d);
+                                             f.y_lo + (t / ntx) * kTileH, with_d);
       }
     }
     __syncthreads();
@@ -452,7 +515,7 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
   for (int j = 0;; ++j) {
     const int tile = blockIdx.x + j * gridDim.x;
     if (tile >= ntiles) break;
-    const int tx0 = (tile % ntx) * kTileW, ty0 = (tile / ntx) * kTileH;
+    const int tx0 = (tile % ntx) * kTileW, ty0 = f.y_lo + (tile / ntx) * kTileH;
     const int st = (NST == 2) ? (j & 1) : 0;
     float* sX = smem + st * STAGE;
     float* sXR = sX + e_off_XR(NT);
@@ -480,18 +543,18 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
     }
     const float* sYT = with_d ? sD + 3 * kSP : sX + 3 * kSP;
     const float* sYR = with_d ? sDR : sXR;
-    const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H;
+    const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H && ty0 + kTileH <= f.y_hi;
     if (interior)
       energy_pixel<NT, MODE, true>(f, c, sX, sXR, sYT, sYR, tx0 + lx, ty0 + ly, cx, cy, rx, ry, Xout, r_out, d_out,
                                    u_out, b_raw, diag_raw, acc);
-    else if (tx0 + lx < W && ty0 + ly < H)
+    else if (tx0 + lx < W && ty0 + ly < f.y_hi)
       energy_pixel<NT, MODE, false>(f, c, sX, sXR, sYT, sYR, tx0 + lx, ty0 + ly, cx, cy, rx, ry, Xout, r_out, d_out,
                                     u_out, b_raw, diag_raw, acc);
     if (TMA) {
       __syncthreads();
       if (threadIdx.x == 0) {
         const int t = blockIdx.x + (j + NST) * gridDim.x;
-        if (t < ntiles) tma_issue_energy<NT>(sX, maps, &bars[st], (t % ntx) * kTileW, (t / ntx) * kTileH, with_d);
+        if (t < ntiles) tma_issue_energy<NT>(sX, maps, &bars[st], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH, with_d);
       }
     }
   }
@@ -502,46 +565,12 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
 #pragma unroll
   for (int j = 0; j < NV; ++j) tot[j] = sum_partials<NV>(part, gridDim.x, j);
   if (threadIdx.x == 0) {
-    bool finite = true;
-    for (int j = 0; j < kTerms; ++j) finite = finite && isfinite(tot[j]);
-    if (!TRIAL) {
-      double e0 = 0.0;   // Python sum() order over the blocks (solver.py:139-140)
-      for (int j = 0; j < kTerms; ++j) e0 += tot[j];
-      sc->e0 = e0;
-      sc->ls_done = 0;
-      sc->accepted = 0;
-      sc->fault = 0;
-      sc->alpha_ls = 0.0;
-      sc->e1 = e0;
-      for (int j = 0; j < kTerms; ++j) sc->terms0[j] = tot[j];
-      sc->gamma = tot[kTerms];
-      sc->gamma_prev = 0.0;
-      sc->bnorm2 = tot[kTerms + 1];
-      sc->rnorm2 = tot[kTerms + 1];
-      sc->alpha = sc->alpha_prev = sc->beta = sc->delta = 0.0;
-      sc->iterations = 0;
-      sc->pending = 0;
-      sc->xinit = 0;
-      sc->plast = 0;
-      // zero rhs -> x = 0 (solver.py:85-86); non-finite -> host raises
-      sc->stop = (!finite || tot[kTerms + 1] == 0.0 || r_out == nullptr) ? 1 : 0;
+    if (f.bsum) {
+      for (int j = 0; j < NV; ++j) f.bsum[j] = tot[j];
+    } else if (!TRIAL) {
+      fin_energy_eg(tot, sc, r_out != nullptr);
     } else {
-      for (int j = 0; j < kTerms; ++j) sc->terms1[j] = tot[j];
-      if (dev_ls) {   // accept / halve decision of solver.py:169-178 on the device
-        double e1 = 0.0;
-        for (int j = 0; j < kTerms; ++j) e1 += tot[j];
-        if (!isfinite(sc->e0)) {
-          sc->fault = 1;
-          sc->ls_done = 1;
-        } else if (isfinite(e1) && e1 <= sc->e0) {
-          sc->ls_done = 1;
-          sc->accepted = 1;
-          sc->alpha_ls = (double)alpha;
-          sc->e1 = e1;
-        } else if (last_trial) {
-          sc->ls_done = 1;
-        }
-      }
+      fin_energy_trial(tot, sc, alpha, dev_ls, last_trial);
     }
     *ticket = 0u;
   }
@@ -726,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_apply(Frame f, Coef<float> c, c
       for (int j = 0; j < 2; ++j) {
         const int t = blockIdx.x + j * gridDim.x;
         if (t < ntiles)
-          tma_issue_tile<NT>(smem + j * STAGE, maps, &bars[j], (t % ntx) * kTileW, (t / ntx) * kTileH);
+          tma_issue_tile<NT>(smem + j * STAGE, maps, &bars[j], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH);
       }
     }
     __syncthreads();
@@ -737,12 +766,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_apply(Frame f, Coef<float> c, c
   for (int j = 0;; ++j) {
     const int tile = blockIdx.x + j * gridDim.x;
     if (tile >= ntiles) break;
-    const int tx0 = (tile % ntx) * kTileW, ty0 = (tile / ntx) * kTileH;
+    const int tx0 = (tile % ntx) * kTileW, ty0 = f.y_lo + (tile / ntx) * kTileH;
     const int st = TMA ? (j & 1) : 0;
     float* sX = smem + st * STAGE;
     float* sT = sX + off_T(NT);
     float* sR = sX + off_R(NT, true);
-    const PixPre pre = pix_prefetch(f, tx0 + lx, ty0 + ly, tx0 + lx < W && ty0 + ly < H);
+    const PixPre pre = pix_prefetch(f, tx0 + lx, ty0 + ly, tx0 + lx < W && ty0 + ly < f.y_hi);
     if (TMA) {
       mbar_wait(&bars[st], (phase >> st) & 1u);
       phase ^= 1u << st;
@@ -753,16 +782,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_apply(Frame f, Coef<float> c, c
       load_halo7(sR, u, nullptr, 0.f, N, W, H, tx0, ty0);
       __syncthreads();
     }
-    const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H;
+    const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H && ty0 + kTileH <= f.y_hi;
     if (interior)
       acc += apply_pixel<NT, true>(f, c, sX, sT, sR, w, tx0 + lx, ty0 + ly, cx, cy, rx, ry, pre);
-    else if (tx0 + lx < W && ty0 + ly < H)
+    else if (tx0 + lx < W && ty0 + ly < f.y_hi)
       acc += apply_pixel<NT, false>(f, c, sX, sT, sR, w, tx0 + lx, ty0 + ly, cx, cy, rx, ry, pre);
     if (TMA) {
       __syncthreads();   // every thread is done with this stage
       if (threadIdx.x == 0) {
         const int t = blockIdx.x + (j + 2) * gridDim.x;
-        if (t < ntiles) tma_issue_tile<NT>(sX, maps, &bars[st], (t % ntx) * kTileW, (t / ntx) * kTileH);
+        if (t < ntiles) tma_issue_tile<NT>(sX, maps, &bars[st], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH);
       }
     }
     accd += (double)acc;   // fp64 across tiles
@@ -922,7 +951,7 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
       fence_barrier_init();
       if ((int)blockIdx.x < ntiles) {
         const int t = blockIdx.x;
-        tma_issue_pcg<NT>(smem, maps, &bars[0], (t % ntx) * kTileW, (t / ntx) * kTileH, with_p);
+        tma_issue_pcg<NT>(smem, maps, &bars[0], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH, with_p);
       }
     }
     __syncthreads();
@@ -933,9 +962,9 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
   for (int j = 0;; ++j) {
     const int tile = blockIdx.x + j * gridDim.x;
     if (tile >= ntiles) break;
-    const int tx0 = (tile % ntx) * kTileW, ty0 = (tile / ntx) * kTileH;
+    const int tx0 = (tile % ntx) * kTileW, ty0 = f.y_lo + (tile / ntx) * kTileH;
     const int x = tx0 + lx, y = ty0 + ly;
-    const bool own = x < W && y < H;
+    const bool own = x < W && y < f.y_hi;
     const PixPre pre = pix_prefetch(f, x, y, own);
     if (TMA) {
       mbar_wait(&bars[0], phase);
@@ -969,7 +998,7 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
       form(sZR, sPR, 3 * kRP / 4);
       __syncthreads();
     }
-    const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H;
+    const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H && ty0 + kTileH <= f.y_hi;
     if (interior)
       acc += apply_pixel<NT, true>(f, c, sX, sZT, sZR, q, x, y, cx, cy, rx, ry, pre);
     else if (own)
@@ -992,7 +1021,7 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
       __syncthreads();
       if (threadIdx.x == 0) {
         const int t = blockIdx.x + (j + 1) * gridDim.x;
-        if (t < ntiles) tma_issue_pcg<NT>(smem, maps, &bars[0], (t % ntx) * kTileW, (t / ntx) * kTileH, with_p);
+        if (t < ntiles) tma_issue_pcg<NT>(smem, maps, &bars[0], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH, with_p);
       }
     }
     accd += (double)acc;
@@ -1003,28 +1032,39 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
   if (!last_block(ticket)) return;
   const double pap = sum_partials<1>(part, gridDim.x, 0);
   if (threadIdx.x == 0) {
-    sc->delta = pap;
-    if (!(pap > 0.0) || !isfinite(pap)) {
-      sc->stop = 1;                       // solver.py:95-96: break before the update
-    } else {
-      sc->alpha_prev = sc->alpha;
-      sc->alpha = sc->gamma / pap;
-    }
+    if (f.bsum) f.bsum[0] = pap;
+    else fin_pcg_apply(pap, sc);
     *ticket = 0u;
   }
+}
+
+// Row bands (band.planes > 0): only rows [y_lo, y_hi) of every plane, as
+// band.planes x band.len4 float4s starting at band.off4 of each plane.
+struct BandSpan {
+  int planes;
+  int len4;
+  int64_t off4, plane4;
+};
+
+__device__ __forceinline__ int64_t span_index(const BandSpan& b, int64_t j) {
+  const int pl = (int)((uint32_t)j / (uint32_t)b.len4);
+  return (int64_t)pl * b.plane4 + b.off4 + (j - (int64_t)pl * b.len4);
 }
 
 __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __restrict__ r, const float* __restrict__ q,
                                                          const float* __restrict__ dinv, float* __restrict__ z,
                                                          const float* __restrict__ p, float* __restrict__ xv,
-                                                         double* part, unsigned* ticket, Scalars* sc, int iter) {
+                                                         double* part, unsigned* ticket, Scalars* sc, int iter,
+                                                         BandSpan band, double* bsum) {
   if (sc->stop) return;
   const float a = (float)sc->alpha;
   const bool first = iter == 0;            // x_0 = 0 (solver.py:82)
   double acc[2] = {0.0, 0.0};
-  const int64_t M4 = M >> 2;
+  const bool banded = band.planes > 0;
+  const int64_t M4 = banded ? (int64_t)band.planes * band.len4 : (M >> 2);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M4; j += stride) {
+  for (int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < M4; jj += stride) {
+    const int64_t j = banded ? span_index(band, jj) : jj;
     float4 rr = reinterpret_cast<const float4*>(r)[j];
     const float4 qq = __ldg(reinterpret_cast<const float4*>(q) + j);
     const float4 di = __ldg(reinterpret_cast<const float4*>(dinv) + j);
@@ -1039,7 +1079,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
     acc[0] += (double)fmaf(rr.x, zz.x, fmaf(rr.y, zz.y, fmaf(rr.z, zz.z, rr.w * zz.w)));
     acc[1] += (double)fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, fmaf(rr.z, rr.z, rr.w * rr.w)));
   }
-  for (int64_t j = (M4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride) {
+  for (int64_t j = banded ? M : (M4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride) {
     xv[j] = fmaf(a, p[j], first ? 0.f : xv[j]);
     const float rr = fmaf(-a, q[j], r[j]);
     const float zz = rr * dinv[j];
@@ -1053,13 +1093,12 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
   const double rz = sum_partials<2>(part, gridDim.x, 0);
   const double rn = sum_partials<2>(part, gridDim.x, 1);
   if (threadIdx.x == 0) {
-    sc->iterations = iter + 1;
-    sc->xinit = 1;
-    sc->gamma_prev = sc->gamma;
-    sc->gamma = rz;
-    sc->rnorm2 = rn;
-    sc->beta = rz / sc->gamma_prev;
-    if (rz <= 0.0) sc->stop = 1;          // solver.py:101-103
+    if (bsum) {
+      bsum[0] = rz;
+      bsum[1] = rn;
+    } else {
+      fin_pcg_update(rz, rn, sc, iter);
+    }
     *ticket = 0u;
   }
 }
@@ -1259,8 +1298,43 @@ void launch_pcg_apply(const Launch& L, const Frame& f, const Coef<float>& c, con
 }
 
 void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
-                       const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter) {
-  k_pcg_update<<<L.grid, kThreads, 0, L.stream>>>(M, r, q, dinv, z, p, xv, part, ticket, sc, iter);
+                       const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter,
+                       const Frame* band) {
+  BandSpan bs{0, 0, 0, 0};
+  double* bsum = nullptr;
+  if (band && (band->y_lo != 0 || band->y_hi != band->H)) {   // W % 4 == 0 checked by ls_band_set
+    bs.planes = band->NT + 3;
+    bs.len4 = (band->y_hi - band->y_lo) * band->W / 4;
+    bs.off4 = (int64_t)band->y_lo * band->W / 4;
+    bs.plane4 = (int64_t)band->N / 4;
+  }
+  if (band) bsum = band->bsum;
+  k_pcg_update<<<L.grid, kThreads, 0, L.stream>>>(M, r, q, dinv, z, p, xv, part, ticket, sc, iter, bs, bsum);
+}
+
+// band-ordered sum of the gathered partials [nbands][nv], then the same
+// finalisation the single-frame kernels run in their last CTA
+__global__ void k_band_finalize(int phase, const double* __restrict__ g, int nbands, int nv, Scalars* sc, int iter,
+                                float alpha, int dev_ls, int last_trial) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double tot[kTerms + 2];
+  for (int j = 0; j < nv && j < kTerms + 2; ++j) {
+    double s = 0.0;
+    for (int b = 0; b < nbands; ++b) s += g[(size_t)b * nv + j];
+    tot[j] = s;
+  }
+  switch (phase) {
+    case BAND_EG: fin_energy_eg(tot, sc, true); break;
+    case BAND_TRIAL: fin_energy_trial(tot, sc, alpha, dev_ls, last_trial); break;
+    case BAND_APPLY: if (!sc->stop) fin_pcg_apply(tot[0], sc); break;
+    case BAND_UPDATE: if (!sc->stop) fin_pcg_update(tot[0], tot[1], sc, iter); break;
+    default: break;
+  }
+}
+
+void launch_band_finalize(cudaStream_t s, int phase, const double* gathered, int nbands, int nv, Scalars* sc,
+                          int iter, float alpha, int dev_ls, int last_trial) {
+  k_band_finalize<<<1, 32, 0, s>>>(phase, gathered, nbands, nv, sc, iter, alpha, dev_ls, last_trial);
 }
 
 int pcg_apply_grid_limit(int NT) {

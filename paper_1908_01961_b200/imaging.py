@@ -7,7 +7,7 @@ and argmins match the reference bit for bit.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from pathlib import Path
 
 import numpy as np
@@ -43,6 +43,9 @@ class Frame:
     as float32 (inputs are expected to be float32-representable)."""
 
     data: torch.Tensor  # (H, W, 3) float32, CUDA
+    # solve as row bands (bands.py): a band count (all bands in this process)
+    # or a bands.BandedSolver (e.g. one band per rank); 0 = whole frame
+    bands: object = field(default=0, compare=False, repr=False)
 
     def __post_init__(self):
         d = self.data

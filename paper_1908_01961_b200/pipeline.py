@@ -44,8 +44,10 @@ class PipelineResult:
         return [ls.illumination(self.palette) for ls in self.layer_stacks]
 
 
-def _as_frame(f) -> Frame:
-    return f if isinstance(f, Frame) else Frame(as_cuda(f))
+def _as_frame(f, bands=0) -> Frame:
+    if isinstance(f, Frame):
+        return f if (not bands or f.bands is bands) else Frame(f.data, bands=bands)
+    return Frame(as_cuda(f), bands=bands)
 
 
 class StreamingDecomposer:
@@ -55,7 +57,8 @@ class StreamingDecomposer:
     warm-started from the previous one."""
 
     def __init__(self, palette: BaseColorPalette, weights: EnergyWeights, config: SolveConfig,
-                 seed: int = 0, streaming_outer: int = 2):
+                 seed: int = 0, streaming_outer: int = 2, bands=0):
+        self.bands = bands          # row bands (bands.py), 0 = whole frames
         self.palette = palette
         self.weights = weights
         self.config = config
@@ -66,7 +69,7 @@ class StreamingDecomposer:
         self.prev_chroma = None
 
     def first(self, frame, cluster_map: ClusterMap | None = None) -> SolverState:
-        frame = _as_frame(frame)
+        frame = _as_frame(frame, self.bands)
         if cluster_map is None:
             cluster_map = segment(frame, self.palette)
         aux = build_aux(frame, cluster_map, seed=self.seed)
@@ -86,7 +89,7 @@ class StreamingDecomposer:
         return state
 
     def step(self, frame) -> SolverState:
-        frame = _as_frame(frame)
+        frame = _as_frame(frame, self.bands)
         cmap = segment(frame, self.palette)
         aux = build_aux(frame, cmap, seed=self.seed + self.index, prev_chroma=self.prev_chroma,
                         prev_r=self.prev_layers.r)

@@ -83,6 +83,15 @@ class SolverState:
 
 
 def _solver_for(state: SolverState):
+    bands = getattr(state.frame, "bands", 0)
+    if bands:     # row bands (bands.py): same calls, band-partitioned
+        from .bands import BandedSolver, banded_solver
+        H, W = state.frame.height, state.frame.width
+        s = bands if isinstance(bands, BandedSolver) else banded_solver(
+            state.layers.X.device, H, W, state.palette.K, int(bands))
+        s.configure(state.weights, state.config)
+        s.install(state.frame, state.aux)
+        return s
     H, W = state.layers.shape
     s = _device.get_solver(state.layers.X.device, H, W, state.palette.K)
     s.configure(state.weights, state.config)
