@@ -43,14 +43,23 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--height", type=int, default=1080)
-    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--workload", default="1080p", choices=["1080p", "4k"],
+                    help="1080p: BASELINE configs[2] (N>1: one clip per GPU, configs[4]); "
+                         "4k: configs[3], 3840x2160 split into row bands, one band per GPU")
+    ap.add_argument("--bands", type=int, default=0,
+                    help="4k on one process: solve as this many row bands (0: whole frame)")
+    ap.add_argument("--height", type=int, default=None)
+    ap.add_argument("--width", type=int, default=None)
     ap.add_argument("--K", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true",
                     help="run warmup + steps without the extra legs (for ncu)")
     return ap.parse_args()
+
+
+def metric_for(args) -> str:
+    return METRIC if args.workload == "1080p" else "decomposed frames/sec at 2160p"
 
 
 def dist_env():
@@ -213,7 +222,7 @@ def run_reference(args):
     sample = (f"streaming frames (segment + aux + 2x2 GN x 16 PCG) of the oracle port on a "
               f"{W}x{STRIP_ROWS} strip of the synthetic K={K} clip, per-pixel time scaled x{scale:.1f} "
               f"to {W}x{H}")
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    line = {"metric": metric_for(args), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": sec_per_frame * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
@@ -232,7 +241,7 @@ def run_reference(args):
 def run_ours(args):
     import numpy as np
     import torch
-    from paper_1908_01961_b200 import synth, _device, clips
+    from paper_1908_01961_b200 import synth, _device, clips, bands as band_mod
     from paper_1908_01961_b200.energy import EnergyWeights
     from paper_1908_01961_b200.palette import BaseColorPalette
     from paper_1908_01961_b200.pipeline import StreamingDecomposer
@@ -249,11 +258,22 @@ def run_ours(args):
     steps, warmup = args.steps, args.warmup
     e2e_on = not (args.no_e2e or args.profile_only)
     n_frames = 1 + warmup + steps + (steps if e2e_on else 0)
-    clip = synth.make_clip(H, W, K, n_frames, seed=rank, device=dev)
+    four_k = args.workload == "4k"
+    pal_seed = 0 if four_k else rank      # 4k: every rank holds a band of the same clip
+    clip = synth.make_clip(H, W, K, n_frames, seed=pal_seed, device=dev)
     frames = clip.frames
     pal = BaseColorPalette(colors=clip.colors)
     cfg = SolveConfig(tol_rel=0.0)        # fixed iteration counts
-    dec = StreamingDecomposer(pal, EnergyWeights(), cfg, seed=rank)
+    bands, nb_total, spec = 0, 1, None
+    if four_k and world > 1:              # one row band per GPU
+        specs = band_mod.plan_bands(H, world)
+        spec = specs[rank]
+        bands = band_mod.BandedSolver(dev, H, W, K, exchange=band_mod.DistExchange(specs))
+        frames = [f[spec.ya:spec.yb].contiguous() for f in frames]
+        nb_total = world
+    elif four_k and args.bands > 1:       # all bands in this process
+        bands, nb_total = args.bands, args.bands
+    dec = StreamingDecomposer(pal, EnergyWeights(), cfg, seed=pal_seed, bands=bands)
 
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -265,8 +285,14 @@ def run_ours(args):
         dec.step(frames[1 + i])
     torch.cuda.synchronize()
 
-    solver = _device.get_solver(dev, H, W, K)
-    solver.profile(True)
+    if isinstance(bands, band_mod.BandedSolver):
+        prof_solvers = [b.solver for b in bands.bands]
+    elif bands:
+        prof_solvers = [b.solver for b in band_mod.banded_solver(dev, H, W, K, bands).bands]
+    else:
+        prof_solvers = [_device.get_solver(dev, H, W, K)]
+    for ps in prof_solvers:
+        ps.profile(True)
     clocks = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local])
                           if os.environ.get("CUDA_VISIBLE_DEVICES") else local)
     if world > 1:
@@ -283,14 +309,29 @@ def run_ours(args):
     wall_ms = (time.perf_counter() - wall0) * 1e3
     clk = clocks.stop()
     t_ms = ev0.elapsed_time(ev1)
-    prof = solver.profile_read()
-    solver.profile(False)
-    th = clips.aggregate(steps, t_ms / 1e3)     # frames summed, time = max over ranks
+    prof = None
+    for ps in prof_solvers:
+        pr = ps.profile_read()
+        ps.profile(False)
+        if prof is None:
+            prof = pr
+            continue
+        for k, v in pr.items():
+            if isinstance(v, dict):
+                prof[k] = {"count": prof[k]["count"] + v["count"], "ms": prof[k]["ms"] + v["ms"]}
+            else:
+                prof[k] += v
+    if four_k and world > 1:   # strong scaling: the same frames, time = max over ranks
+        th = clips.aggregate(steps if rank == 0 else 0, t_ms / 1e3)
+    else:
+        th = clips.aggregate(steps, t_ms / 1e3)     # frames summed, time = max over ranks
     t_ms = th.seconds * 1e3
     value = th.fps
 
     # --- roofline of the dominant kernel (algorithmic bytes / event time) ---
-    N = H * W
+    split = world if (four_k and world > 1) else 1     # GPUs sharing one frame
+    # one launch covers one band's own rows (the whole frame without bands)
+    N = H * W // nb_total
     U = K + 4
     ent_per_px = prof["adjacency_entries"] / N
     # k_pcg_apply: reads X, z, p_prev (3U), edge, row_ptr, entries; writes p, q (2U)
@@ -323,15 +364,16 @@ def run_ours(args):
                 "per_kernel": per_kernel,
                 # SURVEY.md 8(d) compulsory-traffic model of a whole streaming
                 # frame, B_frame = 4 N (860 U + 298) bytes, over the measured frame time
-                "frame_model": {"bytes": 4 * N * (860 * U + 298),
-                                "achieved_gbs": 4 * N * (860 * U + 298) / (t_ms / steps / 1e3) / 1e9,
-                                "frac": 4 * N * (860 * U + 298) / (t_ms / steps / 1e3) / 1e9 / peak}}
+                "frame_model": {"bytes": 4 * H * W * (860 * U + 298),
+                                "achieved_gbs": 4 * H * W * (860 * U + 298) / (t_ms / steps / 1e3) / 1e9 / split,
+                                "frac": 4 * H * W * (860 * U + 298) / (t_ms / steps / 1e3) / 1e9 / split / peak,
+                                "note": "per GPU"}}
 
     # --- e2e through the public API with host buffers ---
     e2e = None
     if e2e_on:
         host = [frames[1 + warmup + steps + i].cpu().pin_memory() for i in range(steps)]
-        out_host = [torch.empty((U, H, W), dtype=torch.float32).pin_memory() for _ in range(2)]
+        out_host = [torch.empty(tuple(st.layers.X.shape), dtype=torch.float32).pin_memory() for _ in range(2)]
         side = torch.cuda.Stream(device=dev)
         torch.cuda.synchronize()
         if world > 1:
@@ -353,9 +395,11 @@ def run_ours(args):
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1)
         eth = clips.aggregate(steps, e_ms / 1e3)
+        if four_k and world > 1:
+            eth = clips.aggregate(steps if rank == 0 else 0, e_ms / 1e3)
         e2e = {"value": eth.fps, "unit": UNIT,
                "h2d_bytes_per_step": int(host[0].numel() * 4),
-               "d2h_bytes_per_step": int(U * H * W * 4),
+               "d2h_bytes_per_step": int(out_host[0].numel() * 4),
                "api": "pipeline.StreamingDecomposer.step (reference decompose_frames loop)"}
 
     # --- CPU baseline (rank 0, N = 1 only) ---
@@ -376,11 +420,16 @@ def run_ours(args):
         del guard
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+        line = {"metric": metric_for(args), "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
                 "warmup": warmup, "ms_per_step": t_ms / steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": f"{W}x{H} K={K} streaming frames (BASELINE configs[2]); "
-                                       f"N>1: one independent clip per GPU (configs[4])",
+                "scaling": "strong" if four_k else "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": {"workload": (f"{W}x{H} K={K} streaming frames as {nb_total} row band(s) "
+                                        f"(BASELINE configs[3]; one band per GPU, halo + all-gather over "
+                                        f"NCCL)" if four_k else
+                                        f"{W}x{H} K={K} streaming frames (BASELINE configs[2]); "
+                                        f"N>1: one independent clip per GPU (configs[4])"),
+                           "bands": nb_total,
                            "H": H, "W": W, "K": K, "gn_steps_per_frame": 4, "pcg_iterations": 16,
                            "l2": "per-frame working set (~0.9 GB) exceeds the 126 MB L2; no flush",
                            "first_frame_ms": first_ms, "first_frame_records": n_first_records,
@@ -394,6 +443,10 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.height is None:
+        args.height = 2160 if args.workload == "4k" else 1080
+    if args.width is None:
+        args.width = 3840 if args.workload == "4k" else 1920
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -68,10 +68,16 @@ def segment(frame: Frame, palette: BaseColorPalette, chroma=None) -> ClusterMap:
     """palette.py:195-224 on the device."""
     img = frame.data
     H, W = int(img.shape[0]), int(img.shape[1])
-    solver = _device.get_solver(img.device, H, W, palette.K)
-    solver.set_image(img)
-    solver.installed = None
-    ids = solver.segment(palette.colors)
+    bands = getattr(frame, "bands", 0)
+    if bands and not isinstance(bands, int) and not bands.whole:
+        # one band of a multi-process banded frame: the dark-pixel
+        # inheritance crosses band boundaries (bands.BandedSolver.segment)
+        ids = bands.segment(img, palette.colors)
+    else:
+        solver = _device.get_solver(img.device, H, W, palette.K)
+        solver.set_image(img)
+        solver.installed = None
+        ids = solver.segment(palette.colors)
     cols = torch.as_tensor(palette.colors, dtype=torch.float32, device=img.device)
     return ClusterMap(ids=ids, r_cluster=cols[(ids - 1).long()])
 
