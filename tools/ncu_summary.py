@@ -102,7 +102,7 @@ def main():
                   f"{a.get('sm__throughput.avg.pct_of_peak_sustained_elapsed', 0):.1f} | "
                   f"{a.get('smsp__issue_active.avg.pct_of_peak_sustained_active', 0):.1f} | "
                   f"{a.get('launch__registers_per_thread', 0):.0f} |")
-    md += ["", "## launch list (`--metrics gpu__time_duration.sum`, all launches of tools/profile_step.py)", "",
+    md += ["", "## launch list (`ncu --metrics gpu__time_duration.sum --clock-control none` over `python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline`, every launch incl. frame 1 and clip synthesis)", "",
            "| kernel | launches | total ms | share |", "|---|---|---|---|"]
     for k, v in launch_share.items():
         md.append(f"| {k} | {v['launches']} | {v['total_ms']:.2f} | {100 * v['share']:.1f}% |")
