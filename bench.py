@@ -334,10 +334,11 @@ def run_ours(args):
     N = H * W // nb_total
     U = K + 4
     ent_per_px = prof["adjacency_entries"] / N
-    # k_pcg_apply: reads X, z, p_prev (3U), edge, row_ptr, entries; writes p, q (2U)
-    bytes_apply = N * (4 * (5 * U + 2) + 2 * ent_per_px)
-    # k_pcg_update: reads r, q, dinv, p, x (5U); writes r, z, x (3U)
-    bytes_update = N * 4 * 8 * U
+    # k_pcg_apply: reads X, z, p_prev, x (4U), edge, row_ptr, entries; writes p, q, x (3U)
+    # (the x-update of the previous iteration is folded in; 15 of 16 launches)
+    bytes_apply = N * (4 * (7 * U + 2) + 2 * ent_per_px)
+    # k_pcg_update: reads r, q, dinv (3U); writes r, z (2U)
+    bytes_update = N * 4 * 5 * U
     kern = {
         "apply": (prof["apply"], bytes_apply),
         "update": (prof["update"], bytes_update),

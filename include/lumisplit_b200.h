@@ -236,6 +236,8 @@ LS_API int ls_band_set_zeros(ls_ctx* ctx, const int64_t* lists, int n_lists);
 LS_API int ls_band_eg(ls_ctx* ctx, const double* colors_host, const float* X);
 LS_API int ls_band_pcg_apply(ls_ctx* ctx, const double* colors_host, const float* X, int iter);
 LS_API int ls_band_pcg_update(ls_ctx* ctx, int iter);
+/* after the last update: the deferred x += alpha p of the final iteration */
+LS_API int ls_band_pcg_finish(ls_ctx* ctx);
 LS_API int ls_band_trial(ls_ctx* ctx, const double* colors_host, const float* X, double alpha, float* X_out);
 LS_API int ls_band_finalize(ls_ctx* ctx, int phase, const double* gathered, int nbands, int iter, double alpha);
 /* host out[21]: terms0[8], terms1[8], |b|^2, |r|^2, iterations, stop, xinit */

@@ -98,6 +98,7 @@ SIGNATURES = {
     "ls_band_eg": [P, DBL_P, P],
     "ls_band_pcg_apply": [P, DBL_P, P, C.c_int],
     "ls_band_pcg_update": [P, C.c_int],
+    "ls_band_pcg_finish": [P],
     "ls_band_trial": [P, DBL_P, P, C.c_double, P],
     "ls_band_finalize": [P, C.c_int, P, C.c_int, C.c_int, C.c_double],
     "ls_band_read": [P, DBL_P],

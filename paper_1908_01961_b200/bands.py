@@ -384,6 +384,8 @@ class BandedSolver:
                 b.chk(b.lib.ls_band_pcg_update(b.ctx, it))
             self._gather_finalize(L.BAND_UPDATE, 2, it)
             ex.halo([b.z for b in bands])
+        for b in bands:
+            b.chk(b.lib.ls_band_pcg_finish(b.ctx))
         ex.halo([b.x for b in bands])
         info = np.zeros(21)
         alpha, e0, e1, accepted = 1.0, 0.0, 0.0, False

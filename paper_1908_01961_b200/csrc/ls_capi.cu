@@ -784,13 +784,15 @@ static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, f
   for (int it = 0; it < iters; ++it) {
     pi = prof_begin(c);
     launch_pcg_apply(La, f, cd, X, c->u, pbuf[(it + 1) & 1], pbuf[it & 1], c->wv, c->part, c->tickets + 1, c->sc,
-                     it, tma ? &maps[it & 1] : nullptr);
+                     it, tma ? &maps[it & 1] : nullptr, x);
     prof_end(c, PC_APPLY, pi);
     pi = prof_begin(c);
     launch_pcg_update(L_update(c), M, c->r, c->wv, c->d, c->u, pbuf[it & 1], x, c->part, c->tickets + 2, c->sc, it);
     prof_end(c, PC_UPDATE, pi);
   }
-  c->launches += 1 + 2LL * iters;
+  // the last x += alpha p (the applies fold in the earlier ones)
+  launch_pcg_xfinal(L_update(c), M, x, pbuf[0], pbuf[1], c->sc, c->tickets + 4);
+  c->launches += 2 + 2LL * iters;
   LS_CK(cudaGetLastError());
   return LS_OK;
 }
@@ -1169,7 +1171,7 @@ int ls_band_pcg_apply(ls_ctx* c, const double* colors, const float* X, int iter)
   const Launch La{c->grid_pcg, c->ntiles, c->stream};
   const size_t pi = prof_begin(c);
   launch_pcg_apply(La, f, cd, X, c->u, pbuf[(iter + 1) & 1], pbuf[iter & 1], c->wv, c->part, c->tickets + 1, c->sc,
-                   iter, tma ? &maps : nullptr);
+                   iter, tma ? &maps : nullptr, c->x);
   prof_end(c, PC_APPLY, pi);
   c->launches += 1;
   LS_CK(cudaGetLastError());
@@ -1187,6 +1189,16 @@ int ls_band_pcg_update(ls_ctx* c, int iter) {
   launch_pcg_update(L_update(c), M, c->r, c->wv, c->d, c->u, pbuf[iter & 1], c->x, c->part, c->tickets + 2, c->sc,
                     iter, &f);
   prof_end(c, PC_UPDATE, pi);
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_pcg_finish(ls_ctx* c) {
+  int rc = band_ready(c);
+  if (rc) return rc;
+  const Frame f = frame_of(c);
+  launch_pcg_xfinal(L_update(c), (int64_t)c->U * c->N, c->x, c->p, c->s, c->sc, c->tickets + 4, &f);
   c->launches += 1;
   LS_CK(cudaGetLastError());
   return LS_OK;

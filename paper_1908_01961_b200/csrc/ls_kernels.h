@@ -51,10 +51,12 @@ void launch_update(const Launch& L, int64_t M, float* x, float* r, float* p, flo
                    const float* d, float* u, double* part, unsigned* ticket, Scalars* sc, int iter);
 void launch_pcg_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* z,
                       const float* pprev, float* pnew, float* q, double* part, unsigned* ticket, Scalars* sc,
-                      int iter, const PcgMaps* maps);
+                      int iter, const PcgMaps* maps, float* x);
 void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
                        const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter,
                        const Frame* band = nullptr);
+void launch_pcg_xfinal(const Launch& L, int64_t M, float* xv, const float* p0, const float* p1, Scalars* sc,
+                       unsigned* ticket, const Frame* band = nullptr);
 // row bands: phases whose partial sums are gathered across bands
 enum BandPhase { BAND_EG = 0, BAND_APPLY = 1, BAND_UPDATE = 2, BAND_TRIAL = 3, BAND_DENSE = 4 };
 void launch_band_sum(cudaStream_t s, const double* gathered, int nbands, int nv, double* out);

@@ -445,6 +445,10 @@ __device__ void fin_energy_trial(const double* tot, Scalars* sc, float alpha, in
 }
 
 __device__ void fin_pcg_apply(double pap, Scalars* sc) {
+  if (sc->pending) {      // this apply folded alpha_{i-1} p_{i-1} into x
+    sc->pending = 0;
+    sc->xinit = 1;
+  }
   sc->delta = pap;
   if (!(pap > 0.0) || !isfinite(pap)) {
     sc->stop = 1;                       // solver.py:95-96: break before the update
@@ -456,7 +460,7 @@ __device__ void fin_pcg_apply(double pap, Scalars* sc) {
 
 __device__ void fin_pcg_update(double rz, double rn, Scalars* sc, int iter) {
   sc->iterations = iter + 1;
-  sc->xinit = 1;
+  sc->pending = 1;        // x += alpha_i p_i is deferred to the next apply (or k_pcg_xfinal)
   sc->gamma_prev = sc->gamma;
   sc->gamma = rz;
   sc->rnorm2 = rn;
@@ -929,7 +933,8 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
                                                            const float* __restrict__ pprev,
                                                            float* __restrict__ pnew, float* __restrict__ q, double* part, unsigned* ticket,
                                                            Scalars* sc, int iter, int ntiles,
-                                                           const __grid_constant__ PcgMaps maps) {
+                                                           const __grid_constant__ PcgMaps maps,
+                                                           float* __restrict__ xv) {
   constexpr int U = NT + 3;
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bars[1];
@@ -940,6 +945,12 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
   const int ntx = (W + kTileW - 1) / kTileW;
   const bool with_p = LS_ABLATE != 2 && iter > 0;
   const float beta = (float)sc->beta;
+  // deferred PCG x-update (solver.py:98): x += alpha_{i-1} p_{i-1} for the own
+  // pixels, p_{i-1} taken from the staged window -- k_pcg_update then streams
+  // only r, q, dinv -> r, z
+  const bool xupd = with_p && sc->pending;
+  const bool xread = sc->xinit;
+  const float ax = (float)sc->alpha;
   float* sX = smem;
   float* sZT = smem + pad32(U * kSP);
   float* sZR = sZT + pad32(NT * kSP);
@@ -1003,6 +1014,7 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
       acc += apply_pixel<NT, true>(f, c, sX, sZT, sZR, q, x, y, cx, cy, rx, ry, pre);
     else if (own)
       acc += apply_pixel<NT, false>(f, c, sX, sZT, sZR, q, x, y, cx, cy, rx, ry, pre);
+    float pold[U];
     if (own) {
       const int i = y * W + x;
       const int sc0 = cy * kSW + cx, rc0 = ry * kRW + rx;
@@ -1016,6 +1028,12 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
         const size_t o = (size_t)(3 + k) * N + i;
         pnew[o] = sZT[k * kSP + sc0];
       }
+      if (xupd) {   // p_{i-1} of the own pixel into registers before the stage is released
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) pold[ch] = sPR[ch * kRP + rc0];
+#pragma unroll
+        for (int k = 0; k < NT; ++k) pold[3 + k] = sPT[k * kSP + sc0];
+      }
     }
     if (TMA) {
       __syncthreads();
@@ -1023,6 +1041,14 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
         const int t = blockIdx.x + (j + 1) * gridDim.x;
         if (t < ntiles) tma_issue_pcg<NT>(smem, maps, &bars[0], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH, with_p);
       }
+    }
+    if (xupd && own) {   // x += alpha_{i-1} p_{i-1}, overlapping the next tile's loads
+      const size_t i = (size_t)y * W + x;
+      float xo[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xo[u] = xread ? xv[(size_t)u * N + i] : 0.f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[(size_t)u * N + i] = fmaf(ax, pold[u], xo[u]);
     }
     accd += (double)acc;
     acc = 0.f;
@@ -1053,12 +1079,10 @@ __device__ __forceinline__ int64_t span_index(const BandSpan& b, int64_t j) {
 
 __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __restrict__ r, const float* __restrict__ q,
                                                          const float* __restrict__ dinv, float* __restrict__ z,
-                                                         const float* __restrict__ p, float* __restrict__ xv,
                                                          double* part, unsigned* ticket, Scalars* sc, int iter,
                                                          BandSpan band, double* bsum) {
   if (sc->stop) return;
   const float a = (float)sc->alpha;
-  const bool first = iter == 0;            // x_0 = 0 (solver.py:82)
   double acc[2] = {0.0, 0.0};
   const bool banded = band.planes > 0;
   const int64_t M4 = banded ? (int64_t)band.planes * band.len4 : (M >> 2);
@@ -1068,19 +1092,14 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
     float4 rr = reinterpret_cast<const float4*>(r)[j];
     const float4 qq = __ldg(reinterpret_cast<const float4*>(q) + j);
     const float4 di = __ldg(reinterpret_cast<const float4*>(dinv) + j);
-    const float4 pp = __ldg(reinterpret_cast<const float4*>(p) + j);
-    float4 xx = first ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4*>(xv)[j];
-    xx = make_float4(fmaf(a, pp.x, xx.x), fmaf(a, pp.y, xx.y), fmaf(a, pp.z, xx.z), fmaf(a, pp.w, xx.w));
     rr = make_float4(fmaf(-a, qq.x, rr.x), fmaf(-a, qq.y, rr.y), fmaf(-a, qq.z, rr.z), fmaf(-a, qq.w, rr.w));
     const float4 zz = make_float4(rr.x * di.x, rr.y * di.y, rr.z * di.z, rr.w * di.w);
     reinterpret_cast<float4*>(r)[j] = rr;
     reinterpret_cast<float4*>(z)[j] = zz;
-    reinterpret_cast<float4*>(xv)[j] = xx;
     acc[0] += (double)fmaf(rr.x, zz.x, fmaf(rr.y, zz.y, fmaf(rr.z, zz.z, rr.w * zz.w)));
     acc[1] += (double)fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, fmaf(rr.z, rr.z, rr.w * rr.w)));
   }
   for (int64_t j = banded ? M : (M4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride) {
-    xv[j] = fmaf(a, p[j], first ? 0.f : xv[j]);
     const float rr = fmaf(-a, q[j], r[j]);
     const float zz = rr * dinv[j];
     r[j] = rr;
@@ -1282,34 +1301,75 @@ void launch_apply(const Launch& L, const Frame& f, const Coef<float>& c, const f
 template <int NT>
 static void launch_pcg_apply_nt(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* z,
                                 const float* pprev, float* pnew, float* q, double* part, unsigned* ticket,
-                                Scalars* sc, int iter, const PcgMaps* maps) {
+                                Scalars* sc, int iter, const PcgMaps* maps, float* x) {
   if (maps)
     k_pcg_apply<NT, true><<<L.grid, kThreads, pcg_smem<NT>(true), L.stream>>>(f, c, X, z, pprev, pnew, q, part, ticket,
-                                                                         sc, iter, L.ntiles, *maps);
+                                                                         sc, iter, L.ntiles, *maps, x);
   else
     k_pcg_apply<NT, false><<<L.grid, kThreads, pcg_smem<NT>(false), L.stream>>>(f, c, X, z, pprev, pnew, q, part, ticket,
-                                                                          sc, iter, L.ntiles, PcgMaps{});
+                                                                          sc, iter, L.ntiles, PcgMaps{}, x);
 }
 
 void launch_pcg_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* z,
                       const float* pprev, float* pnew, float* q, double* part, unsigned* ticket, Scalars* sc,
-                      int iter, const PcgMaps* maps) {
-  LS_DISPATCH_NT(f.NT, (launch_pcg_apply_nt<NT_>(L, f, c, X, z, pprev, pnew, q, part, ticket, sc, iter, maps)));
+                      int iter, const PcgMaps* maps, float* x) {
+  LS_DISPATCH_NT(f.NT, (launch_pcg_apply_nt<NT_>(L, f, c, X, z, pprev, pnew, q, part, ticket, sc, iter, maps, x)));
 }
 
-void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
-                       const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter,
-                       const Frame* band) {
+// the last deferred x-update after the PCG loop: x += alpha_j p_j for the
+// last completed iteration j (k_pcg_update's finalisation left it pending)
+__global__ void __launch_bounds__(kThreads) k_pcg_xfinal(int64_t M, float* __restrict__ xv,
+                                                         const float* __restrict__ p0,
+                                                         const float* __restrict__ p1, Scalars* sc,
+                                                         unsigned* ticket, BandSpan band) {
+  if (!sc->pending) return;
+  const float a = (float)sc->alpha;
+  const float* __restrict__ p = ((sc->iterations - 1) & 1) ? p1 : p0;
+  const bool xread = sc->xinit;
+  const bool banded = band.planes > 0;
+  const int64_t M4 = banded ? (int64_t)band.planes * band.len4 : (M >> 2);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < M4; jj += stride) {
+    const int64_t j = banded ? span_index(band, jj) : jj;
+    const float4 pp = __ldg(reinterpret_cast<const float4*>(p) + j);
+    float4 xx = xread ? reinterpret_cast<const float4*>(xv)[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+    xx = make_float4(fmaf(a, pp.x, xx.x), fmaf(a, pp.y, xx.y), fmaf(a, pp.z, xx.z), fmaf(a, pp.w, xx.w));
+    reinterpret_cast<float4*>(xv)[j] = xx;
+  }
+  for (int64_t j = banded ? M : (M4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride)
+    xv[j] = fmaf(a, p[j], xread ? xv[j] : 0.f);
+  if (!last_block(ticket)) return;
+  if (threadIdx.x == 0) {
+    sc->pending = 0;
+    sc->xinit = 1;
+    *ticket = 0u;
+  }
+}
+
+static BandSpan band_span(const Frame* band) {
   BandSpan bs{0, 0, 0, 0};
-  double* bsum = nullptr;
   if (band && (band->y_lo != 0 || band->y_hi != band->H)) {   // W % 4 == 0 checked by ls_band_set
     bs.planes = band->NT + 3;
     bs.len4 = (band->y_hi - band->y_lo) * band->W / 4;
     bs.off4 = (int64_t)band->y_lo * band->W / 4;
     bs.plane4 = (int64_t)band->N / 4;
   }
-  if (band) bsum = band->bsum;
-  k_pcg_update<<<L.grid, kThreads, 0, L.stream>>>(M, r, q, dinv, z, p, xv, part, ticket, sc, iter, bs, bsum);
+  return bs;
+}
+
+void launch_pcg_xfinal(const Launch& L, int64_t M, float* xv, const float* p0, const float* p1, Scalars* sc,
+                       unsigned* ticket, const Frame* band) {
+  k_pcg_xfinal<<<L.grid, kThreads, 0, L.stream>>>(M, xv, p0, p1, sc, ticket, band_span(band));
+}
+
+void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
+                       const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter,
+                       const Frame* band) {
+  (void)p;
+  (void)xv;
+  const BandSpan bs = band_span(band);
+  double* bsum = band ? band->bsum : nullptr;
+  k_pcg_update<<<L.grid, kThreads, 0, L.stream>>>(M, r, q, dinv, z, part, ticket, sc, iter, bs, bsum);
 }
 
 // band-ordered sum of the gathered partials [nbands][nv], then the same
