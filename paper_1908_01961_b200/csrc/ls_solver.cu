@@ -187,13 +187,34 @@ __device__ __forceinline__ void tma_issue_energy(float* stage, const EnergyMaps&
 
 // per-pixel energy terms (+ gradient / diagonal / PCG init in MODE_EG);
 // acc[] receives the 8 term energies (fp32 per pixel) and rz, |b|^2
+// per-pixel global inputs of the energy kernel, read before the tile's TMA
+// wait so their latency overlaps it
+struct EPre {
+  float img[3];
+  float edge;
+  int id, e0, e1;
+};
+__device__ __forceinline__ EPre energy_prefetch(const Frame& f, int x, int y, bool own) {
+  EPre p{{0.f, 0.f, 0.f}, 0.f, 0, 0, 0};
+  if (own) {
+    const int i = y * f.W + x;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) p.img[ch] = __ldg(f.img + ch * f.N + i);
+    p.edge = __ldg(f.edge + i);
+    p.id = f.ids ? __ldg(f.ids + i) : 0;
+    p.e0 = __ldg(f.row_ptr + i);
+    p.e1 = __ldg(f.row_ptr + i + 1);
+  }
+  return p;
+}
+
 template <int NT, int MODE, bool IN>
 __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& c, const float* sX, const float* sXR,
                                              const float* sYT, const float* sYR, int x, int y, int cx, int cy,
                                              int rx, int ry, float* __restrict__ Xout, float* __restrict__ r_out,
                                              float* __restrict__ d_out, float* __restrict__ u_out,
                                              float* __restrict__ b_raw, float* __restrict__ diag_raw,
-                                             double* acc) {
+                                             double* acc, const EPre& pre) {
   const int W = f.W, H = f.H, N = f.N;
   const int i = y * W + x;
   const bool hx = IN || x < W - 1, hy = IN || y < H - 1, hl = IN || x > 0, hu = IN || y > 0;
@@ -211,16 +232,15 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
   }
   float img[3], anc[3];
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) img[ch] = __ldg(f.img + ch * N + i);
+  for (int ch = 0; ch < 3; ++ch) img[ch] = pre.img[ch];
   if (f.ids) {
-    const int id = __ldg(f.ids + i);
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) anc[ch] = c.anchor[id][ch];
+    for (int ch = 0; ch < 3; ++ch) anc[ch] = c.anchor[pre.id][ch];
   } else {
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) anc[ch] = __ldg(f.anchor + ch * N + i);
   }
-  const float lm = c.lam_m * __ldg(f.edge + i);
+  const float lm = c.lam_m * pre.edge;
 
   // data (energy.py:207-209), clustering (234-235), monochrome (399-401)
   float S[3], R[3], res[3], m[3];
@@ -294,13 +314,12 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
   // src; gradient / diagonal from every incident pair (energy.py:359-381)
   float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, dcons = 0.f;
   {
-    const int e0 = __ldg(f.row_ptr + i), e1 = __ldg(f.row_ptr + i + 1);
+    const int e0 = pre.e0, e1 = pre.e1;
     float ec = 0.f;
     const float* YR = sYR + rc0;
-    for (int e = e0; e < e1; ++e) {
-      const uint16_t ent = __ldg(f.ent + e);
-      const float we = c.lam_rc * (f.ent_w ? __ldg(f.ent_w + e) : 1.f);
-      float p0, p1, p2;
+    // partner values of one entry: the previous frame's r (temporal, global)
+    // or the staged window (spatial)
+    auto partner = [&](uint16_t ent, float& p0, float& p1, float& p2) {
       if (ent & kEntTemporal) {
         int ddy, ddx;
         decode_offset(ent, ddy, ddx);
@@ -314,12 +333,37 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
         p1 = YR[kRP + o];
         p2 = YR[2 * kRP + o];
       }
+    };
+    auto accum = [&](uint16_t ent, float wgt, float p0, float p1, float p2) {
+      const float we = c.lam_rc * wgt;
       const float d0 = yr[0] - p0, d1 = yr[1] - p1, d2 = yr[2] - p2;
       if (!(ent & kEntIncoming)) ec = fmaf(we, fmaf(d0, d0, fmaf(d1, d1, d2 * d2)), ec);
       gc0 = fmaf(we, d0, gc0);
       gc1 = fmaf(we, d1, gc1);
       gc2 = fmaf(we, d2, gc2);
       dcons += we;
+    };
+    // four entries per round: their loads are issued together, the
+    // accumulation stays in CSR order
+    int e = e0;
+    for (; e + 4 <= e1; e += 4) {
+      uint16_t q[4];
+      float wv[4], pv[4][3];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        q[j] = __ldg(f.ent + e + j);
+        wv[j] = f.ent_w ? __ldg(f.ent_w + e + j) : 1.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) partner(q[j], pv[j][0], pv[j][1], pv[j][2]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) accum(q[j], wv[j], pv[j][0], pv[j][1], pv[j][2]);
+    }
+    for (; e < e1; ++e) {
+      const uint16_t ent = __ldg(f.ent + e);
+      float p0, p1, p2;
+      partner(ent, p0, p1, p2);
+      accum(ent, f.ent_w ? __ldg(f.ent_w + e) : 1.f, p0, p1, p2);
     }
     acc[T_CONSIST] += (double)ec;
   }
@@ -525,6 +569,7 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
     float* sXR = sX + e_off_XR(NT);
     float* sD = sX + e_off_D(NT);
     float* sDR = sX + e_off_DR(NT);
+    const EPre pre = energy_prefetch(f, tx0 + lx, ty0 + ly, tx0 + lx < W && ty0 + ly < f.y_hi);
     if (TMA) {
       mbar_wait(&bars[st], (phase >> st) & 1u);
       phase ^= 1u << st;
@@ -550,10 +595,10 @@ __global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, con
     const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H && ty0 + kTileH <= f.y_hi;
     if (interior)
       energy_pixel<NT, MODE, true>(f, c, sX, sXR, sYT, sYR, tx0 + lx, ty0 + ly, cx, cy, rx, ry, Xout, r_out, d_out,
-                                   u_out, b_raw, diag_raw, acc);
+                                   u_out, b_raw, diag_raw, acc, pre);
     else if (tx0 + lx < W && ty0 + ly < f.y_hi)
       energy_pixel<NT, MODE, false>(f, c, sX, sXR, sYT, sYR, tx0 + lx, ty0 + ly, cx, cy, rx, ry, Xout, r_out, d_out,
-                                    u_out, b_raw, diag_raw, acc);
+                                    u_out, b_raw, diag_raw, acc, pre);
     if (TMA) {
       __syncthreads();
       if (threadIdx.x == 0) {
