@@ -137,3 +137,8 @@ def decompose_frames(frames: list, weights: EnergyWeights, config: SolveConfig, 
             on_frame(idx, state)
     result.palette = dec.palette
     return result
+
+
+# disk-to-disk pipeline and per-frame outputs (pipeline.py:183-270)
+from .frameio import (find_frames, run_pipeline, write_diagnostics,  # noqa: E402,F401
+                      write_frame_outputs)
