@@ -370,6 +370,17 @@ def run_ours(args):
                                 "frac": 4 * H * W * (860 * U + 298) / (t_ms / steps / 1e3) / 1e9 / split / peak,
                                 "note": "per GPU"}}
 
+    # --- frame 1 again with everything warm (refinement path, host-driven) ---
+    first_warm_ms = None
+    if not args.profile_only:
+        dec1 = StreamingDecomposer(pal, EnergyWeights(), cfg, seed=pal_seed, bands=bands)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dec1.first(frames[0])
+        torch.cuda.synchronize()
+        first_warm_ms = (time.perf_counter() - t0) * 1e3
+        del dec1
+
     # --- e2e through the public API with host buffers ---
     e2e = None
     if e2e_on:
@@ -401,7 +412,8 @@ def run_ours(args):
         e2e = {"value": eth.fps, "unit": UNIT,
                "h2d_bytes_per_step": int(host[0].numel() * 4),
                "d2h_bytes_per_step": int(out_host[0].numel() * 4),
-               "api": "pipeline.StreamingDecomposer.step (reference decompose_frames loop)"}
+               "api": "pipeline.StreamingDecomposer.step (reference decompose_frames loop); "
+                      "frame i's D2H on a copy stream beside frame i+1's solve"}
 
     # --- CPU baseline (rank 0, N = 1 only) ---
     cpu = None
@@ -433,7 +445,8 @@ def run_ours(args):
                            "bands": nb_total,
                            "H": H, "W": W, "K": K, "gn_steps_per_frame": 4, "pcg_iterations": 16,
                            "l2": "per-frame working set (~0.9 GB) exceeds the 126 MB L2; no flush",
-                           "first_frame_ms": first_ms, "first_frame_records": n_first_records,
+                           "first_frame_ms": first_ms, "first_frame_warm_ms": first_warm_ms,
+                           "first_frame_records": n_first_records,
                            "wall_ms_per_step": wall_ms / steps},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": prof["launches"], "clocks": clk}
