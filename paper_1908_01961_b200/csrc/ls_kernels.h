@@ -47,8 +47,6 @@ void launch_apply(const Launch& L, const Frame& f, const Coef<float>& c, const f
                   float* w, double* part, unsigned* ticket, Scalars* sc, int iter, const TileMaps* maps);
 int tile_box_w();
 int tile_box_rw();
-void launch_update(const Launch& L, int64_t M, float* x, float* r, float* p, float* s, const float* w,
-                   const float* d, float* u, double* part, unsigned* ticket, Scalars* sc, int iter);
 void launch_pcg_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* z,
                       const float* pprev, float* pnew, float* q, double* part, unsigned* ticket, Scalars* sc,
                       int iter, const PcgMaps* maps, float* x);

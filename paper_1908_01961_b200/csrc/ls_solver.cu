@@ -6,9 +6,12 @@
 //   k_energy<NT, MODE_TRIAL> line-search trial: candidate Y = X + a*dx (or an
 //                            external Y) written, 8 energies with the IRLS
 //                            weights frozen at X (solver.py:166-178)
-//   k_apply<NT>              w = J^T J u (matrix-free, solver.py:110-122)
-//                            + <w,u>; last block advances the PCG scalars
-//   k_update                 Chronopoulos-Gear vector update + <r,u>, |r|^2
+//   k_apply<NT>              w = J^T J u (matrix-free, solver.py:110-122), the
+//                            API operator (ls_apply_normal)
+//   k_pcg_apply<NT>          PCG iteration: p = z + beta p formed over the
+//                            tile + halo, q = J^T J p, <p,q>, deferred x-update
+//   k_pcg_update             r -= alpha q, z = r / diag, <r,z>, |r|^2
+//   k_pcg_xfinal             the last deferred x-update
 //
 // Tile scheme: persistent blocks of 256 threads walk 32x8 pixel tiles (one
 // warp per tile row).  Each tile stages in shared memory
@@ -846,93 +849,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_apply(Frame f, Coef<float> c, c
     accd += (double)acc;   // fp64 across tiles
     acc = 0.f;
   }
-  if (!sc) return;
-  double accv[1] = {accd};
-  block_reduce_store<1>(accv, part);
-  if (!last_block(ticket)) return;
-  const double delta = sum_partials<1>(part, gridDim.x, 0);
-  if (threadIdx.x == 0) {
-    // Chronopoulos-Gear: the denominator equals p.Ap of the textbook loop
-    // (solver.py:93-97); same break rule
-    double beta = 0.0, denom = delta;
-    if (iter > 0) {
-      beta = sc->gamma / sc->gamma_prev;
-      denom = delta - beta * sc->gamma / sc->alpha_prev;
-    }
-    sc->delta = delta;
-    sc->beta = beta;
-    if (!(denom > 0.0) || !isfinite(denom)) sc->stop = 1;
-    else sc->alpha = sc->gamma / denom;
-    *ticket = 0u;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// PCG vector update (pointwise, float4):  p = u + b p ; s = w + b s ;
-// x += a p ; r -= a s ; u = r / d   and partials <r,u>, <r,r>
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_update(int64_t M, float* __restrict__ x, float* __restrict__ r,
-                                                     float* __restrict__ p, float* __restrict__ s,
-                                                     const float* __restrict__ w, const float* __restrict__ d,
-                                                     float* __restrict__ u, double* part, unsigned* ticket,
-                                                     Scalars* sc, int iter) {
-  if (sc->stop) return;
-  const float a = (float)sc->alpha, b = (float)sc->beta;
-  const bool first = (iter == 0);
-  double acc[2] = {0.0, 0.0};
-  const int64_t M4 = M >> 2;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M4; j += stride) {
-    float4 uu = reinterpret_cast<const float4*>(u)[j];
-    float4 ww = __ldg(reinterpret_cast<const float4*>(w) + j);
-    float4 rr = reinterpret_cast<const float4*>(r)[j];
-    float4 dd = __ldg(reinterpret_cast<const float4*>(d) + j);
-    float4 pp, ss, xx;
-    if (first) {
-      pp = uu; ss = ww;
-      xx = make_float4(a * pp.x, a * pp.y, a * pp.z, a * pp.w);
-    } else {
-      pp = reinterpret_cast<const float4*>(p)[j];
-      ss = reinterpret_cast<const float4*>(s)[j];
-      xx = reinterpret_cast<const float4*>(x)[j];
-      pp = make_float4(fmaf(b, pp.x, uu.x), fmaf(b, pp.y, uu.y), fmaf(b, pp.z, uu.z), fmaf(b, pp.w, uu.w));
-      ss = make_float4(fmaf(b, ss.x, ww.x), fmaf(b, ss.y, ww.y), fmaf(b, ss.z, ww.z), fmaf(b, ss.w, ww.w));
-      xx = make_float4(fmaf(a, pp.x, xx.x), fmaf(a, pp.y, xx.y), fmaf(a, pp.z, xx.z), fmaf(a, pp.w, xx.w));
-    }
-    rr = make_float4(fmaf(-a, ss.x, rr.x), fmaf(-a, ss.y, rr.y), fmaf(-a, ss.z, rr.z), fmaf(-a, ss.w, rr.w));
-    uu = make_float4(rr.x / dd.x, rr.y / dd.y, rr.z / dd.z, rr.w / dd.w);
-    reinterpret_cast<float4*>(p)[j] = pp;
-    reinterpret_cast<float4*>(s)[j] = ss;
-    reinterpret_cast<float4*>(x)[j] = xx;
-    reinterpret_cast<float4*>(r)[j] = rr;
-    reinterpret_cast<float4*>(u)[j] = uu;
-    acc[0] += (double)rr.x * uu.x + (double)rr.y * uu.y + (double)rr.z * uu.z + (double)rr.w * uu.w;
-    acc[1] += (double)rr.x * rr.x + (double)rr.y * rr.y + (double)rr.z * rr.z + (double)rr.w * rr.w;
-  }
-  // scalar tail (M not a multiple of 4)
-  for (int64_t j = (M4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride) {
-    float uu = u[j], ww = w[j], rr = r[j], dd = d[j], pp, ss, xx;
-    if (first) { pp = uu; ss = ww; xx = a * pp; }
-    else { pp = fmaf(b, p[j], uu); ss = fmaf(b, s[j], ww); xx = fmaf(a, pp, x[j]); }
-    rr = fmaf(-a, ss, rr);
-    uu = rr / dd;
-    p[j] = pp; s[j] = ss; x[j] = xx; r[j] = rr; u[j] = uu;
-    acc[0] += (double)rr * uu;
-    acc[1] += (double)rr * rr;
-  }
-  block_reduce_store<2>(acc, part);
-  if (!last_block(ticket)) return;
-  const double g = sum_partials<2>(part, gridDim.x, 0);
-  const double rn = sum_partials<2>(part, gridDim.x, 1);
-  if (threadIdx.x == 0) {
-    sc->iterations = iter + 1;
-    sc->gamma_prev = sc->gamma;
-    sc->gamma = g;
-    sc->alpha_prev = sc->alpha;
-    sc->rnorm2 = rn;
-    if (g <= 0.0) sc->stop = 1;   // solver.py:101-103
-    *ticket = 0u;
-  }
+  (void)accd;   // the API operator (ls_apply_normal) needs no reduction
 }
 
 // ---------------------------------------------------------------------------
@@ -1449,10 +1366,6 @@ int pcg_apply_grid_limit(int NT) {
   return nb;
 }
 
-void launch_update(const Launch& L, int64_t M, float* x, float* r, float* p, float* s, const float* w,
-                   const float* d, float* u, double* part, unsigned* ticket, Scalars* sc, int iter) {
-  k_update<<<L.grid, kThreads, 0, L.stream>>>(M, x, r, p, s, w, d, u, part, ticket, sc, iter);
-}
 
 int energy_grid_limit(int NT) {
   int nb = 0;
@@ -1472,7 +1385,7 @@ int tile_box_w() { return kSW; }
 int tile_box_rw() { return kRW; }
 int update_grid_limit() {
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_update, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg_update, kThreads, 0);
   return nb;
 }
 
