@@ -257,7 +257,7 @@ def run_ours(args):
     H, W, K = args.height, args.width, args.K
     steps, warmup = args.steps, args.warmup
     e2e_on = not (args.no_e2e or args.profile_only)
-    n_frames = 1 + warmup + steps + (steps if e2e_on else 0)
+    n_frames = 1 + warmup + 2 * steps + (steps if e2e_on else 0)
     four_k = args.workload == "4k"
     pal_seed = 0 if four_k else rank      # 4k: every rank holds a band of the same clip
     clip = synth.make_clip(H, W, K, n_frames, seed=pal_seed, device=dev)
@@ -292,23 +292,34 @@ def run_ours(args):
     else:
         prof_solvers = [_device.get_solver(dev, H, W, K)]
     for ps in prof_solvers:
-        ps.profile(True)
+        ps.profile(False)              # resets the launch counters; no per-kernel events
     clocks = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local])
                           if os.environ.get("CUDA_VISIBLE_DEVICES") else local)
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
+
+    def timed(first_frame):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        e_a.record()
+        for i in range(steps):
+            dec.step(frames[first_frame + i])
+        e_b.record()
+        torch.cuda.synchronize()
+        return e_a.elapsed_time(e_b), (time.perf_counter() - w0) * 1e3
+
+    # (1) the headline: K frames, nothing but the solve in the timed region
     clocks.start()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    wall0 = time.perf_counter()
-    ev0.record()
-    for i in range(steps):
-        st = dec.step(frames[1 + warmup + i])
-    ev1.record()
-    torch.cuda.synchronize()
-    wall_ms = (time.perf_counter() - wall0) * 1e3
+    t_ms, wall_ms = timed(1 + warmup)
     clk = clocks.stop()
-    t_ms = ev0.elapsed_time(ev1)
+    launches = sum(ps.profile_read()["launches"] for ps in prof_solvers)
+    # (2) the next K frames again with CUDA events around every solver kernel
+    #     (per-kernel durations for the roofline; the events cost ~5% of the
+    #     frame time, so this pass is not the headline)
+    for ps in prof_solvers:
+        ps.profile(True)
+    prof_t_ms, _ = timed(1 + warmup + steps)
     prof = None
     for ps in prof_solvers:
         pr = ps.profile_read()
@@ -350,7 +361,7 @@ def run_ours(args):
     peak, peak_src = peaks()
     achieved = bpl / (avg_ms / 1e3) / 1e9
     per_kernel = {k: {"launches": v[0]["count"], "avg_us": 1e3 * v[0]["ms"] / max(v[0]["count"], 1),
-                      "share_of_step": v[0]["ms"] / t_ms if world == 1 else None,
+                      "share_of_step": v[0]["ms"] / prof_t_ms if world == 1 else None,
                       "algorithmic_bytes": v[1],
                       "achieved_gbs": v[1] / (v[0]["ms"] / max(v[0]["count"], 1) / 1e3) / 1e9
                       if v[0]["count"] else None}
@@ -363,6 +374,8 @@ def run_ours(args):
                 "kernel": kname[dom], "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bpl, "avg_launch_us": avg_ms * 1e3,
                 "per_kernel": per_kernel,
+                "timing": f"per-kernel CUDA events over a second timed pass of {steps} frames "
+                          f"({prof_t_ms / steps:.2f} ms/frame with the events)",
                 # SURVEY.md 8(d) compulsory-traffic model of a whole streaming
                 # frame, B_frame = 4 N (860 U + 298) bytes, over the measured frame time
                 "frame_model": {"bytes": 4 * H * W * (860 * U + 298),
@@ -384,7 +397,7 @@ def run_ours(args):
     # --- e2e through the public API with host buffers ---
     e2e = None
     if e2e_on:
-        host = [frames[1 + warmup + steps + i].cpu().pin_memory() for i in range(steps)]
+        host = [frames[1 + warmup + 2 * steps + i].cpu().pin_memory() for i in range(steps)]
         out_host = [torch.empty(tuple(st.layers.X.shape), dtype=torch.float32).pin_memory() for _ in range(2)]
         side = torch.cuda.Stream(device=dev)
         torch.cuda.synchronize()
@@ -449,7 +462,7 @@ def run_ours(args):
                            "first_frame_records": n_first_records,
                            "wall_ms_per_step": wall_ms / steps},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": prof["launches"], "clocks": clk}
+                "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -187,6 +187,13 @@ LS_API int ls_gn_step(ls_ctx* ctx, const double* colors_host, const float* X, fl
 LS_API int ls_flip_flop_stream(ls_ctx* ctx, const double* colors_host, float* X0, float* X1, float* X2, int outer,
                                int gn_steps, double tol_rel, ls_gn_record* out, int* n_records, int* status,
                                int* final_buffer, int* fault_step);
+/* ls_flip_flop_stream as ONE CUDA graph launch (captured on first use over
+ * context-owned state buffers, replayed while palette, weights, config and
+ * the frame's buffers are unchanged -- the streaming case).  X_in is copied
+ * in, the final state is written to X_out (stream-ordered after return). */
+LS_API int ls_flip_flop_graph(ls_ctx* ctx, const double* colors_host, const float* X_in, float* X_out, int outer,
+                              int gn_steps, double tol_rel, ls_gn_record* out, int* n_records, int* status,
+                              int* fault_step);
 /* Dense 3K x 3K refinement normal system at delta_b = 0 (energy.py:563-610);
  * uses the cluster ids set by ls_set_anchor when use_ids != 0.  Host outputs. */
 LS_API int ls_dense_normal(ls_ctx* ctx, const double* colors_host, const float* X, int use_ids,

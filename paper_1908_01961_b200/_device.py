@@ -8,6 +8,7 @@ or CUDA device raises (no CPU path).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 
 import numpy as np
@@ -239,10 +240,26 @@ class DeviceSolver:
             self._chk(rc)
         return rc, rec
 
-    def flip_flop_stream(self, colors, X0, outer: int, gn_steps: int, tol_rel: float):
+    def flip_flop_stream(self, colors, X0, outer: int, gn_steps: int, tol_rel: float,
+                         graph: bool | None = None):
         """Device-resident streaming flip-flop; returns (rc, records, status,
-        final state tensor, fault step)."""
+        final state tensor, fault step).  By default one CUDA-graph launch
+        (ls_flip_flop_graph); LS_NO_GRAPH=1 or graph=False enqueues the
+        kernels one by one (ls_flip_flop_stream) -- same results, bit for bit."""
         a, pa = L.dbl_array(colors)
+        if graph is None:
+            graph = not os.environ.get("LS_NO_GRAPH")
+        if graph:
+            Xo = torch.empty_like(X0)
+            n = max(1, outer * gn_steps)
+            recs = (L.GNRecord * n)()
+            nrec, status, fault = C.c_int(), C.c_int(), C.c_int()
+            self._enter()
+            rc = self.lib.ls_flip_flop_graph(self.ctx, pa, L.dptr(X0), L.dptr(Xo), int(outer), int(gn_steps),
+                                             float(tol_rel), recs, C.byref(nrec), C.byref(status), C.byref(fault))
+            if rc not in (L.LS_OK, L.LS_ERR_NONFINITE):
+                self._chk(rc)
+            return rc, [recs[i] for i in range(nrec.value)], status.value, Xo, fault.value
         X1 = torch.empty_like(X0)
         X2 = torch.empty_like(X0)
         n = max(1, outer * gn_steps)

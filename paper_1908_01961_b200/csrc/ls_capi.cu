@@ -146,6 +146,12 @@ struct ls_ctx {
   double* bsum = nullptr;        // 512 doubles
   long long* zlist = nullptr;    // kZeroList
   int* seg_sum = nullptr;        // 4 ints
+  float* ring[3] = {nullptr, nullptr, nullptr};   // state buffers of the graph flip-flop
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  unsigned char graph_key[1024] = {0};
+  long long graph_launches = 0;
+  int graph_steps = 0;
   const long long* band_zeros = nullptr;   // gathered zero lists (caller memory) for the next draw
   int band_zero_lists = 0;
   std::vector<void*> allocs;
@@ -393,6 +399,8 @@ int ls_ctx_destroy(ls_ctx* c) {
   if (!c) return LS_OK;
   cudaSetDevice(c->dev);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (void* p : c->allocs) cudaFree(p);
   for (auto& e : c->prof.pool) cudaEventDestroy(e);
   cudaFree(c->ent);
@@ -884,27 +892,22 @@ int ls_gn_step(ls_ctx* c, const double* colors, const float* X, float* X_out, ls
 // Whole streaming flip-flop (solver.py:311-338 with refine = False) enqueued
 // without host round trips: per GN step the EG kernel, the PCG, up to
 // max_halvings+1 trial kernels deciding accept / halve on the device, and a
-// step-end kernel; per outer iteration the convergence test.  One host
-// synchronisation at the end to read the records.
-extern "C" int ls_flip_flop_stream(ls_ctx* c, const double* colors, float* X0, float* X1, float* X2, int outer,
-                                   int gn_steps, double tol_rel, ls_gn_record* out, int* n_records, int* status,
-                                   int* final_buffer, int* fault_step) {
-  int rc = whole_frame_only(c);
-  if (!rc) rc = check_ready(c);
-  if (rc) return rc;
-  LS_ARG(X0 && X1 && X2 && out && n_records && status && final_buffer && fault_step, "bad arguments");
-  LS_ARG(outer >= 0 && gn_steps >= 0 && (int64_t)outer * gn_steps <= kMaxStepRecords, "too many GN steps");
-  LS_CK(cudaSetDevice(c->dev));
+// step-end kernel; per outer iteration the convergence test; finally the
+// device -> pinned-host copies of the control block and the step records.
+// `bufs` are the three state buffers (bufs[0] holds the input).  Enqueue only
+// (also used under stream capture for the CUDA-graph variant).
+static int enqueue_flip_flop(ls_ctx* c, const double* colors, float* const bufs[3], int outer, int gn_steps,
+                             double tol_rel, int* nsteps) {
   const Frame f = frame_of(c);
   const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
   const int64_t M = (int64_t)c->U * c->N;
-  float* bufs[3] = {X0, X1, X2};
   launch_frame_init(c->stream, c->ctl);
+  c->launches += 1;
   int k = 0;
   for (int o = 0; o < outer; ++o) {
     for (int g = 0; g < gn_steps; ++g, ++k) {
       const int in_id = (k == 0) ? 0 : 1 + ((k - 1) & 1), out_id = 1 + (k & 1);
-      rc = run_pcg(c, colors, bufs[in_id], c->cfg.pcg_iterations, c->x, c->ctl);
+      const int rc = run_pcg(c, colors, bufs[in_id], c->cfg.pcg_iterations, c->x, c->ctl);
       if (rc) return rc;
       EnergyMaps em;
       const bool etma = energy_maps(c, bufs[in_id], c->x, &em);
@@ -926,10 +929,14 @@ extern "C" int ls_flip_flop_stream(ls_ctx* c, const double* colors, float* X0, f
   LS_CK(cudaMemcpyAsync(c->ctl_host, c->ctl, sizeof(FrameCtl), cudaMemcpyDeviceToHost, c->stream));
   if (k > 0)
     LS_CK(cudaMemcpyAsync(c->recs_host, c->recs, sizeof(StepRecord) * k, cudaMemcpyDeviceToHost, c->stream));
-  if (!c->sampled_counts_known)
-    LS_CK(cudaMemcpyAsync(c->host_buf, &c->sstate->error, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  LS_CK(cudaStreamSynchronize(c->stream));
-  prof_harvest(c);
+  LS_CK(cudaMemcpyAsync(c->host_buf, &c->sstate->error, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  *nsteps = k;
+  return LS_OK;
+}
+
+// after the stream synchronisation: records, status, state buffer
+static int finish_flip_flop(ls_ctx* c, ls_gn_record* out, int* n_records, int* status, int* final_buffer,
+                            int* fault_step) {
   if (!c->sampled_counts_known && *reinterpret_cast<int*>(c->host_buf)) {
     g_err = "consistency sampler: too many PCG64 rejections in one frame";
     return LS_ERR_CUDA;
@@ -953,6 +960,125 @@ extern "C" int ls_flip_flop_stream(ls_ctx* c, const double* colors, float* X0, f
   *final_buffer = ctl.cur;
   *fault_step = ctl.fault_step;
   return ctl.fault_step >= 0 ? LS_ERR_NONFINITE : LS_OK;
+}
+
+extern "C" int ls_flip_flop_stream(ls_ctx* c, const double* colors, float* X0, float* X1, float* X2, int outer,
+                                   int gn_steps, double tol_rel, ls_gn_record* out, int* n_records, int* status,
+                                   int* final_buffer, int* fault_step) {
+  int rc = whole_frame_only(c);
+  if (!rc) rc = check_ready(c);
+  if (rc) return rc;
+  LS_ARG(X0 && X1 && X2 && out && n_records && status && final_buffer && fault_step, "bad arguments");
+  LS_ARG(outer >= 0 && gn_steps >= 0 && (int64_t)outer * gn_steps <= kMaxStepRecords, "too many GN steps");
+  LS_CK(cudaSetDevice(c->dev));
+  float* const bufs[3] = {X0, X1, X2};
+  int k = 0;
+  rc = enqueue_flip_flop(c, colors, bufs, outer, gn_steps, tol_rel, &k);
+  if (rc) return rc;
+  LS_CK(cudaStreamSynchronize(c->stream));
+  prof_harvest(c);
+  return finish_flip_flop(c, out, n_records, status, final_buffer, fault_step);
+}
+
+// The same flip-flop as ONE CUDA graph launch.  The graph is captured once
+// over context-owned state buffers (so every pointer it bakes in -- kernel
+// arguments and TMA descriptors -- stays valid) and replayed while the
+// palette, weights, configuration and per-frame buffers are unchanged (the
+// streaming case: the palette is frozen after frame 1).  Per frame: copy
+// X_in into the ring, launch, synchronise, copy the final state to X_out.
+struct GraphKey {
+  double colors[3 * LS_MAX_K];
+  ls_weights w;
+  ls_solve_cfg cfg;
+  Frame f;
+  int outer, gn_steps, use_tma, pad;
+  double tol_rel;
+  cudaStream_t stream;
+};
+
+static_assert(sizeof(GraphKey) <= 1024, "graph key buffer");
+
+extern "C" int ls_flip_flop_graph(ls_ctx* c, const double* colors, const float* X_in, float* X_out, int outer,
+                                  int gn_steps, double tol_rel, ls_gn_record* out, int* n_records, int* status,
+                                  int* fault_step) {
+  int rc = whole_frame_only(c);
+  if (!rc) rc = check_ready(c);
+  if (rc) return rc;
+  LS_ARG(X_in && X_out && out && n_records && status && fault_step, "bad arguments");
+  LS_ARG(outer >= 0 && gn_steps >= 0 && (int64_t)outer * gn_steps <= kMaxStepRecords, "too many GN steps");
+  LS_CK(cudaSetDevice(c->dev));
+  const size_t bytes = sizeof(float) * (size_t)c->U * c->N;
+  if (!c->ring[0])
+    for (float*& r : c->ring) LS_CK(dalloc(c, &r, (size_t)c->U * c->N));
+  GraphKey key;
+  std::memset(&key, 0, sizeof(key));
+  for (int i = 0; i < 3 * c->K; ++i) key.colors[i] = colors[i];
+  key.w = c->w;
+  key.cfg = c->cfg;
+  key.f = frame_of(c);
+  key.outer = outer;
+  key.gn_steps = gn_steps;
+  key.use_tma = c->use_tma;
+  key.tol_rel = tol_rel;
+  key.stream = c->stream;
+  const bool reuse = c->graph_exec && !c->prof.on && std::memcmp(&key, c->graph_key, sizeof(key)) == 0;
+  LS_CK(cudaMemcpyAsync(c->ring[0], X_in, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  int k = 0;
+  if (c->prof.on) {   // profiling records events around kernels: run eagerly
+    rc = enqueue_flip_flop(c, colors, c->ring, outer, gn_steps, tol_rel, &k);
+    if (rc) return rc;
+  } else {
+    if (!reuse) {
+      if (c->graph_exec) {
+        cudaGraphExecDestroy(c->graph_exec);
+        c->graph_exec = nullptr;
+      }
+      const long long before = c->launches;
+      cudaGraph_t g = nullptr;
+      // capture on a private stream (the caller's may be the legacy default
+      // stream, which cannot capture); the graph is launched on the caller's
+      if (!c->cap_stream) LS_CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+      cudaStream_t user = c->stream;
+      c->stream = c->cap_stream;
+      cudaError_t be = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+      if (be != cudaSuccess) {
+        c->stream = user;
+        g_err = std::string("graph capture: ") + cudaGetErrorString(be);
+        return LS_ERR_CUDA;
+      }
+      rc = enqueue_flip_flop(c, colors, c->ring, outer, gn_steps, tol_rel, &k);
+      const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+      c->stream = user;
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (ce != cudaSuccess) {
+        g_err = std::string("graph capture: ") + cudaGetErrorString(ce);
+        return LS_ERR_CUDA;
+      }
+      const cudaError_t ie = cudaGraphInstantiate(&c->graph_exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ie != cudaSuccess) {
+        c->graph_exec = nullptr;
+        g_err = std::string("graph instantiate: ") + cudaGetErrorString(ie);
+        return LS_ERR_CUDA;
+      }
+      c->graph_launches = c->launches - before;
+      c->graph_steps = k;
+      c->launches = before;
+      std::memcpy(c->graph_key, &key, sizeof(key));
+    }
+    k = c->graph_steps;
+    LS_CK(cudaGraphLaunch(c->graph_exec, c->stream));
+    c->launches += c->graph_launches;
+  }
+  LS_CK(cudaStreamSynchronize(c->stream));
+  prof_harvest(c);
+  int final_buffer = 0;
+  rc = finish_flip_flop(c, out, n_records, status, &final_buffer, fault_step);
+  LS_CK(cudaMemcpyAsync(X_out, c->ring[final_buffer], bytes, cudaMemcpyDeviceToDevice, c->stream));
+  return rc;
 }
 
 static int dense_system(ls_ctx* c, const double* colors, const float* X, int use_ids) {

@@ -208,3 +208,28 @@ def test_device_flip_flop_equals_host_loop():
     for a, b in zip(r0, r1):
         assert a == b
     assert torch.equal(X0, X1)
+
+
+def test_graph_flip_flop_equals_eager_and_replays():
+    """ls_flip_flop_graph (one CUDA-graph launch, captured once and replayed
+    for the next frames) gives the eager ls_flip_flop_stream's records and
+    state bit for bit, frame after frame."""
+    import os
+    from paper_1908_01961_b200.energy import EnergyWeights
+    from paper_1908_01961_b200.palette import BaseColorPalette
+    from paper_1908_01961_b200.pipeline import StreamingDecomposer
+    from paper_1908_01961_b200.solver import SolveConfig
+    clip = _clip(96, 128, 4, n=4, seed=12)
+    runs = []
+    for no_graph in ("", "1"):
+        os.environ["LS_NO_GRAPH"] = no_graph
+        try:
+            dec = StreamingDecomposer(BaseColorPalette(colors=clip.colors), EnergyWeights(),
+                                      SolveConfig(tol_rel=0.0, refine=False, outer_iterations=2))
+            sts = [dec.first(clip.frames[0].cuda())] + [dec.step(f.cuda()) for f in clip.frames[1:]]
+            runs.append([(s.records, s.status, s.layers.X.clone()) for s in sts])
+        finally:
+            os.environ.pop("LS_NO_GRAPH", None)
+    for (ra, sa, Xa), (rb, sb, Xb) in zip(*runs):
+        assert ra == rb and sa == sb
+        assert torch.equal(Xa, Xb)
