@@ -286,8 +286,10 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
     acc[T_RSPARSE] += (double)(wrs * e);
   }
 
-  // per-layer diagonal terms and smoothness (energy.py:414-452, 308-318)
-  float wd[NT];
+  // per-layer diagonal terms and smoothness (energy.py:414-452, 308-318); in
+  // MODE_EG the T_k rows of g = J^T F and diag(J^T J) are produced in the
+  // same pass, reusing the two smoothness weights the energy needs
+  float rz = 0.f, bb = 0.f;
   {
     float eis = 0.f, enn = 0.f, esm = 0.f;
 #pragma unroll
@@ -296,16 +298,48 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
       const float* Q = sYT + k * kSP + sc0;
       const float wis = (k >= 1) ? c.lam_is * irls1f(T0[k], c) : 0.f;
       const float wnn = c.lam_nn * nonneg_wf(T0[k], c.eps_nn);
-      wd[k] = wis + wnn;
       eis = fmaf(wis * yT[k], yT[k], eis);
       enn = fmaf(wnn * yT[k], yT[k], enn);
+      float wx = 0.f, wy = 0.f;
       if (hx) {
+        wx = irls1f(P[1] - T0[k], c);
         const float g = Q[1] - yT[k];
-        esm = fmaf(irls1f(P[1] - T0[k], c) * g, g, esm);
+        esm = fmaf(wx * g, g, esm);
       }
       if (hy) {
+        wy = irls1f(P[kSW] - T0[k], c);
         const float g = Q[kSW] - yT[k];
-        esm = fmaf(irls1f(P[kSW] - T0[k], c) * g, g, esm);
+        esm = fmaf(wy * g, g, esm);
+      }
+      if (MODE == MODE_EG) {
+        float g = 0.f, d = 0.f, gm = 0.f, g2 = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const float rb = R[ch] * c.B[k][ch];
+          g = fmaf(rb, res[ch], g);
+          d = fmaf(rb, rb, d);
+          gm = fmaf(c.G[k][ch], m[ch], gm);
+          g2 = fmaf(c.G[k][ch], c.G[k][ch], g2);
+        }
+        const float wdk = wis + wnn;
+        g = fmaf(-c.lam_d, g, fmaf(lm, gm, wdk * T0[k]));
+        d = fmaf(c.lam_d, d, fmaf(lm, g2, wdk));
+        const float v = T0[k];
+        float gs = 0.f, ds = 0.f;
+        if (hx) { gs = fmaf(wx, v - P[1], gs); ds += wx; }
+        if (hl) { const float a = irls1f(v - P[-1], c); gs = fmaf(a, v - P[-1], gs); ds += a; }
+        if (hy) { gs = fmaf(wy, v - P[kSW], gs); ds += wy; }
+        if (hu) { const float a = irls1f(v - P[-kSW], c); gs = fmaf(a, v - P[-kSW], gs); ds += a; }
+        g = fmaf(c.lam_sm, gs, g);
+        d = fmaf(c.lam_sm, ds, d);
+        const float bf = -g;
+        const float di = 1.f / (d > 0.f ? d : 1.f);   // Jacobi preconditioner (solver.py:87)
+        const float zf = bf * di;
+        const size_t o = (size_t)(3 + k) * N + i;
+        if (r_out) { r_out[o] = bf; d_out[o] = di; u_out[o] = zf; }
+        if (b_raw) { b_raw[o] = bf; diag_raw[o] = d; }
+        rz = fmaf(bf, zf, rz);
+        bb = fmaf(bf, bf, bb);
       }
     }
     acc[T_ISPARSE] += (double)eis;
@@ -385,7 +419,6 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
   const float wl = hl ? wrs_s(sXR, rx - 1, ry, true, hy, c, kRW, kRP) : 0.f;
   const float wu = hu ? wrs_s(sXR, rx, ry - 1, hx, true, c, kRW, kRP) : 0.f;
   const float gcons[3] = {gc0, gc1, gc2};
-  float rz = 0.f, bb = 0.f;
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
     const float* P = sXR + ch * kRP + rc0;
@@ -404,37 +437,6 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
     const float zf = bf * di;
     if (r_out) { r_out[ch * N + i] = bf; d_out[ch * N + i] = di; u_out[ch * N + i] = zf; }
     if (b_raw) { b_raw[ch * N + i] = bf; diag_raw[ch * N + i] = d; }
-    rz = fmaf(bf, zf, rz);
-    bb = fmaf(bf, bf, bb);
-  }
-#pragma unroll
-  for (int k = 0; k < NT; ++k) {
-    const float* P = sX + (3 + k) * kSP + sc0;
-    float g = 0.f, d = 0.f, gm = 0.f, g2 = 0.f;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      const float rb = R[ch] * c.B[k][ch];
-      g = fmaf(rb, res[ch], g);
-      d = fmaf(rb, rb, d);
-      gm = fmaf(c.G[k][ch], m[ch], gm);
-      g2 = fmaf(c.G[k][ch], c.G[k][ch], g2);
-    }
-    g = fmaf(-c.lam_d, g, fmaf(lm, gm, wd[k] * T0[k]));
-    d = fmaf(c.lam_d, d, fmaf(lm, g2, wd[k]));
-    const float v = T0[k];
-    float gs = 0.f, ds = 0.f;
-    if (hx) { const float a = irls1f(P[1] - v, c); gs = fmaf(a, v - P[1], gs); ds += a; }
-    if (hl) { const float a = irls1f(v - P[-1], c); gs = fmaf(a, v - P[-1], gs); ds += a; }
-    if (hy) { const float a = irls1f(P[kSW] - v, c); gs = fmaf(a, v - P[kSW], gs); ds += a; }
-    if (hu) { const float a = irls1f(v - P[-kSW], c); gs = fmaf(a, v - P[-kSW], gs); ds += a; }
-    g = fmaf(c.lam_sm, gs, g);
-    d = fmaf(c.lam_sm, ds, d);
-    const float bf = -g;
-    const float di = 1.f / (d > 0.f ? d : 1.f);
-    const float zf = bf * di;
-    const size_t o = (size_t)(3 + k) * N + i;
-    if (r_out) { r_out[o] = bf; d_out[o] = di; u_out[o] = zf; }
-    if (b_raw) { b_raw[o] = bf; diag_raw[o] = d; }
     rz = fmaf(bf, zf, rz);
     bb = fmaf(bf, bf, bb);
   }
@@ -516,7 +518,7 @@ __device__ void fin_pcg_update(double rz, double rn, Scalars* sc, int iter) {
 }
 
 template <int NT, int MODE, bool TMA>
-__global__ void __launch_bounds__(kThreads) k_energy(Frame f, Coef<float> c, const float* __restrict__ X,
+__global__ void __launch_bounds__(kThreads, 3) k_energy(Frame f, Coef<float> c, const float* __restrict__ X,
                                                      const float* __restrict__ dx, float alpha,
                                                      const float* __restrict__ Yext, float* __restrict__ Xout,
                                                      float* __restrict__ r_out, float* __restrict__ d_out,
