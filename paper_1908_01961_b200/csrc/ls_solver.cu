@@ -871,20 +871,23 @@ __host__ __device__ constexpr int op_floats(int NT) { return pad32(NT * kSP) + p
 __host__ __device__ constexpr int pcg_stage(int NT, bool) { return pad32((NT + 3) * kSP) + 2 * op_floats(NT); }
 
 template <int NT>
+// two barriers: bar[0] the operand windows (z, p_{i-1}) the formation pass
+// needs first, bar[1] the state window, which lands during the formation
 __device__ __forceinline__ void tma_issue_pcg(float* stage, const PcgMaps& m, uint64_t* bar, int tx0, int ty0,
                                               bool with_p) {
   constexpr uint32_t xb = sizeof(float) * (NT + 3) * kSP;
   constexpr uint32_t ob = sizeof(float) * (NT * kSP + 3 * kRP);
-  mbar_expect_tx(bar, xb + (with_p ? 2 : 1) * ob);
+  mbar_expect_tx(&bar[0], (with_p ? 2 : 1) * ob);
+  mbar_expect_tx(&bar[1], xb);
   float* z = stage + pad32((NT + 3) * kSP);
   float* pp = z + op_floats(NT);
-  tma_load_3d(stage, &m.X, bar, tx0 - kSX, ty0 - 1, 0);
-  tma_load_3d(z, &m.ZT, bar, tx0 - kSX, ty0 - 1, 0);
-  tma_load_3d(z + pad32(NT * kSP), &m.ZR, bar, tx0 - kRX, ty0 - kHalf, 0);
+  tma_load_3d(z, &m.ZT, &bar[0], tx0 - kSX, ty0 - 1, 0);
+  tma_load_3d(z + pad32(NT * kSP), &m.ZR, &bar[0], tx0 - kRX, ty0 - kHalf, 0);
   if (with_p) {
-    tma_load_3d(pp, &m.PT, bar, tx0 - kSX, ty0 - 1, 0);
-    tma_load_3d(pp + pad32(NT * kSP), &m.PR, bar, tx0 - kRX, ty0 - kHalf, 0);
+    tma_load_3d(pp, &m.PT, &bar[0], tx0 - kSX, ty0 - 1, 0);
+    tma_load_3d(pp + pad32(NT * kSP), &m.PR, &bar[0], tx0 - kRX, ty0 - kHalf, 0);
   }
+  tma_load_3d(stage, &m.X, &bar[1], tx0 - kSX, ty0 - 1, 0);
 }
 
 
@@ -901,7 +904,7 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
                                                            float* __restrict__ xv) {
   constexpr int U = NT + 3;
   extern __shared__ __align__(128) float smem[];
-  __shared__ __align__(8) uint64_t bars[1];
+  __shared__ __align__(8) uint64_t bars[2];
   if (sc->stop) return;
   const int W = f.W, H = f.H, N = f.N;
   const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
@@ -923,6 +926,7 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
   if (TMA) {
     if (threadIdx.x == 0) {
       mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
       fence_barrier_init();
       if ((int)blockIdx.x < ntiles) {
         const int t = blockIdx.x;
@@ -941,10 +945,8 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
     const int x = tx0 + lx, y = ty0 + ly;
     const bool own = x < W && y < f.y_hi;
     const PixPre pre = pix_prefetch(f, x, y, own);
-    if (TMA) {
-      mbar_wait(&bars[0], phase);
-      phase ^= 1u;
-    } else {
+    if (TMA) mbar_wait(&bars[0], phase);   // operand windows
+    else {
       __syncthreads();
       load_halo1<U>(sX, X, N, W, H, tx0, ty0);
       load_halo1<NT>(sZT, z + 3 * (size_t)N, N, W, H, tx0, ty0);
@@ -971,7 +973,12 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
       };
       form(sZT, sPT, NT * kSP / 4);
       form(sZR, sPR, 3 * kRP / 4);
-      __syncthreads();
+      if (!TMA) __syncthreads();
+    }
+    if (TMA) {   // state window (arrived during the formation); the wait's
+      mbar_wait(&bars[1], phase);   // acquire + the barrier below order the formed operand
+      phase ^= 1u;
+      if (with_p) __syncthreads();
     }
     const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < H && ty0 + kTileH <= f.y_hi;
     if (interior)
