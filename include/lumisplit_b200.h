@@ -223,6 +223,10 @@ LS_API int ls_dense_step(ls_ctx* ctx, double* colors_inout_host, const float* X,
  * the reference solves the frame as one problem (solver.py:143-192); the
  * bands reproduce that problem's arithmetic up to the summation grouping. */
 enum { LS_BAND_EG = 0, LS_BAND_APPLY = 1, LS_BAND_UPDATE = 2, LS_BAND_TRIAL = 3 };
+/* kernels this context launched (ls_profile resets it); a caller replaying
+ * captured ls_band_* work as its own CUDA graph adds the replayed launches */
+LS_API int ls_launch_count(ls_ctx* ctx, int64_t* n);
+LS_API int ls_add_launches(ls_ctx* ctx, int64_t n);
 LS_API int ls_band_set(ls_ctx* ctx, int gy0, int GH, int y_lo, int y_hi);
 LS_API int ls_band_clear(ls_ctx* ctx);
 /* out[6] = {partials (512 doubles), z, p_even, p_odd, x, r}: the PCG vectors
@@ -247,6 +251,23 @@ LS_API int ls_band_pcg_update(ls_ctx* ctx, int iter);
 LS_API int ls_band_pcg_finish(ls_ctx* ctx);
 LS_API int ls_band_trial(ls_ctx* ctx, const double* colors_host, const float* X, double alpha, float* X_out);
 LS_API int ls_band_finalize(ls_ctx* ctx, int phase, const double* gathered, int nbands, int iter, double alpha);
+/* Device-resident band flip-flop (the band form of ls_flip_flop_stream):
+ * frame_begin; per GN step eg / apply / update / finish as above, then up to
+ * max_halvings+1 trial_dev + finalize_dev(TRIAL, last) -- the accept / halve
+ * decision of solver.py:169-178 on the device, identical on every band --
+ * and step_end (state moves to X_out, copied through on a reject, record);
+ * per outer iteration outer_end (solver.py:328-336); frame_end reads the
+ * records (one synchronisation).  No host decision inside a frame, so the
+ * sequence with its gathers and halo copies can be one CUDA graph. */
+LS_API int ls_band_frame_begin(ls_ctx* ctx);
+LS_API int ls_band_trial_dev(ls_ctx* ctx, const double* colors_host, const float* X, double alpha, float* X_out,
+                             int last);
+LS_API int ls_band_finalize_dev(ls_ctx* ctx, int phase, const double* gathered, int nbands, int iter,
+                                double alpha, int last);
+LS_API int ls_band_step_end(ls_ctx* ctx, const float* X_in, float* X_out, int out_id);
+LS_API int ls_band_outer_end(ls_ctx* ctx, double tol_rel);
+LS_API int ls_band_frame_end(ls_ctx* ctx, int nsteps, ls_gn_record* out, int* n_records, int* status,
+                             int* final_buffer, int* fault_step);
 /* host out[21]: terms0[8], terms1[8], |b|^2, |r|^2, iterations, stop, xinit */
 LS_API int ls_band_read(ls_ctx* ctx, double* out_host);
 /* Dense system (energy.py:563-610) of the band's own pixels as partial sums

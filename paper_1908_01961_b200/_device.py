@@ -65,6 +65,7 @@ class DeviceSolver:
                                              C.byref(config_struct(SolveConfig())),
                                              C.byref(self.ctx)))
         self.installed = None       # (frame_key, aux_key) of the installed frame context
+        self.prof_on = False        # per-kernel CUDA events (no graph capture while on)
         self.sample_gen = 0         # bumps whenever the adjacency is rebuilt
         self.csr_owner = None       # device-backed ConsistencySamples using the adjacency
 
@@ -95,6 +96,7 @@ class DeviceSolver:
                                           C.byref(config_struct(config))))
 
     def profile(self, enable: bool):
+        self.prof_on = bool(enable)
         self._enter()
         self._chk(self.lib.ls_profile(self.ctx, int(bool(enable))))
 

@@ -92,6 +92,8 @@ SIGNATURES = {
     "ls_svd_solve": [P, C.c_int, DBL_P, DBL_P, C.c_double, DBL_P],
     "ls_dense_step": [P, DBL_P, P, DBL_P, C.POINTER(DenseRecord)],
     # row bands
+    "ls_launch_count": [P, C.POINTER(I64)],
+    "ls_add_launches": [P, I64],
     "ls_band_set": [P, C.c_int, C.c_int, C.c_int, C.c_int],
     "ls_band_clear": [P],
     "ls_band_buffers": [P, C.POINTER(C.c_void_p)],
@@ -104,6 +106,13 @@ SIGNATURES = {
     "ls_band_trial": [P, DBL_P, P, C.c_double, P],
     "ls_band_finalize": [P, C.c_int, P, C.c_int, C.c_int, C.c_double],
     "ls_band_read": [P, DBL_P],
+    "ls_band_frame_begin": [P],
+    "ls_band_trial_dev": [P, DBL_P, P, C.c_double, P, C.c_int],
+    "ls_band_finalize_dev": [P, C.c_int, P, C.c_int, C.c_int, C.c_double, C.c_int],
+    "ls_band_step_end": [P, P, P, C.c_int],
+    "ls_band_outer_end": [P, C.c_double],
+    "ls_band_frame_end": [P, C.c_int, C.POINTER(GNRecord), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                          C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "ls_band_dense_accum": [P, DBL_P, P, C.c_int],
     "ls_band_dense_nsums": [P],
     "ls_band_dense_solve": [P, DBL_P, P, C.c_int, C.c_int, DBL_P],

@@ -222,6 +222,7 @@ class _Band:
                   _view(ptrs[3], (U, Hl, W), torch.float32, device)]
         self.x = _view(ptrs[4], (U, Hl, W), torch.float32, device)
         self.zlist = torch.zeros(L.ZERO_LIST, dtype=torch.int64, device=device)
+        self.ring = None        # state buffers of the device-resident flip-flop
         self.summary = torch.zeros(3, dtype=torch.int32, device=device)
 
     def chk(self, rc):
@@ -264,7 +265,7 @@ class BandedSolver:
         self.bands = [_Band(self.specs[i], device, H, W, K) for i in exchange.local]
         self.installed = None
         self.cfg = None
-        self.launch_log = 0
+        self._graph, self._graph_key, self._graph_steps = None, None, 0
 
     # -- plumbing ---------------------------------------------------------------
     def configure(self, weights, config):
@@ -490,8 +491,9 @@ class BandedSolver:
         return cols.reshape(K, 3), applied.reshape(K, 3), rec
 
     # -- streaming flip-flop (solver.py:311-338, refine = False) ----------------
-    def flip_flop_stream(self, colors, X0, outer: int, gn_steps: int, tol_rel: float):
-        """Same contract as DeviceSolver.flip_flop_stream, host-driven."""
+    def flip_flop_stream_host(self, colors, X0, outer: int, gn_steps: int, tol_rel: float):
+        """Host-driven reference loop (one host decision per line-search
+        trial); the device-resident flip_flop_stream must match it."""
         a, pa = L.dbl_array(colors)
         self._enter()
         Xs = self._local(X0)
@@ -526,6 +528,122 @@ class BandedSolver:
             out.copy_(X0)
         self._store(Xs, out)
         return L.LS_OK, recs, status, out, -1
+
+    @staticmethod
+    def _launches(b) -> int:
+        n = C.c_int64()
+        b.chk(b.lib.ls_launch_count(b.ctx, C.byref(n)))
+        return int(n.value)
+
+    def _gfd(self, phase: int, nv: int, it: int = 0, alpha: float = 0.0, last: int = 0):
+        """gather + device-side finalisation (ls_band_finalize_dev)."""
+        gs = self.exchange.gather([b.bsum[:nv].clone() for b in self.bands])
+        for b, g in zip(self.bands, gs):
+            b.chk(b.lib.ls_band_finalize_dev(b.ctx, phase, L.dptr(g), len(self.specs), it, float(alpha), last))
+        self._keep = gs
+
+    def _enqueue_frame(self, pa, outer: int, gn_steps: int, tol_rel: float) -> int:
+        """The whole device-resident frame (no host decision): enqueue only."""
+        bands, ex = self.bands, self.exchange
+        iters, mh = self.cfg.pcg_iterations, self.cfg.max_halvings
+        self._enter()
+        for b in bands:
+            b.chk(b.lib.ls_band_frame_begin(b.ctx))
+        k = 0
+        for _ in range(outer):
+            for _ in range(gn_steps):
+                in_id, out_id = (0 if k == 0 else 1 + ((k - 1) & 1)), 1 + (k & 1)
+                Xs = [b.ring[in_id] for b in bands]
+                Xo = [b.ring[out_id] for b in bands]
+                for b, Xb in zip(bands, Xs):
+                    b.chk(b.lib.ls_band_eg(b.ctx, pa, L.dptr(Xb)))
+                self._gfd(L.BAND_EG, L.NUM_TERMS + 2)
+                ex.halo([b.z for b in bands])
+                for it in range(iters):
+                    for b, Xb in zip(bands, Xs):
+                        b.chk(b.lib.ls_band_pcg_apply(b.ctx, pa, L.dptr(Xb), it))
+                    self._gfd(L.BAND_APPLY, 1, it)
+                    ex.halo([b.p[it & 1] for b in bands])
+                    for b in bands:
+                        b.chk(b.lib.ls_band_pcg_update(b.ctx, it))
+                    self._gfd(L.BAND_UPDATE, 2, it)
+                    ex.halo([b.z for b in bands])
+                for b in bands:
+                    b.chk(b.lib.ls_band_pcg_finish(b.ctx))
+                ex.halo([b.x for b in bands])
+                alpha = 1.0
+                for h in range(mh + 1):    # speculative trials, decided on the device
+                    last = int(h == mh)
+                    for b, Xb, Xob in zip(bands, Xs, Xo):
+                        b.chk(b.lib.ls_band_trial_dev(b.ctx, pa, L.dptr(Xb), alpha, L.dptr(Xob), last))
+                    self._gfd(L.BAND_TRIAL, L.NUM_TERMS, 0, alpha, last)
+                    alpha *= 0.5
+                for b, Xb, Xob in zip(bands, Xs, Xo):
+                    b.chk(b.lib.ls_band_step_end(b.ctx, L.dptr(Xb), L.dptr(Xob), out_id))
+                ex.halo(Xo)
+                k += 1
+            for b in bands:
+                b.chk(b.lib.ls_band_outer_end(b.ctx, float(tol_rel)))
+        return k
+
+    def flip_flop_stream(self, colors, X0, outer: int, gn_steps: int, tol_rel: float, graph=None):
+        """Device-resident streaming flip-flop over the bands, same contract
+        as DeviceSolver.flip_flop_stream.  With every band in this process
+        the frame is captured once as a CUDA graph (torch.cuda.graph) and
+        replayed while palette and configuration are unchanged."""
+        a, pa = L.dbl_array(colors)
+        if outer * gn_steps > 256:
+            raise ValueError("too many GN steps")
+        for b in self.bands:
+            if b.ring is None:
+                b.ring = [torch.empty((self.U, b.spec.height, self.W), dtype=torch.float32, device=self.device)
+                          for _ in range(3)]
+        for b, Xb in zip(self.bands, self._local(X0)):
+            b.ring[0].copy_(Xb)
+        if graph is None:
+            import os
+            graph = (self.whole and not os.environ.get("LS_NO_GRAPH")
+                     and not any(b.solver.prof_on for b in self.bands))
+        key = (np.asarray(colors, dtype=np.float64).tobytes(), outer, gn_steps, float(tol_rel),
+               self.cfg.pcg_iterations, self.cfg.max_halvings)
+        if graph:
+            if self._graph is None or self._graph_key != key:
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(device=self.device)
+                side.wait_stream(torch.cuda.current_stream(self.device))
+                before = [self._launches(b) for b in self.bands]
+                with torch.cuda.stream(side):
+                    with torch.cuda.graph(g, stream=side):
+                        nsteps = self._enqueue_frame(pa, outer, gn_steps, tol_rel)
+                torch.cuda.current_stream(self.device).wait_stream(side)
+                self._graph_launches = [self._launches(b) - n0 for b, n0 in zip(self.bands, before)]
+                for b, n in zip(self.bands, self._graph_launches):   # capture ran nothing
+                    b.chk(b.lib.ls_add_launches(b.ctx, -n))
+                self._graph, self._graph_key, self._graph_steps = g, key, nsteps
+                self._enter()
+            self._graph.replay()
+            for b, n in zip(self.bands, self._graph_launches):
+                b.chk(b.lib.ls_add_launches(b.ctx, n))
+            nsteps = self._graph_steps
+        else:
+            nsteps = self._enqueue_frame(pa, outer, gn_steps, tol_rel)
+        self._enter()
+        results = []
+        for b in self.bands:
+            n = max(1, nsteps)
+            recs = (L.GNRecord * n)()
+            nrec, status, final, fault = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+            rc = b.lib.ls_band_frame_end(b.ctx, nsteps, recs, C.byref(nrec), C.byref(status), C.byref(final),
+                                         C.byref(fault))
+            if rc not in (L.LS_OK, L.LS_ERR_NONFINITE):
+                b.chk(rc)
+            results.append((rc, [recs[i] for i in range(nrec.value)], status.value, final.value, fault.value))
+        rc, recs, status, final, fault = results[0]
+        out = torch.empty_like(X0)
+        if self.whole:
+            out.copy_(X0)
+        self._store([b.ring[final] for b in self.bands], out)
+        return rc, recs, status, out, fault
 
 
 _cache: dict = {}

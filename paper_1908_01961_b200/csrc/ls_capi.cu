@@ -146,6 +146,7 @@ struct ls_ctx {
   double* bsum = nullptr;        // 512 doubles
   long long* zlist = nullptr;    // kZeroList
   int* seg_sum = nullptr;        // 4 ints
+  bool band_dev = false;         // inside ls_band_frame_begin / _end: device-side decisions
   float* ring[3] = {nullptr, nullptr, nullptr};   // state buffers of the graph flip-flop
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -374,6 +375,20 @@ int ls_profile(ls_ctx* c, int enable) {
   for (int i = 0; i < PC_N; ++i) { c->prof.ms[i] = 0.0; c->prof.cnt[i] = 0; }
   c->prof.on = enable != 0;
   c->launches = 0;
+  return LS_OK;
+}
+
+// launch bookkeeping for work replayed outside the context (a caller-side
+// CUDA graph of ls_band_* calls): read the counter / add replayed launches
+int ls_launch_count(ls_ctx* c, int64_t* n) {
+  LS_ARG(c && n, "bad arguments");
+  *n = c->launches;
+  return LS_OK;
+}
+
+int ls_add_launches(ls_ctx* c, int64_t n) {
+  LS_ARG(c && c->launches + n >= 0, "bad arguments");
+  c->launches += n;
   return LS_OK;
 }
 
@@ -1278,7 +1293,7 @@ int ls_band_eg(ls_ctx* c, const double* colors, const float* X) {
   const bool etma = energy_maps(c, X, nullptr, &em);
   const size_t pi = prof_begin(c);
   launch_energy(0, L_energy(c), f, cd, X, nullptr, 0.f, nullptr, nullptr, c->r, c->d, c->u, nullptr, nullptr,
-                c->part, c->tickets + 0, c->sc, etma ? &em : nullptr);
+                c->part, c->tickets + 0, c->sc, etma ? &em : nullptr, c->band_dev ? c->ctl : nullptr);
   prof_end(c, PC_EG, pi);
   c->launches += 1;
   LS_CK(cudaGetLastError());
@@ -1356,6 +1371,79 @@ int ls_band_finalize(ls_ctx* c, int phase, const double* gathered, int nbands, i
   c->launches += 1;
   LS_CK(cudaGetLastError());
   return LS_OK;
+}
+
+// ---- device-resident band flip-flop (the band form of ls_flip_flop_stream):
+// every decision (line search, step bookkeeping, convergence) on the device,
+// identical on every band, so the whole frame can be one CUDA graph (NCCL
+// collectives and P2P copies included).
+int ls_band_frame_begin(ls_ctx* c) {
+  int rc = band_ready(c);
+  if (rc) return rc;
+  launch_frame_init(c->stream, c->ctl);
+  c->band_dev = true;
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_trial_dev(ls_ctx* c, const double* colors, const float* X, double alpha, float* X_out, int last) {
+  int rc = band_ready(c);
+  if (rc) return rc;
+  LS_ARG(X && X_out && c->band_dev, "bad arguments (ls_band_frame_begin first)");
+  const Frame f = frame_of(c);
+  const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
+  EnergyMaps em;
+  const bool etma = energy_maps(c, X, c->x, &em);
+  const size_t pi = prof_begin(c);
+  launch_energy(1, L_energy(c), f, cd, X, c->x, (float)alpha, nullptr, X_out, nullptr, nullptr, nullptr, nullptr,
+                nullptr, c->part, c->tickets + 0, c->sc, etma ? &em : nullptr, c->ctl, 1, last);
+  prof_end(c, PC_TRIAL, pi);
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_finalize_dev(ls_ctx* c, int phase, const double* gathered, int nbands, int iter, double alpha,
+                         int last) {
+  LS_ARG(c && c->band_partial && c->band_dev && gathered && nbands >= 1, "bad arguments");
+  LS_ARG(phase >= BAND_EG && phase <= BAND_TRIAL, "bad band phase");
+  const int nv = phase == BAND_EG ? kTerms + 2 : phase == BAND_APPLY ? 1 : phase == BAND_UPDATE ? 2 : kTerms;
+  launch_band_finalize(c->stream, phase, gathered, nbands, nv, c->sc, iter, (float)alpha, 1, last, c->ctl);
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_step_end(ls_ctx* c, const float* X_in, float* X_out, int out_id) {
+  LS_ARG(c && c->band_dev && X_in && X_out, "bad arguments");
+  launch_step_end(c->stream, c->grid_update, c->ctl, c->sc, X_in, X_out, (int64_t)c->U * c->N, out_id, c->recs);
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_outer_end(ls_ctx* c, double tol_rel) {
+  LS_ARG(c && c->band_dev, "bad arguments");
+  launch_outer_end(c->stream, c->ctl, tol_rel);
+  c->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+int ls_band_frame_end(ls_ctx* c, int nsteps, ls_gn_record* out, int* n_records, int* status, int* final_buffer,
+                      int* fault_step) {
+  LS_ARG(c && c->band_partial && out && n_records && status && final_buffer && fault_step, "bad arguments");
+  LS_ARG(nsteps >= 0 && nsteps <= kMaxStepRecords, "bad step count");   // (band_dev is host state of
+  // the enqueue; a CUDA-graph replay runs without it)
+  c->band_dev = false;
+  LS_CK(cudaMemcpyAsync(c->ctl_host, c->ctl, sizeof(FrameCtl), cudaMemcpyDeviceToHost, c->stream));
+  if (nsteps > 0)
+    LS_CK(cudaMemcpyAsync(c->recs_host, c->recs, sizeof(StepRecord) * nsteps, cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaMemcpyAsync(c->host_buf, &c->sstate->error, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  LS_CK(cudaStreamSynchronize(c->stream));
+  prof_harvest(c);
+  return finish_flip_flop(c, out, n_records, status, final_buffer, fault_step);
 }
 
 int ls_band_read(ls_ctx* c, double* out) {

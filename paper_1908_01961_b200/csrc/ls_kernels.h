@@ -59,7 +59,7 @@ void launch_pcg_xfinal(const Launch& L, int64_t M, float* xv, const float* p0, c
 enum BandPhase { BAND_EG = 0, BAND_APPLY = 1, BAND_UPDATE = 2, BAND_TRIAL = 3, BAND_DENSE = 4 };
 void launch_band_sum(cudaStream_t s, const double* gathered, int nbands, int nv, double* out);
 void launch_band_finalize(cudaStream_t s, int phase, const double* gathered, int nbands, int nv, Scalars* sc,
-                          int iter, float alpha, int dev_ls, int last_trial);
+                          int iter, float alpha, int dev_ls, int last_trial, const FrameCtl* ctl = nullptr);
 int pcg_apply_grid_limit(int NT);
 int energy_grid_limit(int NT);
 void prepare_kernels(int NT);

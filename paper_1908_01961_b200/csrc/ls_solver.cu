@@ -1346,8 +1346,12 @@ void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, con
 // band-ordered sum of the gathered partials [nbands][nv], then the same
 // finalisation the single-frame kernels run in their last CTA
 __global__ void k_band_finalize(int phase, const double* __restrict__ g, int nbands, int nv, Scalars* sc, int iter,
-                                float alpha, int dev_ls, int last_trial) {
+                                float alpha, int dev_ls, int last_trial, const FrameCtl* ctl) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  // device-resident flip-flop: the kernels of a finished frame / decided
+  // line search exited without writing partials
+  if (ctl && ctl->done) return;
+  if (phase == BAND_TRIAL && dev_ls && sc->ls_done) return;
   double tot[kTerms + 2];
   for (int j = 0; j < nv && j < kTerms + 2; ++j) {
     double s = 0.0;
@@ -1364,8 +1368,8 @@ __global__ void k_band_finalize(int phase, const double* __restrict__ g, int nba
 }
 
 void launch_band_finalize(cudaStream_t s, int phase, const double* gathered, int nbands, int nv, Scalars* sc,
-                          int iter, float alpha, int dev_ls, int last_trial) {
-  k_band_finalize<<<1, 32, 0, s>>>(phase, gathered, nbands, nv, sc, iter, alpha, dev_ls, last_trial);
+                          int iter, float alpha, int dev_ls, int last_trial, const FrameCtl* ctl) {
+  k_band_finalize<<<1, 32, 0, s>>>(phase, gathered, nbands, nv, sc, iter, alpha, dev_ls, last_trial, ctl);
 }
 
 int pcg_apply_grid_limit(int NT) {
