@@ -233,3 +233,21 @@ def test_graph_flip_flop_equals_eager_and_replays():
     for (ra, sa, Xa), (rb, sb, Xb) in zip(*runs):
         assert ra == rb and sa == sb
         assert torch.equal(Xa, Xb)
+
+
+def test_graph_recaptures_when_the_palette_changes():
+    """The captured flip-flop bakes the palette into its kernels: a new
+    palette must re-capture (results equal the eager path for A, B, A)."""
+    import numpy as np
+    from paper_1908_01961_b200 import _device
+    clip = _clip(64, 96, 3, n=2, seed=13)
+    st = _state(clip, idx=1)
+    from paper_1908_01961_b200.solver import _solver_for
+    s = _solver_for(st)
+    A = st.palette.colors
+    B = np.clip(A * 0.9 + 0.05, 0.0, 1.0)
+    for cols in (A, B, A):
+        rg = s.flip_flop_stream(cols, st.layers.X, 1, 2, 0.0, graph=True)
+        re = s.flip_flop_stream(cols, st.layers.X, 1, 2, 0.0, graph=False)
+        assert torch.equal(rg[3], re[3])
+        assert [r.energy_after for r in rg[1]] == [r.energy_after for r in re[1]]
