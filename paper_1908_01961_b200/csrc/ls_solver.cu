@@ -71,14 +71,14 @@ __device__ __forceinline__ float rsqrtf_fast(float v) {
 __device__ __forceinline__ float nonneg_wf(float t, float eps) { return t > 0.f ? 0.f : rcpf(fabsf(t) + eps); }
 
 // smoothness / i-sparsity IRLS factor (p = 1): 1/|g| above eps, else 1/eps
+// (min(1/|g|, 1/eps) as one MUFU reciprocal of max(|g|, eps))
 __device__ __forceinline__ float irls1f(float g, const Coef<float>& c) {
-  g = fabsf(g);
-  return g >= c.eps_irls ? rcpf(g) : c.inv_eps;
+  return rcpf(fmaxf(fabsf(g), c.eps_irls));
 }
 
 // r-sparsity IRLS factor from the squared gradient magnitude s = |grad r|^2
 __device__ __forceinline__ float irls_sq(float s, const Coef<float>& c) {
-  if (c.p == 1.f) return s >= c.eps_irls * c.eps_irls ? rsqrtf_fast(s) : c.inv_eps;
+  if (c.p == 1.f) return rsqrtf_fast(fmaxf(s, c.eps_irls * c.eps_irls));
   if (c.p >= 2.f) return 1.f;
   const float mag = sqrtf(s);
   if (!(mag >= c.floor_rs)) return c.inv_eps;
@@ -742,12 +742,16 @@ __device__ __forceinline__ float apply_pixel(const Frame& f, const Coef<float>& 
     // the accumulation order is the CSR order either way
     if (LS_ABLATE == 1) {
     } else if (f.ent_w == nullptr) {
+      // unit weights: sum_e (u - u_partner) = deg * u - sum of the spatial
+      // partners (a temporal partner is the constant previous frame)
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f;
       auto one = [&](uint16_t ent) {
-        const int o = ent_soff(ent);
-        const bool tmp = ent & kEntTemporal;
-        a0 += ur[0] - (tmp ? 0.f : R0p[o]);
-        a1 += ur[1] - (tmp ? 0.f : R0p[kRP + o]);
-        a2 += ur[2] - (tmp ? 0.f : R0p[2 * kRP + o]);
+        if (!(ent & kEntTemporal)) {
+          const int o = ent_soff(ent);
+          s0 += R0p[o];
+          s1 += R0p[kRP + o];
+          s2 += R0p[2 * kRP + o];
+        }
       };
       int e = e0;
       for (; e + 4 <= e1; e += 4) {
@@ -756,7 +760,10 @@ __device__ __forceinline__ float apply_pixel(const Frame& f, const Coef<float>& 
         one(q0); one(q1); one(q2); one(q3);
       }
       for (; e < e1; ++e) one(__ldg(f.ent + e));
-      a0 *= c.lam_rc; a1 *= c.lam_rc; a2 *= c.lam_rc;
+      const float deg = (float)(e1 - e0);
+      a0 = c.lam_rc * fmaf(deg, ur[0], -s0);
+      a1 = c.lam_rc * fmaf(deg, ur[1], -s1);
+      a2 = c.lam_rc * fmaf(deg, ur[2], -s2);
     } else {
       auto one = [&](uint16_t ent, float wgt) {
         const float we = c.lam_rc * wgt;
