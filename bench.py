@@ -438,9 +438,28 @@ def run_ours(args):
         if world > 1:
             torch.distributed.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        main = torch.cuda.current_stream()
+        up = torch.cuda.Stream(device=dev)
+
+        def upload(j):   # frame j's host -> device copy on the upload stream
+            with torch.cuda.stream(up):
+                t = host[j].to(dev, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(up)
+            return t, ev
+
         e0.record()
+        up.wait_stream(main)
+        nxt = upload(0)
         for i in range(steps):
-            fdev = host[i].to(dev, non_blocking=True)
+            fdev, ev = nxt
+            main.wait_event(ev)
+            fdev.record_stream(main)
+            if i + 1 < steps and not os.environ.get("LS_E2E_SERIAL"):
+                nxt = upload(i + 1)          # the next frame's upload overlaps this solve
+            elif i + 1 < steps:
+                nxt = (host[i + 1].to(dev, non_blocking=True), torch.cuda.Event())
+                nxt[1].record(main)
             s2 = dec.step(fdev)
             done = torch.cuda.Event()
             done.record()
@@ -460,7 +479,7 @@ def run_ours(args):
                "h2d_bytes_per_step": int(host[0].numel() * 4),
                "d2h_bytes_per_step": int(out_host[0].numel() * 4),
                "api": "pipeline.StreamingDecomposer.step (reference decompose_frames loop); "
-                      "frame i's D2H on a copy stream beside frame i+1's solve"}
+                      "frame i+1's H2D and frame i's D2H on copy streams beside frame i's / i+1's solve"}
 
     # --- CPU baseline (rank 0, N = 1 only) ---
     cpu = None

@@ -119,6 +119,12 @@ LS_API int ls_set_image(ls_ctx* ctx, const float* image_hwc);
 LS_API int ls_sample_consistency(ls_ctx* ctx, const double* chroma_planes, const double* prev_chroma_planes,
                           uint64_t state_hi, uint64_t state_lo,
                           uint64_t inc_hi, uint64_t inc_lo, int64_t* n_pairs_out);
+/* Device-to-device copy on the SMs (stream-ordered; unlike a D2D
+ * cudaMemcpyAsync it never waits for a copy engine busy with host I/O). */
+LS_API int ls_device_copy(void* dst, const void* src, int64_t bytes, void* stream);
+/* Frame validity (imaging.py:36-57): *all_finite = no NaN / inf in x[0..n).
+ * Synchronises `stream`; the flag comes back through mapped host memory. */
+LS_API int ls_all_finite(const float* x, int64_t n, void* stream, int* all_finite);
 /* Counts of the installed partner rows (synchronises the stream): pairs,
  * temporal pairs, adjacency entries.  ls_sample_consistency itself does not
  * synchronise and reports n_pairs_out = -1. */

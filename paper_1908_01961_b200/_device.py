@@ -306,6 +306,32 @@ class DeviceSolver:
         return cols, applied, rec
 
 
+def device_copy(dst: torch.Tensor, src: torch.Tensor) -> torch.Tensor:
+    """dst <- src (same-size contiguous CUDA tensors) with an SM copy kernel on
+    the current stream: a D2D cudaMemcpyAsync (torch's clone / copy_) runs on
+    a copy engine and would queue behind a large host transfer."""
+    if dst.numel() != src.numel() or dst.dtype != src.dtype or not (dst.is_contiguous() and src.is_contiguous()):
+        raise ValueError("device_copy needs same-size contiguous tensors of one dtype")
+    lib = L.load()
+    st = torch.cuda.current_stream(src.device).cuda_stream
+    rc = lib.ls_device_copy(L.dptr(dst), L.dptr(src), C.c_int64(src.numel() * src.element_size()), C.c_void_p(st))
+    if rc != L.LS_OK:
+        raise L.NativeError(L.last_error())
+    return dst
+
+
+def all_finite(t: torch.Tensor) -> bool:
+    """No NaN / inf in a contiguous float32 CUDA tensor (synchronises the
+    current stream; no copy-engine read-back)."""
+    lib = L.load()
+    flag = C.c_int(0)
+    st = torch.cuda.current_stream(t.device).cuda_stream
+    rc = lib.ls_all_finite(L.dptr(t), C.c_int64(t.numel()), C.c_void_p(st), C.byref(flag))
+    if rc != L.LS_OK:
+        raise L.NativeError(L.last_error())
+    return bool(flag.value)
+
+
 def chromaticity_planes(image_hwc: torch.Tensor) -> torch.Tensor:
     """(2, H, W) fp64 chroma planes of a CUDA (H, W, 3) float32 image."""
     lib = L.load()

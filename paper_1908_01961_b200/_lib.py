@@ -75,6 +75,8 @@ SIGNATURES = {
     "ls_set_anchor": [P, P, P],
     "ls_get_edge": [P, P],
     "ls_get_chroma": [P, P],
+    "ls_device_copy": [P, P, I64, P],
+    "ls_all_finite": [P, I64, P, C.POINTER(C.c_int)],
     "ls_chromaticity": [P, C.c_int, C.c_int, P, P],
     "ls_edge_from_chroma": [P, C.c_int, C.c_int, P, P],
     "ls_segment": [P, DBL_P, P],

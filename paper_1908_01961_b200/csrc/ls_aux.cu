@@ -626,6 +626,39 @@ void launch_initialize(cudaStream_t s, const float* img, const int32_t* ids, int
                        float* X) {
   k_initialize<<<grid_for(N), 256, 0, s>>>(img, ids, N, NT, colors, X);
 }
+// device-to-device copy on the SMs: a cudaMemcpyAsync D2D would go to a copy
+// engine and queue behind a large host transfer on another stream
+__global__ void k_copy16(const int4* __restrict__ src, int4* __restrict__ dst, int64_t n16) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void k_copy1(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+void launch_copy(cudaStream_t s, void* dst, const void* src, int64_t bytes) {
+  if (bytes <= 0 || dst == src) return;
+  const int64_t n16 = (((uintptr_t)dst | (uintptr_t)src) & 15) ? 0 : bytes / 16;
+  if (n16) k_copy16<<<grid_for(n16), 256, 0, s>>>(static_cast<const int4*>(src), static_cast<int4*>(dst), n16);
+  const int64_t done = n16 * 16;
+  if (done < bytes)
+    k_copy1<<<grid_for(bytes - done), 256, 0, s>>>(static_cast<const unsigned char*>(src) + done,
+                                                     static_cast<unsigned char*>(dst) + done, bytes - done);
+}
+
+// flag = 0 if any value is NaN / inf (flag preset to 1 by the caller)
+__global__ void k_all_finite(const float* __restrict__ x, int64_t n, int* flag) {
+  bool ok = true;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    ok = ok && isfinite(x[i]);
+  if (!__syncthreads_and(ok) && threadIdx.x == 0) *flag = 0;
+}
+__global__ void k_set_flag(int* flag) { *flag = 1; }
+void launch_all_finite(cudaStream_t s, const float* x, int64_t n, int* flag) {
+  k_set_flag<<<1, 1, 0, s>>>(flag);
+  if (n > 0) k_all_finite<<<grid_for(n), 256, 0, s>>>(x, n, flag);
+}
+
 void launch_set_i32(cudaStream_t s, int32_t* p, int n, int32_t v) {
   k_set_i32<<<grid_for(n), 256, 0, s>>>(p, n, v);
 }

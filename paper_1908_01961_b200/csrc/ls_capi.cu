@@ -343,9 +343,9 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   A_(cudaMallocHost((void**)&c->sc_host, sizeof(Scalars)));
   A_(dalloc(c, &c->ctl, 1));
   A_(dalloc(c, &c->recs, kMaxStepRecords));
-  A_(cudaMallocHost((void**)&c->recs_host, sizeof(StepRecord) * kMaxStepRecords));
-  A_(cudaMallocHost((void**)&c->ctl_host, sizeof(FrameCtl)));
-  A_(cudaMallocHost((void**)&c->host_buf, sizeof(double) * (2 * 36 * 36 + 64)));
+  A_(cudaHostAlloc((void**)&c->recs_host, sizeof(StepRecord) * kMaxStepRecords, cudaHostAllocMapped));   // kernel-written (UVA)
+  A_(cudaHostAlloc((void**)&c->ctl_host, sizeof(FrameCtl), cudaHostAllocMapped));   // kernel-written (UVA)
+  A_(cudaHostAlloc((void**)&c->host_buf, sizeof(double) * (2 * 36 * 36 + 64), cudaHostAllocMapped));   // kernel-written (UVA)
   A_(cudaMemset(c->tickets, 0, 8 * sizeof(unsigned)));
   A_(cudaMemset(c->sc, 0, sizeof(Scalars)));
   // CUB scratch: max of the int exclusive-sum over N+1 and the max-scan over N
@@ -456,19 +456,19 @@ int ls_set_image(ls_ctx* c, const float* image_hwc) {
 
 int ls_set_edge(ls_ctx* c, const float* edge) {
   LS_ARG(c && edge, "bad arguments");
-  LS_CK(cudaMemcpyAsync(c->edge, edge, sizeof(float) * c->N, cudaMemcpyDeviceToDevice, c->stream));
+  launch_copy(c->stream, c->edge, edge, sizeof(float) * c->N); LS_CK(cudaGetLastError());
   return LS_OK;
 }
 
 int ls_get_edge(ls_ctx* c, float* out) {
   LS_ARG(c && out, "bad arguments");
-  LS_CK(cudaMemcpyAsync(out, c->edge, sizeof(float) * c->N, cudaMemcpyDeviceToDevice, c->stream));
+  launch_copy(c->stream, out, c->edge, sizeof(float) * c->N); LS_CK(cudaGetLastError());
   return LS_OK;
 }
 
 int ls_get_chroma(ls_ctx* c, double* out) {
   LS_ARG(c && out, "bad arguments");
-  LS_CK(cudaMemcpyAsync(out, c->chroma, sizeof(double) * 2 * c->N, cudaMemcpyDeviceToDevice, c->stream));
+  launch_copy(c->stream, out, c->chroma, sizeof(double) * 2 * c->N); LS_CK(cudaGetLastError());
   return LS_OK;
 }
 
@@ -478,7 +478,7 @@ int ls_set_prev_r(ls_ctx* c, const float* prev) {
     c->has_prev_r = false;
     return LS_OK;
   }
-  LS_CK(cudaMemcpyAsync(c->prev_r, prev, sizeof(float) * 3 * c->N, cudaMemcpyDeviceToDevice, c->stream));
+  launch_copy(c->stream, c->prev_r, prev, sizeof(float) * 3 * c->N); LS_CK(cudaGetLastError());
   c->has_prev_r = true;
   return LS_OK;
 }
@@ -487,11 +487,11 @@ int ls_set_anchor(ls_ctx* c, const int32_t* ids, const float* anchor) {
   LS_ARG(c, "null context");
   LS_ARG((ids != nullptr) != (anchor != nullptr), "exactly one of cluster_ids / r_cluster_log");
   if (ids) {
-    LS_CK(cudaMemcpyAsync(c->ids, ids, sizeof(int32_t) * c->N, cudaMemcpyDeviceToDevice, c->stream));
+    launch_copy(c->stream, c->ids, ids, sizeof(int32_t) * c->N); LS_CK(cudaGetLastError());
     c->has_ids = true;
     c->has_anchor = false;
   } else {
-    LS_CK(cudaMemcpyAsync(c->anchor, anchor, sizeof(float) * 3 * c->N, cudaMemcpyDeviceToDevice, c->stream));
+    launch_copy(c->stream, c->anchor, anchor, sizeof(float) * 3 * c->N); LS_CK(cudaGetLastError());
     c->has_anchor = true;
     c->has_ids = false;
   }
@@ -509,6 +509,27 @@ static int build_rows(ls_ctx* c, int64_t* total) {
   LS_CK(cudaMemcpyAsync(&tot, c->row_ptr + N, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   LS_CK(cudaStreamSynchronize(c->stream));
   *total = tot;
+  return LS_OK;
+}
+
+int ls_device_copy(void* dst, const void* src, int64_t bytes, void* stream) {
+  LS_ARG((dst && src) || bytes == 0, "bad arguments");
+  LS_ARG(bytes >= 0, "bad size");
+  launch_copy((cudaStream_t)stream, dst, src, bytes);
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+// imaging.py:36-57 frame check without a copy-engine read-back: the flag is
+// written by the kernel into mapped host memory (one per host thread)
+int ls_all_finite(const float* x, int64_t n, void* stream, int* all_finite) {
+  LS_ARG((x || n == 0) && all_finite && n >= 0, "bad arguments");
+  static thread_local int* flag = nullptr;
+  if (!flag) LS_CK(cudaHostAlloc((void**)&flag, sizeof(int), cudaHostAllocMapped));
+  launch_all_finite((cudaStream_t)stream, x, n, flag);
+  LS_CK(cudaGetLastError());
+  LS_CK(cudaStreamSynchronize((cudaStream_t)stream));
+  *all_finite = *(volatile int*)flag;
   return LS_OK;
 }
 
@@ -941,10 +962,12 @@ static int enqueue_flip_flop(ls_ctx* c, const double* colors, float* const bufs[
     c->launches += 1;
   }
   LS_CK(cudaGetLastError());
-  LS_CK(cudaMemcpyAsync(c->ctl_host, c->ctl, sizeof(FrameCtl), cudaMemcpyDeviceToHost, c->stream));
-  if (k > 0)
-    LS_CK(cudaMemcpyAsync(c->recs_host, c->recs, sizeof(StepRecord) * k, cudaMemcpyDeviceToHost, c->stream));
-  LS_CK(cudaMemcpyAsync(c->host_buf, &c->sstate->error, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  // records to mapped host memory by a kernel, not a copy engine (which may
+  // be busy with the caller's large host transfers on another stream)
+  launch_copy(c->stream, c->ctl_host, c->ctl, sizeof(FrameCtl));
+  if (k > 0) launch_copy(c->stream, c->recs_host, c->recs, sizeof(StepRecord) * k);
+  launch_copy(c->stream, c->host_buf, &c->sstate->error, sizeof(int));
+  LS_CK(cudaGetLastError());
   *nsteps = k;
   return LS_OK;
 }
@@ -1037,7 +1060,7 @@ extern "C" int ls_flip_flop_graph(ls_ctx* c, const double* colors, const float* 
   key.tol_rel = tol_rel;
   key.stream = c->stream;
   const bool reuse = c->graph_exec && !c->prof.on && std::memcmp(&key, c->graph_key, sizeof(key)) == 0;
-  LS_CK(cudaMemcpyAsync(c->ring[0], X_in, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  launch_copy(c->stream, c->ring[0], X_in, bytes); LS_CK(cudaGetLastError());
   int k = 0;
   if (c->prof.on) {   // profiling records events around kernels: run eagerly
     rc = enqueue_flip_flop(c, colors, c->ring, outer, gn_steps, tol_rel, &k);
@@ -1092,7 +1115,7 @@ extern "C" int ls_flip_flop_graph(ls_ctx* c, const double* colors, const float* 
   prof_harvest(c);
   int final_buffer = 0;
   rc = finish_flip_flop(c, out, n_records, status, &final_buffer, fault_step);
-  LS_CK(cudaMemcpyAsync(X_out, c->ring[final_buffer], bytes, cudaMemcpyDeviceToDevice, c->stream));
+  launch_copy(c->stream, X_out, c->ring[final_buffer], bytes); LS_CK(cudaGetLastError());
   return rc;
 }
 
@@ -1437,10 +1460,10 @@ int ls_band_frame_end(ls_ctx* c, int nsteps, ls_gn_record* out, int* n_records, 
   LS_ARG(nsteps >= 0 && nsteps <= kMaxStepRecords, "bad step count");   // (band_dev is host state of
   // the enqueue; a CUDA-graph replay runs without it)
   c->band_dev = false;
-  LS_CK(cudaMemcpyAsync(c->ctl_host, c->ctl, sizeof(FrameCtl), cudaMemcpyDeviceToHost, c->stream));
-  if (nsteps > 0)
-    LS_CK(cudaMemcpyAsync(c->recs_host, c->recs, sizeof(StepRecord) * nsteps, cudaMemcpyDeviceToHost, c->stream));
-  LS_CK(cudaMemcpyAsync(c->host_buf, &c->sstate->error, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  launch_copy(c->stream, c->ctl_host, c->ctl, sizeof(FrameCtl));
+  if (nsteps > 0) launch_copy(c->stream, c->recs_host, c->recs, sizeof(StepRecord) * nsteps);
+  launch_copy(c->stream, c->host_buf, &c->sstate->error, sizeof(int));
+  LS_CK(cudaGetLastError());
   LS_CK(cudaStreamSynchronize(c->stream));
   prof_harvest(c);
   return finish_flip_flop(c, out, n_records, status, final_buffer, fault_step);

@@ -84,6 +84,8 @@ struct SampleState {
 };
 constexpr int kSamplePasses = 4;
 constexpr int kMaxStepRecords = 256;
+void launch_copy(cudaStream_t s, void* dst, const void* src, int64_t bytes);
+void launch_all_finite(cudaStream_t s, const float* x, int64_t n, int* flag);
 void launch_pack_hwc(cudaStream_t s, const float* hwc, int C, int N, float* planes);
 void launch_unpack_hwc(cudaStream_t s, const float* planes, int C, int N, float* hwc);
 void launch_image(cudaStream_t s, const float* hwc, int N, float* img_planes, double* chroma);

@@ -120,6 +120,8 @@ class LayerStack:
         return torch.einsum("khw,kc->hwc", self.X[3:], B)
 
     def copy(self) -> "LayerStack":
+        if self.X.is_cuda and self.X.is_contiguous():
+            return LayerStack(planes=_device.device_copy(torch.empty_like(self.X), self.X))
         return LayerStack(planes=self.X.clone())
 
 

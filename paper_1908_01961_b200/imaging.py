@@ -54,7 +54,7 @@ class Frame:
         if d.shape[0] < MIN_SIZE or d.shape[1] < MIN_SIZE:
             raise FrameError(f"frame too small: {d.shape[1]}x{d.shape[0]} (min {MIN_SIZE})")
         t = as_cuda(d)
-        if not bool(torch.isfinite(t).all()):
+        if not _device.all_finite(t):
             raise FrameError("frame contains non-finite values")
         object.__setattr__(self, "data", t)
 
