@@ -125,6 +125,18 @@ LS_API int ls_device_copy(void* dst, const void* src, int64_t bytes, void* strea
 /* Frame validity (imaging.py:36-57): *all_finite = no NaN / inf in x[0..n).
  * Synchronises `stream`; the flag comes back through mapped host memory. */
 LS_API int ls_all_finite(const float* x, int64_t n, void* stream, int* all_finite);
+/* Misclustering correction (correction.py:54-68): mask (H*W uint8) = the
+ * 4-connected pixels with ids == target reachable from seeds (uint8), by
+ * device dilation; scratch is H*W bytes.  Synchronises `stream`. */
+LS_API int ls_flood_fill(const int32_t* ids, int target, const uint8_t* seeds, int H, int W, uint8_t* mask,
+                         uint8_t* scratch, void* stream);
+/* Layer edits (editing.py:24-74): out (H, W, 3) = clip(R' * sum_k T_k B'_k, 0, 1)
+ * from the planar state X, the (K+1) x 3 host matrix B' (row 0 white), the
+ * reflectance of cluster k (ids == k, 0 = none) scaled by ratio[3] (host);
+ * pixels with matte != 0 copy bg (H, W, 3).  fp64 per pixel. */
+LS_API int ls_recompose(const float* X, int K, int H, int W, const double* B_host, int k,
+                        const double* ratio_host, const int32_t* ids, const uint8_t* matte, const float* bg,
+                        float* out_hwc, void* stream);
 /* Counts of the installed partner rows (synchronises the stream): pairs,
  * temporal pairs, adjacency entries.  ls_sample_consistency itself does not
  * synchronise and reports n_pairs_out = -1. */

@@ -76,6 +76,8 @@ SIGNATURES = {
     "ls_get_edge": [P, P],
     "ls_get_chroma": [P, P],
     "ls_device_copy": [P, P, I64, P],
+    "ls_flood_fill": [P, C.c_int, P, C.c_int, C.c_int, P, P, P],
+    "ls_recompose": [P, C.c_int, C.c_int, C.c_int, DBL_P, C.c_int, DBL_P, P, P, P, P, P],
     "ls_all_finite": [P, I64, P, C.POINTER(C.c_int)],
     "ls_chromaticity": [P, C.c_int, C.c_int, P, P],
     "ls_edge_from_chroma": [P, C.c_int, C.c_int, P, P],

@@ -533,6 +533,49 @@ int ls_all_finite(const float* x, int64_t n, void* stream, int* all_finite) {
   return LS_OK;
 }
 
+// correction.py:54-68: flood fill of `target` pixels from the seeds, on the
+// device; convergence read back through a mapped flag every 16 steps
+int ls_flood_fill(const int32_t* ids, int target, const uint8_t* seeds, int H, int W, uint8_t* mask,
+                  uint8_t* scratch, void* stream) {
+  LS_ARG(ids && seeds && mask && scratch && H >= 1 && W >= 1, "bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  static thread_local int* changed = nullptr;
+  if (!changed) LS_CK(cudaHostAlloc((void**)&changed, sizeof(int), cudaHostAllocMapped));
+  const int64_t N = (int64_t)H * W;
+  launch_flood_init(st, ids, target, seeds, N, mask);
+  uint8_t* buf[2] = {mask, scratch};
+  int cur = 0;
+  for (int64_t done = 0; done <= N; done += 16) {
+    launch_set_flag(st, changed, 0);
+    for (int j = 0; j < 16; ++j) {
+      launch_flood_step(st, ids, target, H, W, buf[cur], buf[cur ^ 1], changed);
+      cur ^= 1;
+    }
+    LS_CK(cudaGetLastError());
+    LS_CK(cudaStreamSynchronize(st));
+    if (!*(volatile int*)changed) break;
+  }
+  if (cur != 0) launch_copy(st, mask, buf[cur], N);
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+// editing.py:24-74: clip(R' * (T . B')), optional matte -> background
+int ls_recompose(const float* X, int K, int H, int W, const double* B, int k, const double* ratio,
+                 const int32_t* ids, const uint8_t* matte, const float* bg, float* out, void* stream) {
+  LS_ARG(X && B && out && H >= 1 && W >= 1 && K >= 0 && K <= LS_MAX_K, "bad arguments");
+  LS_ARG(!matte || bg, "a matte needs a background");
+  LS_ARG(k == 0 || (k >= 1 && k <= K && ids), "cluster id outside 1..K or no ids");
+  EditParams P;
+  std::memset(&P, 0, sizeof(P));
+  for (int i = 0; i < 3 * (K + 1); ++i) P.B[i] = B[i];
+  for (int c = 0; c < 3; ++c) P.ratio[c] = ratio ? ratio[c] : 1.0;
+  P.k = k;
+  launch_recompose((cudaStream_t)stream, X, K + 1, (int64_t)H * W, P, ids, matte, bg, out);
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
 int ls_chromaticity(const float* image_hwc, int H, int W, double* out, void* stream) {
   LS_ARG(image_hwc && out && H >= 1 && W >= 1, "bad arguments");
   // planar image copy is not needed: write it into the second half of a scratch-free path

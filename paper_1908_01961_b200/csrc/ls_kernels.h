@@ -85,6 +85,19 @@ struct SampleState {
 constexpr int kSamplePasses = 4;
 constexpr int kMaxStepRecords = 256;
 void launch_copy(cudaStream_t s, void* dst, const void* src, int64_t bytes);
+// correction / edits (ls_edit.cu)
+struct EditParams {
+  double B[3 * kMaxNT];   // palette matrix rows (white, b_1..b_K), possibly modified
+  double ratio[3];        // reflectance ratio applied to cluster k
+  int k;                  // cluster whose reflectance is rescaled (0: none)
+};
+void launch_flood_init(cudaStream_t s, const int32_t* ids, int target, const uint8_t* seeds, int64_t N,
+                       uint8_t* mask);
+void launch_flood_step(cudaStream_t s, const int32_t* ids, int target, int H, int W, const uint8_t* in,
+                       uint8_t* out, int* changed);
+void launch_set_flag(cudaStream_t s, int* f, int v);
+void launch_recompose(cudaStream_t s, const float* X, int NT, int64_t N, const EditParams& P, const int32_t* ids,
+                      const uint8_t* matte, const float* bg, float* out);
 void launch_all_finite(cudaStream_t s, const float* x, int64_t n, int* flag);
 void launch_pack_hwc(cudaStream_t s, const float* hwc, int C, int N, float* planes);
 void launch_unpack_hwc(cudaStream_t s, const float* planes, int C, int N, float* hwc);

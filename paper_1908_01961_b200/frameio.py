@@ -190,19 +190,21 @@ def run_pipeline(input_dir, output_dir, weights=None, config=None, seed: int = 0
     """pipeline.py:237-270 disk to disk: read numbered frames, decompose,
     write layer sets (while the next frames solve), palette, diagnostics and
     the manifest.  The energy-history figure (report.py, matplotlib) is not
-    produced; misclustering journals (clicks) are out of scope."""
+    produced."""
     from .energy import EnergyWeights
     from .palette import save_palette
     from .pipeline import decompose_frames
     from .solver import SolveConfig
-    if journal is not None:
-        raise NotImplementedError("misclustering correction (journal clicks) is outside lumisplit_b200's scope")
     weights = weights or EnergyWeights()
     config = config or SolveConfig()
     paths = find_frames(input_dir)
     if not paths:
         raise IOError(f"no frame_*.png or frame_*.pfm files in {input_dir}")
     frames = [load_frame(p) for p in paths]
+    clicks = None
+    if journal is not None:                 # pipeline.py:250-252
+        from .pipeline import journal_clicks, read_journal
+        clicks = journal_clicks(read_journal(journal))
     out = Path(output_dir)
     out.mkdir(parents=True, exist_ok=True)
     writer = AsyncFrameWriter(out)
@@ -211,7 +213,7 @@ def run_pipeline(input_dir, output_dir, weights=None, config=None, seed: int = 0
         writer.submit(idx + 1, state.layers, state.palette, state.cluster_map)
 
     try:
-        result = decompose_frames(frames, weights, config, seed=seed, k_max=k_max,
+        result = decompose_frames(frames, weights, config, seed=seed, k_max=k_max, clicks=clicks,
                                   streaming_outer=streaming_outer, on_frame=on_frame)
     finally:
         writer.close()

@@ -3,9 +3,10 @@
 `decompose_frames` keeps the reference signature and flow: frame 1 is
 clustered (or takes the palette / cluster map given), refined and solved;
 frames 2..N are re-segmented with the frozen palette and solved warm-started
-with temporal consistency pairs.  Interactive misclustering correction
-(`clicks`, correction.py) is outside this framework's scope (SURVEY.md
-section 2, row 7) and is rejected explicitly.
+with temporal consistency pairs.  First-frame clicks mark misclustered
+regions (correction.py): each is flood-filled, its base color chosen by K
+candidate solves, and the region is tracked and re-applied on every later
+frame (pipeline.py:66-84, 100-106, 140-149).
 """
 
 from __future__ import annotations
@@ -19,6 +20,7 @@ import torch
 from .energy import EnergyWeights, LayerStack
 from .imaging import Frame, as_cuda, chromaticity
 from .palette import BaseColorPalette, ClusterMap, estimate_palette, segment
+from .correction import apply_region_correction, correct_reflectance, identify_region, track_region
 from .refine import refine_palette
 from .solver import SolveConfig, SolverState, build_aux, flip_flop, initialize
 
@@ -57,8 +59,9 @@ class StreamingDecomposer:
     warm-started from the previous one."""
 
     def __init__(self, palette: BaseColorPalette, weights: EnergyWeights, config: SolveConfig,
-                 seed: int = 0, streaming_outer: int = 2, bands=0):
+                 seed: int = 0, streaming_outer: int = 2, bands=0, regions=None):
         self.bands = bands          # row bands (bands.py), 0 = whole frames
+        self.regions = list(regions or [])   # tracked misclustering corrections
         self.palette = palette
         self.weights = weights
         self.config = config
@@ -91,6 +94,17 @@ class StreamingDecomposer:
     def step(self, frame) -> SolverState:
         frame = _as_frame(frame, self.bands)
         cmap = segment(frame, self.palette)
+        if self.regions:            # pipeline.py:140-149: track and re-apply corrections
+            tracked = []
+            for region in self.regions:
+                nxt = track_region(region, cmap, frame_index=self.index)
+                if nxt is None:
+                    log.warning("frame %d: region from %s lost", self.index + 1, region.seed_xy)
+                    continue
+                tracked.append(nxt)
+            for region in tracked:
+                cmap = apply_region_correction(cmap, region, self.palette)
+            self.regions = tracked
         aux = build_aux(frame, cmap, seed=self.seed + self.index, prev_chroma=self.prev_chroma,
                         prev_r=self.prev_layers.r)
         layers = initialize(frame, cmap, self.palette, previous=self.prev_layers)
@@ -102,6 +116,40 @@ class StreamingDecomposer:
         self.prev_layers = state.layers
         self.prev_chroma = chromaticity(frame)
         return state
+
+
+def journal_clicks(entries: list) -> list:
+    """pipeline.py:60-63: first-frame click coordinates, in journal order."""
+    return [(int(e["x"]), int(e["y"])) for e in entries
+            if e.get("kind") == "click" and int(e.get("frame", 1)) == 1]
+
+
+def read_journal(path) -> list:
+    """pipeline.py:50-57: one JSON object per line."""
+    import json
+    with open(path) as fh:
+        return [json.loads(line) for line in fh if line.strip()]
+
+
+def _collect_regions(clicks, frame, cluster_map, palette, weights, config, seed):
+    """pipeline.py:66-84: identify clicked regions (same-cluster clicks merge)
+    and solve each region's corrected base color."""
+    regions = []
+    ids = cluster_map.ids
+    for xy in clicks:
+        sid = int(ids[int(xy[1]), int(xy[0])])
+        existing = next((r for r in regions if r.source_id == sid), None)
+        region = identify_region(xy, cluster_map, frame=frame, merge_into=existing)
+        if existing is not None:
+            regions[regions.index(existing)] = region
+        else:
+            regions.append(region)
+    for region in regions:
+        region.corrected_id = correct_reflectance(region, frame, cluster_map, palette, weights=weights,
+                                                  seed=seed)
+        log.info("region at %s (%d px): cluster %d -> %d", region.seed_xy, region.size,
+                 region.source_id, region.corrected_id)
+    return regions
 
 
 def decompose_frames(frames: list, weights: EnergyWeights, config: SolveConfig, seed: int = 0,
@@ -117,14 +165,20 @@ def decompose_frames(frames: list, weights: EnergyWeights, config: SolveConfig, 
     (streams results out without keeping them)."""
     if not frames:
         raise ValueError("no frames")
-    if clicks:
-        raise NotImplementedError("misclustering correction (clicks) is outside lumisplit_b200's scope")
     f0 = _as_frame(frames[0])
     if palette is None:
         palette, cluster_map = estimate_palette(f0, k_max=k_max, seed=seed)
-    result = PipelineResult(palette=palette, layer_stacks=[], cluster_maps=[], regions=[],
+    elif cluster_map is None:
+        cluster_map = segment(f0, palette)
+    regions = []
+    if clicks:                      # pipeline.py:100-106
+        regions = _collect_regions(clicks, f0, cluster_map, palette, weights, config, seed)
+    for region in regions:
+        cluster_map = apply_region_correction(cluster_map, region, palette)
+    result = PipelineResult(palette=palette, layer_stacks=[], cluster_maps=[], regions=regions,
                             records=[], statuses=[])
-    dec = StreamingDecomposer(palette, weights, config, seed=seed, streaming_outer=streaming_outer)
+    dec = StreamingDecomposer(palette, weights, config, seed=seed, streaming_outer=streaming_outer,
+                              regions=regions)
     for idx, f in enumerate(frames):
         t0 = time.perf_counter()
         state = dec.first(f0, cluster_map) if idx == 0 else dec.step(f)
