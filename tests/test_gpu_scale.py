@@ -251,3 +251,36 @@ def test_graph_recaptures_when_the_palette_changes():
         re = s.flip_flop_stream(cols, st.layers.X, 1, 2, 0.0, graph=False)
         assert torch.equal(rg[3], re[3])
         assert [r.energy_after for r in rg[1]] == [r.energy_after for r in re[1]]
+
+
+def test_cfg2_streaming_steps_teacher_forced_vs_oracle():
+    """configs[1] size (640x480, K=6) with temporal partners: two streaming GN
+    steps on the device against the oracle from the same input state and aux
+    (partners bit-exact), per-layer max-abs <= 1e-3, energies within 1e-5."""
+    from paper_1908_01961_b200.solver import gn_step_sparse
+    clip = _clip(480, 640, 6, n=2, seed=21)
+    st0 = _state(clip)                                  # frame 0 initial state
+    r_prev = st0.layers.r.double().cpu().numpy()
+    st = _state(clip, idx=1, prev=(st0.frame, st0.layers), seed=3)
+    img0 = clip.frames[0].double().numpy()
+    img1 = clip.frames[1].double().numpy()
+    ids1 = st.aux.cluster_ids.cpu().numpy()
+    oaux = O.build_aux(img1, ids1, 3, O.chromaticity(img0)[0], r_prev)
+    s = st.aux.samples
+    assert np.array_equal(s.src.cpu().numpy(), oaux.pairs.src)
+    assert np.array_equal(s.temporal.cpu().numpy(), oaux.pairs.temporal)
+    for _ in range(2):
+        r0 = st.layers.r.double().cpu().numpy()
+        T0 = st.layers.T.double().cpu().numpy()
+        ost = O.State(image=img1, colors=np.asarray(clip.colors, dtype=np.float64), r=r0, T=T0, aux=oaux,
+                      weights=O.Weights(), config=O.Config(tol_rel=0.0))
+        orec = O.gn_step_sparse(ost)
+        rec = gn_step_sparse(st)
+        assert rec["accepted"] == orec["accepted"]
+        assert np.isclose(rec["energy_before"], orec["energy_before"], rtol=1e-5)
+        assert np.isclose(rec["energy_after"], orec["energy_after"], rtol=1e-5)
+        dT = np.abs(st.layers.T.double().cpu().numpy() - ost.T).max()
+        dR = np.abs(np.exp(st.layers.r.double().cpu().numpy()) - np.exp(ost.r)).max()
+        assert dT <= 1e-3 and dR <= 1e-3, (dT, dR)
+        st.layers.X.copy_(torch.as_tensor(np.concatenate([ost.r.transpose(2, 0, 1), ost.T.transpose(2, 0, 1)]),
+                                          dtype=torch.float32, device="cuda"))      # teacher forcing
