@@ -284,3 +284,28 @@ def test_cfg2_streaming_steps_teacher_forced_vs_oracle():
         assert dT <= 1e-3 and dR <= 1e-3, (dT, dR)
         st.layers.X.copy_(torch.as_tensor(np.concatenate([ost.r.transpose(2, 0, 1), ost.T.transpose(2, 0, 1)]),
                                           dtype=torch.float32, device="cuda"))      # teacher forcing
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_streaming_fault_raises_with_dump(graph):
+    """A non-finite state in a streaming frame raises NumericalFaultError
+    with the reference's dump (solver.py:153-157) through the device-resident
+    flip-flop, graph or eager, and the next frame still solves."""
+    import os
+    from dataclasses import replace
+    from paper_1908_01961_b200.solver import NumericalFaultError, flip_flop
+    clip = _clip(48, 64, 3, n=2, seed=17)
+    os.environ["LS_NO_GRAPH"] = "" if graph else "1"
+    try:
+        st = _state(clip)
+        st.config = replace(st.config, refine=False, outer_iterations=2)
+        st.layers.X[1, 5, 7] = float("nan")
+        with pytest.raises(NumericalFaultError) as exc:
+            flip_flop(st)
+        assert exc.value.dump["iteration"] == 0 and set(exc.value.dump["terms"]) >= {"data", "smoothness"}
+        ok = _state(clip)
+        ok.config = replace(ok.config, refine=False, outer_iterations=2)
+        flip_flop(ok)
+        assert ok.records and all(np.isfinite(r["energy_after"]) for r in ok.records)
+    finally:
+        os.environ.pop("LS_NO_GRAPH", None)
