@@ -18,7 +18,7 @@ SRC = sorted((PKG / "csrc").glob("*.cu"))
 OUT = PKG / "liblumisplit_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *os.environ.get("LS_NVCC_DEFS", "").split(),
          "-Xcompiler", "-fvisibility=hidden", "-cudart", "static", "--expt-relaxed-constexpr"]
 
 

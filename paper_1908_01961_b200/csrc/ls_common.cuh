@@ -17,8 +17,13 @@ constexpr int kTerms = 8;
 constexpr int kHalf = 7;          // CONSISTENCY_WINDOW // 2 (energy.py:23)
 constexpr int kWin = 15;
 constexpr int kTileW = 32;        // one warp per tile row
-constexpr int kTileH = 8;         // 8 warps per block
+#ifndef LS_TILE_H
+#define LS_TILE_H 8
+#endif
+constexpr int kTileH = LS_TILE_H;   // warps per block (one per tile row)
 constexpr int kThreads = kTileW * kTileH;
+// resident CTAs per SM the stencil kernels are compiled for (80 registers)
+constexpr int kStencilMinBlocks = kTileH <= 8 ? 3 : 2;
 constexpr int kHaloW = kTileW + 2 * kHalf;
 constexpr int kHaloH = kTileH + 2 * kHalf;
 constexpr int kMaxBlocks = 4096;  // partial-sum slots per reduction

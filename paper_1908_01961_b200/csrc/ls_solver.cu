@@ -518,7 +518,7 @@ __device__ void fin_pcg_update(double rz, double rn, Scalars* sc, int iter) {
 }
 
 template <int NT, int MODE, bool TMA>
-__global__ void __launch_bounds__(kThreads, 3) k_energy(Frame f, Coef<float> c, const float* __restrict__ X,
+__global__ void __launch_bounds__(kThreads, kStencilMinBlocks) k_energy(Frame f, Coef<float> c, const float* __restrict__ X,
                                                      const float* __restrict__ dx, float alpha,
                                                      const float* __restrict__ Yext, float* __restrict__ Xout,
                                                      float* __restrict__ r_out, float* __restrict__ d_out,
@@ -900,7 +900,7 @@ __device__ __forceinline__ void tma_issue_pcg(float* stage, const PcgMaps& m, ui
 
 template <int NT, bool TMA>
 #ifndef LS_PCG_MINB
-#define LS_PCG_MINB 3
+#define LS_PCG_MINB kStencilMinBlocks
 #endif
 __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Coef<float> c, const float* __restrict__ X,
                                                            const float* __restrict__ z,
