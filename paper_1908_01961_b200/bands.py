@@ -479,7 +479,10 @@ class BandedSolver:
             et = _esum(self._energy_local(cand, Xs))
             if np.isfinite(et) and et <= e0:
                 applied = cand - cols
-                rec.delta_b_norm = float(np.sqrt(np.sum(applied * applied)))
+                nrm = 0.0                 # left-to-right, as ls_dense_step does
+                for v in applied.tolist():
+                    nrm += v * v
+                rec.delta_b_norm = float(np.sqrt(nrm))
                 cols = cand
                 e1, accepted = et, True
                 break
