@@ -333,7 +333,7 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
         g = fmaf(c.lam_sm, gs, g);
         d = fmaf(c.lam_sm, ds, d);
         const float bf = -g;
-        const float di = 1.f / (d > 0.f ? d : 1.f);   // Jacobi preconditioner (solver.py:87)
+        const float di = __frcp_rn(d > 0.f ? d : 1.f);   // Jacobi preconditioner (solver.py:87)
         const float zf = bf * di;
         const size_t o = (size_t)(3 + k) * N + i;
         if (r_out) { r_out[o] = bf; d_out[o] = di; u_out[o] = zf; }
@@ -433,7 +433,7 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
     g += gcons[ch];
     d += dcons;
     const float bf = -g;
-    const float di = 1.f / (d > 0.f ? d : 1.f);   // Jacobi preconditioner (solver.py:87)
+    const float di = __frcp_rn(d > 0.f ? d : 1.f);   // Jacobi preconditioner (solver.py:87)
     const float zf = bf * di;
     if (r_out) { r_out[ch * N + i] = bf; d_out[ch * N + i] = di; u_out[ch * N + i] = zf; }
     if (b_raw) { b_raw[ch * N + i] = bf; diag_raw[ch * N + i] = d; }
