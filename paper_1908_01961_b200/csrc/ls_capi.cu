@@ -5,8 +5,11 @@
 // adjacency is regrown only if a hand-made pair list outgrows it).  The
 // Gauss-Newton step is orchestrated here, natively: 1 fused energy/gradient
 // kernel, PCG iterations of (apply, update) with device-resident scalars,
-// and line-search trials; the host synchronises once per trial to read the
-// energies (the accept/reject branch of solver.py:169-178).
+// and line-search trials.  ls_gn_step decides accept / halve on the host (one
+// synchronisation per trial, solver.py:169-178); ls_flip_flop_stream /
+// ls_flip_flop_graph decide everything on the device and synchronise once per
+// frame, the latter as one CUDA-graph launch; the ls_band_* entry points are
+// the same phases for one band of rows (bands.py).
 #include <cub/device/device_scan.cuh>
 #include <cudaTypedefs.h>
 

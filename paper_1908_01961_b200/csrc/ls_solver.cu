@@ -20,8 +20,9 @@
 //   sR  the 3 r planes of the operand, + 7 halo   (r-sparsity stencil and the
 //                                                   15x15 consistency window,
 //                                                   energy.py:23, 161-173)
-// with coalesced row loads, so every HBM word is read once per tile and all
-// neighbour / partner reads hit shared memory.  IRLS weights are recomputed
+// by TMA (cp.async.bulk.tensor.3d boxes, mbarrier completion), so every HBM
+// word is read once per tile and all neighbour / partner reads hit shared
+// memory.  IRLS weights are recomputed
 // from sX (cheaper than storing 2K+3 weight planes).  Per-pixel arithmetic is
 // fp32 (the data residual exactly rounded via fp64 FMA); reductions are fp64,
 // fixed order, finished by the last block (no float atomics).
