@@ -16,8 +16,14 @@ import torch
 
 from . import _lib as L
 
-_cache: dict = {}
+from collections import OrderedDict
+
+# (device, H, W, K, thread) -> DeviceSolver, least recently used first; the
+# streaming loop reuses one entry, varying sizes (correction bounding boxes,
+# segmentation of other frame sizes) are evicted beyond MAX_CONTEXTS
+_cache: "OrderedDict" = OrderedDict()
 _cache_lock = threading.Lock()
+MAX_CONTEXTS = 16
 
 
 def _device_of(t) -> torch.device:
@@ -362,6 +368,10 @@ def get_solver(device: torch.device, H: int, W: int, K: int) -> DeviceSolver:
         if s is None:
             s = DeviceSolver(device, H, W, K)
             _cache[key] = s
+            while len(_cache) > MAX_CONTEXTS:     # the context is freed with its last reference
+                _cache.popitem(last=False)
+        else:
+            _cache.move_to_end(key)
         return s
 
 
