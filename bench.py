@@ -513,6 +513,11 @@ def run_ours(args):
                            "l2": "per-frame working set (~0.9 GB) exceeds the 126 MB L2; no flush",
                            "first_frame_ms": first_ms, "first_frame_warm_ms": first_warm_ms,
                            "first_frame_records": n_first_records,
+                           # whole-clip rate of a 300-frame clip including
+                           # frame 1 (refinement), from the warm frame-1 time and the measured
+                           # streaming frame time (extrapolated, not a timed 300-frame run)
+                           "whole_clip_fps_300_est": (300.0 / ((first_warm_ms + 299 * t_ms / steps) / 1e3)
+                                                      if first_warm_ms else None),
                            "wall_ms_per_step": wall_ms / steps},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk}

@@ -103,8 +103,8 @@ def pcg(apply_A: Callable, b, diag, iterations: int):
     """solver.py:79-107 for an arbitrary operator (numpy or torch vectors).
     The solver's own PCG is the fused device loop inside gn_step_sparse."""
     is_np = not isinstance(b, torch.Tensor)
-    bt = torch.as_tensor(np.asarray(b, dtype=np.float64)) if is_np else b
-    dt = torch.as_tensor(np.asarray(diag, dtype=np.float64)) if is_np else diag
+    bt = torch.as_tensor(np.array(b, dtype=np.float64)) if is_np else b
+    dt = torch.as_tensor(np.array(diag, dtype=np.float64)) if is_np else diag
     op = (lambda v: torch.as_tensor(np.asarray(apply_A(v.numpy())))) if is_np else apply_A
     x = torch.zeros_like(bt)
     bn = float(torch.linalg.norm(bt))
