@@ -418,15 +418,20 @@ def run_ours(args):
                                 "note": "per GPU"}}
 
     # --- frame 1 again with everything warm (refinement path, host-driven) ---
-    first_warm_ms = None
+    # (twice: the first re-run still pays for switching the contexts back from
+    # the streaming graphs; the warm figure is the faster of the two)
+    first_warm_ms, first_rerun_ms = None, None
     if not args.profile_only:
-        dec1 = StreamingDecomposer(pal, EnergyWeights(), cfg, seed=pal_seed, bands=bands)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        dec1.first(frames[0])
-        torch.cuda.synchronize()
-        first_warm_ms = (time.perf_counter() - t0) * 1e3
-        del dec1
+        runs = []
+        for _ in range(2):
+            dec1 = StreamingDecomposer(pal, EnergyWeights(), cfg, seed=pal_seed, bands=bands)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dec1.first(frames[0])
+            torch.cuda.synchronize()
+            runs.append((time.perf_counter() - t0) * 1e3)
+            del dec1
+        first_rerun_ms, first_warm_ms = runs[0], min(runs)
 
     # --- e2e through the public API with host buffers ---
     e2e = None
@@ -512,6 +517,7 @@ def run_ours(args):
                            "H": H, "W": W, "K": K, "gn_steps_per_frame": 4, "pcg_iterations": 16,
                            "l2": "per-frame working set (~0.9 GB) exceeds the 126 MB L2; no flush",
                            "first_frame_ms": first_ms, "first_frame_warm_ms": first_warm_ms,
+                           "first_frame_rerun_ms": first_rerun_ms,
                            "first_frame_records": n_first_records,
                            # whole-clip rate of a 300-frame clip including
                            # frame 1 (refinement), from the warm frame-1 time and the measured
