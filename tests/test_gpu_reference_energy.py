@@ -77,17 +77,6 @@ def test_clustering_residual_locality():
     assert np.isclose(e["clustering"], 200.0 * 3 * float(np.float32(0.7)) ** 2, rtol=1e-6)
 
 
-def test_irls_and_nonneg_weight_values():
-    """test_energy.py:122-132 (the reference-named host helpers)."""
-    from paper_1908_01961_b200.energy import irls_weight, nonneg_weight
-    assert np.isclose(irls_weight(np.array(0.5), 1.0, 1e-3), 2.0)
-    assert np.isclose(irls_weight(np.array(0.0), 1.0, 1e-3), 1000.0)
-    assert np.isclose(irls_weight(np.array(0.25), 1.0, 1e-3), 4.0)
-    assert np.isclose(nonneg_weight(np.array(-0.098), 0.002), 10.0)
-    assert np.isclose(nonneg_weight(np.array(0.0), 0.002), 500.0)
-    assert nonneg_weight(np.array(0.5), 0.002) == 0.0
-
-
 def test_rsparsity_constant_reflectance_zero():
     """test_energy.py:135-138."""
     e = energies(np.full((8, 8, 3), 0.5), [[1.0, 0.0, 0.0]], np.full((8, 8, 3), -0.5), np.full((8, 8, 2), 0.5))
