@@ -29,20 +29,30 @@ __device__ __forceinline__ unsigned long long pcg_out(u128 s) {
   return (x >> rot) | (x << ((64u - rot) & 63u));
 }
 
-// state after `delta` LCG steps (Brown's jump-ahead)
-__device__ __forceinline__ u128 pcg_advance(u128 state, u128 inc, unsigned long long delta) {
-  u128 cur_mult = mk128(kPcgMultHi, kPcgMultLo), cur_plus = inc;
-  u128 acc_mult = 1, acc_plus = 0;
-  while (delta > 0) {
-    if (delta & 1ULL) {
-      acc_mult *= cur_mult;
-      acc_plus = acc_plus * cur_mult + cur_plus;
-    }
-    cur_plus = (cur_mult + 1) * cur_plus;
-    cur_mult *= cur_mult;
-    delta >>= 1;
+// host: the jump table of SampleParams.  M_0 = A, S_0 = 1;
+// M_{k+1} = M_k^2, S_{k+1} = S_k (1 + M_k); C_k = inc * S_k (mod 2^128), so
+// 2^k LCG steps map s to M_k s + C_k (the same residue Brown's squaring loop
+// reaches, with one 128-bit multiply-add per set bit of the distance instead
+// of four multiplies per bit)
+static void fill_jump_table(SampleParams& P) {
+  const u128 inc = ((u128)P.inc_hi << 64) | (u128)P.inc_lo;
+  u128 M = ((u128)kPcgMultHi << 64) | (u128)kPcgMultLo, S = 1;
+  for (int k = 0; k < kJumpBits; ++k) {
+    const u128 C = inc * S;
+    P.jump[k][0] = (unsigned long long)(M >> 64);
+    P.jump[k][1] = (unsigned long long)M;
+    P.jump[k][2] = (unsigned long long)(C >> 64);
+    P.jump[k][3] = (unsigned long long)C;
+    S = S * (M + 1);
+    M = M * M;
   }
-  return acc_mult * state + acc_plus;
+}
+
+// state after `delta` LCG steps from the jump table
+__device__ __forceinline__ u128 pcg_jump(const SampleParams& P, u128 state, unsigned long long delta) {
+  for (int k = 0; delta && k < kJumpBits; ++k, delta >>= 1)
+    if (delta & 1ULL) state = mk128(P.jump[k][0], P.jump[k][1]) * state + mk128(P.jump[k][2], P.jump[k][3]);
+  return state;
 }
 
 // sequential reader of the u32 stream (low half of each 64-bit output first)
@@ -50,9 +60,9 @@ struct U32Stream {
   u128 state, inc;
   unsigned long long cur;
   int half;
-  __device__ void seek(u128 s0, u128 inc_, unsigned long long pos) {
+  __device__ void seek(const SampleParams& P, u128 s0, u128 inc_, unsigned long long pos) {
     inc = inc_;
-    state = pcg_advance(s0, inc, (pos >> 1) + 1);   // outputs come from the stepped state
+    state = pcg_jump(P, s0, (pos >> 1) + 1);   // outputs come from the stepped state
     cur = pcg_out(state);
     half = (int)(pos & 1ULL);
   }
@@ -154,7 +164,7 @@ __global__ void k_edge(const double* __restrict__ ch, int H, int W, float* __res
 // (k_sample_fix / redo) -- no host round trip.
 constexpr int kSamplePix = 8;
 
-__global__ void k_sample(SampleParams P, const SampleState* __restrict__ Sg, const double* __restrict__ ch,
+__global__ void k_sample(const __grid_constant__ SampleParams P, const SampleState* __restrict__ Sg, const double* __restrict__ ch,
                          const double* __restrict__ pch, int H, int W, int16_t* __restrict__ codes,
                          int32_t* __restrict__ out_cnt, int32_t* __restrict__ in_cnt, SampleState* Sw) {
   if (!Sg->redo) return;
@@ -174,7 +184,7 @@ __global__ void k_sample(SampleParams P, const SampleState* __restrict__ Sg, con
     // reject iff (u * 15) mod 2^32 < (2^32 mod 15) = 1, i.e. u == 0
     for (int sec = 0; sec < 2; ++sec) {
       unsigned long long pos = shifted_pos(Sg, nz, (unsigned long long)sec * 4ULL * Ng + 4ULL * (goff + p0));
-      st.seek(s0, inc, pos);
+      st.seek(P, s0, inc, pos);
 #pragma unroll
       for (int d = 0; d < 4 * kSamplePix; ++d) {
         if (d >= 4 * np) break;
@@ -191,7 +201,7 @@ __global__ void k_sample(SampleParams P, const SampleState* __restrict__ Sg, con
       }
     }
     if (P.has_prev) {   // rng.integers(0, 2): Lemire threshold 0, no rejection
-      st.seek(s0, inc, shifted_pos(Sg, nz, 8ULL * Ng + 4ULL * (goff + p0)));
+      st.seek(P, s0, inc, shifted_pos(Sg, nz, 8ULL * Ng + 4ULL * (goff + p0)));
 #pragma unroll
       for (int d = 0; d < 4 * kSamplePix; ++d) {
         if (d >= 4 * np) break;
@@ -263,7 +273,7 @@ __global__ void k_sample_init_known(SampleState* S, const long long* lists, int 
 }
 
 constexpr int kScanPerThread = 256;
-__global__ void k_zero_scan(SampleParams P, unsigned long long begin, unsigned long long end, long long* list) {
+__global__ void k_zero_scan(const __grid_constant__ SampleParams P, unsigned long long begin, unsigned long long end, long long* list) {
   const u128 s0 = mk128(P.st_hi, P.st_lo), inc = mk128(P.inc_hi, P.inc_lo);
   const unsigned long long n = end > begin ? end - begin : 0;
   const unsigned long long nth = (n + kScanPerThread - 1) / kScanPerThread;
@@ -271,7 +281,7 @@ __global__ void k_zero_scan(SampleParams P, unsigned long long begin, unsigned l
        t += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long p0 = begin + t * kScanPerThread;
     U32Stream st;
-    st.seek(s0, inc, p0);
+    st.seek(P, s0, inc, p0);
     for (int d = 0; d < kScanPerThread; ++d) {
       const unsigned long long pos = p0 + d;
       if (pos >= end) break;
@@ -560,9 +570,11 @@ void launch_image(cudaStream_t s, const float* hwc, int N, float* img, double* c
 void launch_edge(cudaStream_t s, const double* chroma, int H, int W, float* edge) {
   k_edge<<<grid_for((int64_t)H * W), 256, 0, s>>>(chroma, H, W, edge);
 }
-void launch_sample(cudaStream_t s, const SampleParams& P, SampleState* S, const double* chroma,
+void launch_sample(cudaStream_t s, const SampleParams& P_in, SampleState* S, const double* chroma,
                    const double* prev_chroma, int H, int W, int16_t* codes, int32_t* out_cnt, int32_t* in_cnt,
                    int passes, const long long* known, int n_known_lists) {
+  SampleParams P = P_in;
+  fill_jump_table(P);
   const int N = H * W;
   const int nthreads = (N + kSamplePix - 1) / kSamplePix;
   if (known) k_sample_init_known<<<1, 1, 0, s>>>(S, known, n_known_lists);
@@ -573,8 +585,10 @@ void launch_sample(cudaStream_t s, const SampleParams& P, SampleState* S, const 
     k_sample_fix<<<1, 1, 0, s>>>(S, pass == passes - 1);
   }
 }
-void launch_zero_scan(cudaStream_t s, const SampleParams& P, unsigned long long begin, unsigned long long end,
+void launch_zero_scan(cudaStream_t s, const SampleParams& P_in, unsigned long long begin, unsigned long long end,
                       long long* list) {
+  SampleParams P = P_in;
+  fill_jump_table(P);
   cudaMemsetAsync(list, 0, sizeof(long long) * kZeroList, s);
   const unsigned long long nth = ((end > begin ? end - begin : 0) + kScanPerThread - 1) / kScanPerThread;
   if (nth) k_zero_scan<<<grid_for((int64_t)nth, 128), 128, 0, s>>>(P, begin, end, list);

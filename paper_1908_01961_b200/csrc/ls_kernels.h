@@ -67,6 +67,7 @@ int apply_grid_limit(int NT);
 int update_grid_limit();
 
 // ls_aux.cu
+constexpr int kJumpBits = 40;   // stream positions < 2^41 u32 words
 struct SampleParams {
   unsigned long long st_hi, st_lo, inc_hi, inc_lo;
   int has_prev;
@@ -74,6 +75,9 @@ struct SampleParams {
   // with Ng pixels (the PCG64 stream is indexed by global pixel)
   int gy0, GH;
   long long goff, Ng;
+  // jump table of the LCG (filled by the launchers): 2^k steps are
+  // s -> M_k s + C_k, as {M_k hi, M_k lo, C_k hi, C_k lo}
+  unsigned long long jump[kJumpBits][4];
 };
 constexpr int kMaxRejections = 16;
 // device-resident rejection bookkeeping of the partner sampler

@@ -67,15 +67,27 @@ class Frame:
         return int(self.data.shape[1])
 
 
-@dataclass(frozen=True)
 class ChromaticityImage:
     """(r, g) chroma, channel-sum intensity and dark flag (imaging.py:60-66).
     `planes` is the (2, H, W) fp64 layout the kernels consume; `chroma` is
-    the reference's (H, W, 2) view of it."""
+    the reference's (H, W, 2) view of it.  `intensity` / `dark` are computed
+    from the image on first access (the kernels need only the planes)."""
 
-    planes: torch.Tensor
-    intensity: torch.Tensor
-    dark: torch.Tensor
+    def __init__(self, planes, intensity=None, dark=None, *, image=None):
+        self.planes = planes
+        self._intensity, self._dark, self._image = intensity, dark, image
+
+    @property
+    def intensity(self) -> torch.Tensor:
+        if self._intensity is None:
+            self._intensity = self._image.double().sum(dim=2)
+        return self._intensity
+
+    @property
+    def dark(self) -> torch.Tensor:
+        if self._dark is None:
+            self._dark = self.intensity < DARK_INTENSITY
+        return self._dark
 
     @property
     def chroma(self) -> torch.Tensor:
@@ -96,9 +108,7 @@ def frame_from_array(data) -> Frame:
 def chromaticity(frame: Frame) -> ChromaticityImage:
     """imaging.py:160-171 on the device (fp64)."""
     img = frame.data if isinstance(frame, Frame) else as_cuda(frame)
-    planes = _device.chromaticity_planes(img)
-    inten = img.double().sum(dim=2)
-    return ChromaticityImage(planes=planes, intensity=inten, dark=inten < DARK_INTENSITY)
+    return ChromaticityImage(planes=_device.chromaticity_planes(img), image=img)
 
 
 def chroma_of_color(color) -> np.ndarray:

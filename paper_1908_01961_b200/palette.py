@@ -56,12 +56,35 @@ class BaseColorPalette:
         return chroma_of_color(self.colors)
 
 
-@dataclass
 class ClusterMap:
-    """Per-pixel cluster id (1..K) and clustered reflectance (palette.py:73-78)."""
+    """Per-pixel cluster id (1..K) and clustered reflectance (palette.py:73-78).
 
-    ids: torch.Tensor        # (H, W) int32, CUDA
-    r_cluster: torch.Tensor  # (H, W, 3) float32, CUDA
+    `ClusterMap(ids, r_cluster)` as in the reference; `segment` passes the
+    palette instead and `r_cluster` (= colors[ids - 1]) is gathered on first
+    access -- the streaming solve anchors on the ids alone, so a per-frame
+    (H, W, 3) gather the solver never reads is not launched."""
+
+    def __init__(self, ids, r_cluster=None, *, colors=None):
+        if r_cluster is None and colors is None:
+            raise ValueError("ClusterMap needs r_cluster or the palette colors")
+        self.ids = ids              # (H, W) int32, CUDA
+        self._r_cluster = r_cluster
+        self._colors = colors
+
+    @property
+    def r_cluster(self):            # (H, W, 3) float32, CUDA
+        if self._r_cluster is None:
+            ids = self.ids
+            cols = torch.as_tensor(self._colors, dtype=torch.float32, device=ids.device)
+            self._r_cluster = cols[(ids - 1).long()]
+        return self._r_cluster
+
+    @r_cluster.setter
+    def r_cluster(self, value):
+        self._r_cluster = value
+
+    def __repr__(self):
+        return f"ClusterMap(ids={tuple(self.ids.shape)})"
 
 
 def segment(frame: Frame, palette: BaseColorPalette, chroma=None) -> ClusterMap:
@@ -78,8 +101,7 @@ def segment(frame: Frame, palette: BaseColorPalette, chroma=None) -> ClusterMap:
         solver.set_image(img)
         solver.installed = None
         ids = solver.segment(palette.colors)
-    cols = torch.as_tensor(palette.colors, dtype=torch.float32, device=img.device)
-    return ClusterMap(ids=ids, r_cluster=cols[(ids - 1).long()])
+    return ClusterMap(ids=ids, colors=np.array(palette.colors, dtype=np.float64))
 
 
 # ---- first-frame palette estimation (host; out of the hot path) -------------
