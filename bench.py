@@ -437,46 +437,59 @@ def run_ours(args):
     e2e = None
     if e2e_on:
         host = [frames[1 + warmup + 2 * steps + i].cpu().pin_memory() for i in range(steps)]
+        # the warm-up frames of the headline pass again, as pinned host frames
+        host_warm = [frames[1 + i].cpu().pin_memory() for i in range(warmup)]
         out_host = [torch.empty(tuple(st.layers.X.shape), dtype=torch.float32).pin_memory() for _ in range(2)]
         side = torch.cuda.Stream(device=dev)
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         main = torch.cuda.current_stream()
         up = torch.cuda.Stream(device=dev)
 
-        def upload(j):   # frame j's host -> device copy on the upload stream
-            with torch.cuda.stream(up):
-                t = host[j].to(dev, non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(up)
-            return t, ev
+        def e2e_loop(hf):
+            """len(hf) frames through dec.step from pinned host memory; returns the
+            CUDA-event time of the whole loop (every H2D and D2H inside it)."""
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
-        e0.record()
-        up.wait_stream(main)
-        nxt = upload(0)
-        for i in range(steps):
-            fdev, ev = nxt
-            main.wait_event(ev)
-            fdev.record_stream(main)
-            if i + 1 < steps and not os.environ.get("LS_E2E_SERIAL"):
-                nxt = upload(i + 1)          # the next frame's upload overlaps this solve
-            elif i + 1 < steps:
-                nxt = (host[i + 1].to(dev, non_blocking=True), torch.cuda.Event())
-                nxt[1].record(main)
-            s2 = dec.step(fdev)
-            done = torch.cuda.Event()
-            done.record()
-            side.wait_event(done)
-            with torch.cuda.stream(side):
-                X = s2.layers.X
-                X.record_stream(side)
-                out_host[i % 2].copy_(X, non_blocking=True)
-        torch.cuda.current_stream().wait_stream(side)
-        e1.record()
-        torch.cuda.synchronize()
-        e_ms = e0.elapsed_time(e1)
+            def upload(j):   # frame j's host -> device copy on the upload stream
+                with torch.cuda.stream(up):
+                    t = hf[j].to(dev, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(up)
+                return t, ev
+
+            n = len(hf)
+            e0.record()
+            up.wait_stream(main)
+            nxt = upload(0)
+            for i in range(n):
+                fdev, ev = nxt
+                main.wait_event(ev)
+                fdev.record_stream(main)
+                if i + 1 < n and not os.environ.get("LS_E2E_SERIAL"):
+                    nxt = upload(i + 1)          # the next frame's upload overlaps this solve
+                elif i + 1 < n:
+                    nxt = (hf[i + 1].to(dev, non_blocking=True), torch.cuda.Event())
+                    nxt[1].record(main)
+                s2 = dec.step(fdev)
+                done = torch.cuda.Event()
+                done.record()
+                side.wait_event(done)
+                with torch.cuda.stream(side):
+                    X = s2.layers.X
+                    X.record_stream(side)
+                    out_host[i % 2].copy_(X, non_blocking=True)
+            main.wait_stream(side)
+            e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1)
+
+        # untimed warm-up of the same loop: the first pass pays for the upload
+        # stream's allocator blocks and the copy-stream setup (~1 ms/frame
+        # over 20 frames, tools/e2e_probe.py)
+        e2e_loop(host_warm)
+        e_ms = e2e_loop(host)
         eth = clips.aggregate(steps, e_ms / 1e3)
         if four_k and world > 1:
             eth = clips.aggregate(steps if rank == 0 else 0, e_ms / 1e3)

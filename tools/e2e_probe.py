@@ -19,7 +19,7 @@ host = [f.cpu().pin_memory() for f in clip.frames[4:]]
 out_host = [torch.empty(tuple(st.layers.X.shape), dtype=torch.float32).pin_memory() for _ in range(2)]
 side = torch.cuda.Stream()
 cp = torch.cuda.Stream()
-for mode in ("device", "h2d", "d2h", "both", "overlap", "device"):
+for mode in sys.argv[1:] or ("device", "h2d", "d2h", "both", "overlap", "device"):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
