@@ -245,6 +245,12 @@ enum { LS_BAND_EG = 0, LS_BAND_APPLY = 1, LS_BAND_UPDATE = 2, LS_BAND_TRIAL = 3 
  * captured ls_band_* work as its own CUDA graph adds the replayed launches */
 LS_API int ls_launch_count(ls_ctx* ctx, int64_t* n);
 LS_API int ls_add_launches(ls_ctx* ctx, int64_t n);
+/* Bytes of everything the kernels of this context bake into their launch
+ * arguments (weights, solve config, per-frame pointers and flags such as
+ * prev_r / ids / anchor / pair weights, band rows, TMA use): a caller that
+ * captures ls_band_* work as its own CUDA graph keys the graph on them.
+ * Writes at most cap bytes to out and the full length to *len. */
+LS_API int ls_state_key(ls_ctx* ctx, void* out, int64_t cap, int64_t* len);
 LS_API int ls_band_set(ls_ctx* ctx, int gy0, int GH, int y_lo, int y_hi);
 LS_API int ls_band_clear(ls_ctx* ctx);
 /* out[6] = {partials (512 doubles), z, p_even, p_odd, x, r}: the PCG vectors

@@ -98,6 +98,7 @@ SIGNATURES = {
     # row bands
     "ls_launch_count": [P, C.POINTER(I64)],
     "ls_add_launches": [P, I64],
+    "ls_state_key": [P, P, I64, C.POINTER(I64)],
     "ls_band_set": [P, C.c_int, C.c_int, C.c_int, C.c_int],
     "ls_band_clear": [P],
     "ls_band_buffers": [P, C.POINTER(C.c_void_p)],

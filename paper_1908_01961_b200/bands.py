@@ -533,6 +533,13 @@ class BandedSolver:
         return L.LS_OK, recs, status, out, -1
 
     @staticmethod
+    def _state_key(b) -> bytes:
+        n = C.c_int64()
+        buf = (C.c_char * 1024)()
+        b.chk(b.lib.ls_state_key(b.ctx, buf, 1024, C.byref(n)))
+        return bytes(buf[:min(1024, n.value)])
+
+    @staticmethod
     def _launches(b) -> int:
         n = C.c_int64()
         b.chk(b.lib.ls_launch_count(b.ctx, C.byref(n)))
@@ -607,8 +614,12 @@ class BandedSolver:
             import os
             graph = (self.whole and not os.environ.get("LS_NO_GRAPH")
                      and not any(b.solver.prof_on for b in self.bands))
+        # everything the band kernels bake into their launch arguments: the
+        # palette, the loop shape, and each band context's weights / config /
+        # per-frame pointers and flags (prev_r present, ids vs anchor, ...)
         key = (np.asarray(colors, dtype=np.float64).tobytes(), outer, gn_steps, float(tol_rel),
-               self.cfg.pcg_iterations, self.cfg.max_halvings)
+               self.cfg.pcg_iterations, self.cfg.max_halvings,
+               tuple(self._state_key(b) for b in self.bands))
         if graph:
             if self._graph is None or self._graph_key != key:
                 g = torch.cuda.CUDAGraph()

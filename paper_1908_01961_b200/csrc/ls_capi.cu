@@ -204,6 +204,7 @@ static Coef<R> make_coef(const ls_weights& w, const double* colors, int K) {
 
 static Frame frame_of(const ls_ctx* c) {
   Frame f;
+  std::memset(&f, 0, sizeof(f));   // padding bytes take part in graph keys
   f.H = c->H;
   f.W = c->W;
   f.N = c->N;
@@ -392,6 +393,24 @@ int ls_launch_count(ls_ctx* c, int64_t* n) {
 int ls_add_launches(ls_ctx* c, int64_t n) {
   LS_ARG(c && c->launches + n >= 0, "bad arguments");
   c->launches += n;
+  return LS_OK;
+}
+
+int ls_state_key(ls_ctx* c, void* out, int64_t cap, int64_t* len) {
+  LS_ARG(c && len && (out || cap == 0), "bad arguments");
+  struct {
+    ls_weights w;
+    ls_solve_cfg cfg;
+    Frame f;
+    int use_tma;
+  } key;
+  std::memset(&key, 0, sizeof(key));
+  key.w = c->w;
+  key.cfg = c->cfg;
+  key.f = frame_of(c);
+  key.use_tma = c->use_tma;
+  *len = (int64_t)sizeof(key);
+  if (cap > 0) std::memcpy(out, &key, (size_t)std::min<int64_t>(cap, sizeof(key)));
   return LS_OK;
 }
 

@@ -62,9 +62,25 @@ def find_frames(input_dir) -> list[Path]:
     return [chosen[i] for i in sorted(chosen)]
 
 
-def write_frame_files(out_dir, index: int, X: np.ndarray, colors: np.ndarray, ids: np.ndarray) -> None:
+def cluster_reflectance(cluster_map):
+    """What the reference writes as r_cluster.pfm (pipeline.py:213-214): the
+    map's own clustered reflectance -- for a segmented map the colors of the
+    palette it was segmented with (palette.py:223), which for frame 1 is the
+    palette BEFORE refinement.  Returns ("colors", (K, 3)) when the map is
+    the lazy ids -> colors gather, else ("array", (H, W, 3) host array)."""
+    if getattr(cluster_map, "_r_cluster", None) is None and getattr(cluster_map, "_colors", None) is not None:
+        return "colors", np.array(cluster_map._colors, dtype=np.float64)
+    rc = cluster_map.r_cluster
+    if isinstance(rc, torch.Tensor):
+        rc = rc.detach().cpu().numpy()
+    return "array", np.asarray(rc)
+
+
+def write_frame_files(out_dir, index: int, X: np.ndarray, colors: np.ndarray, ids: np.ndarray,
+                      r_cluster=None) -> None:
     """pipeline.py:197-214 from host arrays: X (U, H, W) planar state,
-    colors (K, 3), ids (H, W)."""
+    colors (K, 3) (the palette the layers were solved with), ids (H, W);
+    r_cluster = cluster_reflectance(cluster_map) (default: colors[ids - 1])."""
     frame_dir = Path(out_dir) / f"frame_{index:06d}"
     frame_dir.mkdir(parents=True, exist_ok=True)
     r = np.transpose(X[:3], (1, 2, 0)).astype(np.float64)
@@ -81,7 +97,8 @@ def write_frame_files(out_dir, index: int, X: np.ndarray, colors: np.ndarray, id
     B = np.vstack([np.ones((1, 3)), colors])
     recon = R * np.tensordot(T, B, axes=([2], [0]))
     save_png_preview(frame_dir / "reconstruction.png", recon)
-    r_cluster = colors[np.asarray(ids, dtype=np.int64) - 1]
+    kind, src = r_cluster if r_cluster is not None else ("colors", colors)
+    r_cluster = src[np.asarray(ids, dtype=np.int64) - 1] if kind == "colors" else src
     save_cluster_map(frame_dir / "cluster_ids.png", frame_dir / "r_cluster.pfm", ids, r_cluster)
 
 
@@ -90,7 +107,8 @@ def write_frame_outputs(out_dir, index: int, layers, palette, cluster_map) -> No
     X = layers.X.detach().float().cpu().numpy()
     ids = cluster_map.ids.detach().cpu().numpy() if isinstance(cluster_map.ids, torch.Tensor) \
         else np.asarray(cluster_map.ids)
-    write_frame_files(out_dir, index, X, np.asarray(palette.colors, dtype=np.float64), ids)
+    write_frame_files(out_dir, index, X, np.asarray(palette.colors, dtype=np.float64), ids,
+                      cluster_reflectance(cluster_map))
 
 
 class AsyncFrameWriter:
@@ -141,17 +159,18 @@ class AsyncFrameWriter:
             hX.copy_(X, non_blocking=True)
             hids.copy_(ids, non_blocking=True)
             done.record(self.stream)
-        self.todo.put((index, hX, hids, np.array(palette.colors, dtype=np.float64), done))
+        self.todo.put((index, hX, hids, np.array(palette.colors, dtype=np.float64),
+                       cluster_reflectance(cluster_map), done))
 
     def _run(self):
         while True:
             item = self.todo.get()
             if item is None:
                 return
-            index, hX, hids, colors, done = item
+            index, hX, hids, colors, rc, done = item
             try:
                 done.synchronize()
-                write_frame_files(self.out_dir, index, hX.numpy(), colors, hids.numpy())
+                write_frame_files(self.out_dir, index, hX.numpy(), colors, hids.numpy(), rc)
             except Exception as e:      # surfaced by the next submit() / close()
                 self.error = e
             finally:
@@ -214,7 +233,7 @@ def run_pipeline(input_dir, output_dir, weights=None, config=None, seed: int = 0
 
     try:
         result = decompose_frames(frames, weights, config, seed=seed, k_max=k_max, clicks=clicks,
-                                  streaming_outer=streaming_outer, on_frame=on_frame)
+                                  streaming_outer=streaming_outer, on_frame=on_frame, bands=bands)
     finally:
         writer.close()
     save_palette(out / "palette.json", result.palette)

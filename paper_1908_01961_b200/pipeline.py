@@ -156,16 +156,17 @@ def decompose_frames(frames: list, weights: EnergyWeights, config: SolveConfig, 
                      k_max: int = 10, clicks: list | None = None, streaming_outer: int = 2,
                      palette: BaseColorPalette | None = None,
                      cluster_map: ClusterMap | None = None,
-                     on_frame=None) -> PipelineResult:
+                     on_frame=None, bands=0) -> PipelineResult:
     """Decompose an in-memory frame sequence (pipeline.py:87-167).
 
     Extra keyword arguments (not in the reference): `palette` /
     `cluster_map` skip first-frame estimation (SURVEY.md section 8d uses the
     generator palette); `on_frame(index, state)` is called after each frame
-    (streams results out without keeping them)."""
+    (streams results out without keeping them); `bands` solves every frame
+    as row bands (bands.py; 0 = whole frames)."""
     if not frames:
         raise ValueError("no frames")
-    f0 = _as_frame(frames[0])
+    f0 = _as_frame(frames[0], bands)
     if palette is None:
         palette, cluster_map = estimate_palette(f0, k_max=k_max, seed=seed)
     elif cluster_map is None:
@@ -178,7 +179,7 @@ def decompose_frames(frames: list, weights: EnergyWeights, config: SolveConfig, 
     result = PipelineResult(palette=palette, layer_stacks=[], cluster_maps=[], regions=regions,
                             records=[], statuses=[])
     dec = StreamingDecomposer(palette, weights, config, seed=seed, streaming_outer=streaming_outer,
-                              regions=regions)
+                              bands=bands, regions=regions)
     for idx, f in enumerate(frames):
         t0 = time.perf_counter()
         state = dec.first(f0, cluster_map) if idx == 0 else dec.step(f)

@@ -34,6 +34,19 @@ def test_write_frame_files_match_reference_bytes(tmp_path):
     assert _hashes(tmp_path) == g["files"]
 
 
+def test_r_cluster_written_from_the_cluster_maps_palette(tmp_path):
+    """after refinement the frame-1 cluster map still holds the
+    pre-refinement palette's reflectance; the reference writes that map
+    (pipeline.py:213-214), not colors[ids - 1] of the refined palette."""
+    g, colors, X, ids = _golden()
+    cc = np.array(g["cluster_colors"])
+    frameio.write_frame_files(tmp_path, 1, X, colors, ids, ("colors", cc))
+    assert _hashes(tmp_path) == g["files_cluster_palette"]
+    d2 = tmp_path / "explicit"
+    frameio.write_frame_files(d2, 1, X, colors, ids, ("array", cc[ids - 1]))
+    assert _hashes(d2) == g["files_cluster_palette"]
+
+
 def test_pfm_png_roundtrip_and_find_frames(tmp_path):
     from paper_1908_01961_b200.imaging import load_pfm, save_pfm
     a = np.random.default_rng(0).uniform(size=(5, 7, 3)).astype(np.float32)
@@ -79,6 +92,13 @@ def test_async_writer_matches_sync_bytes(tmp_path):
         sub = {k.replace(f"frame_{idx:06d}", "frame_000003"): v for k, v in h.items()
                if k.startswith(f"frame_{idx:06d}")}
         assert sub == g["files"]
+    # a cluster map segmented with another (pre-refinement) palette
+    w = frameio.AsyncFrameWriter(tmp_path / "rc", depth=2)
+    pal_c = BaseColorPalette(colors=np.array(g["cluster_colors"]))
+    w.submit(1, LayerStack(planes=torch.as_tensor(X).cuda()), pal,
+             cluster_map_from_ids(ids, pal_c, device=torch.device("cuda")))
+    w.close()
+    assert _hashes(tmp_path / "rc") == g["files_cluster_palette"]
 
 
 @pytest.mark.gpu

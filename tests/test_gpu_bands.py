@@ -155,3 +155,50 @@ def test_banded_device_flip_flop_matches_host_loop_and_graph():
     r2g = bs.flip_flop_stream(st.palette.colors, outs[1][3], 2, 2, 1e-3, graph=True)
     r2e = bs.flip_flop_stream(st.palette.colors, outs[1][3], 2, 2, 1e-3, graph=False)
     assert torch.equal(r2g[3], r2e[3])
+
+
+def test_banded_graph_recaptured_when_frame_state_changes():
+    """frame 1 without refinement and with outer_iterations equal to
+    the streaming count captures the band graph with no previous-frame
+    reflectance; frame 2 (temporal partners) must not replay that graph.
+    Banded and whole-frame clips agree frame by frame."""
+    from paper_1908_01961_b200.energy import EnergyWeights
+    from paper_1908_01961_b200.palette import BaseColorPalette
+    from paper_1908_01961_b200.pipeline import StreamingDecomposer
+    from paper_1908_01961_b200.solver import SolveConfig
+    clip = _clip(160, 192, 4, n=3, seed=11)
+    cfg = SolveConfig(tol_rel=0.0, refine=False, outer_iterations=2)
+    out = []
+    for bands in (0, 3):
+        dec = StreamingDecomposer(BaseColorPalette(colors=clip.colors), EnergyWeights(), cfg,
+                                  seed=0, streaming_outer=2, bands=bands)
+        sts = [dec.first(clip.frames[0].cuda())] + [dec.step(f.cuda()) for f in clip.frames[1:]]
+        torch.cuda.synchronize()
+        out.append(sts)
+    for a, b in zip(*out):
+        assert len(a.records) == len(b.records)
+        for ra, rb in zip(a.records, b.records):
+            assert ra["accepted"] == rb["accepted"]
+            assert abs(ra["energy_after"] - rb["energy_after"]) <= 1e-6 * ra["energy_after"]
+        d = (a.layers.X - b.layers.X).abs()
+        assert float((d <= 1e-3).float().mean()) >= 0.999
+
+
+def test_banded_graph_key_tracks_weights():
+    """Changing the energy weights between frames re-captures the band graph
+    (the weights are baked into the kernels' arguments)."""
+    from paper_1908_01961_b200.bands import banded_solver
+    from paper_1908_01961_b200.energy import EnergyWeights
+    from paper_1908_01961_b200.solver import SolveConfig, _solver_for, gn_step_sparse
+    clip = _clip(160, 128, 4, n=2, seed=12)
+    s0 = _state(clip)
+    gn_step_sparse(s0)
+    st = _state(clip, 1, bands=2, prev=(s0.frame, s0.layers), seed=3)
+    bs = _solver_for(st)
+    X0 = st.layers.X.clone()
+    g1 = bs.flip_flop_stream(st.palette.colors, X0, 1, 2, 0.0, graph=True)
+    bs.configure(EnergyWeights(lambda_smoothness=30.0), SolveConfig(tol_rel=0.0))
+    g2 = bs.flip_flop_stream(st.palette.colors, X0, 1, 2, 0.0, graph=True)
+    e2 = bs.flip_flop_stream(st.palette.colors, X0, 1, 2, 0.0, graph=False)
+    assert torch.equal(g2[3], e2[3])
+    assert not torch.equal(g1[3], g2[3])

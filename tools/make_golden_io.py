@@ -34,8 +34,19 @@ def main():
                               ClusterMap(ids=ids, r_cluster=colors[ids - 1]))
         files = {str(p.relative_to(d)): hashlib.sha256(p.read_bytes()).hexdigest()
                  for p in sorted(d.rglob("*")) if p.is_file()}
+    # frame 1 after refinement: the cluster map keeps the pre-refinement
+    # palette's reflectance while the layers are written with the refined one
+    cluster_colors = np.clip(colors + np.array([0.05, -0.03, 0.02]), 0.0, 1.0)
+    with tempfile.TemporaryDirectory() as d:
+        d = Path(d)
+        P.write_frame_outputs(d, 1, LayerStack(r=r, T=T), BaseColorPalette(colors=colors),
+                              ClusterMap(ids=ids, r_cluster=cluster_colors[ids - 1]))
+        files_rc = {str(p.relative_to(d)): hashlib.sha256(p.read_bytes()).hexdigest()
+                    for p in sorted(d.rglob("*")) if p.is_file()}
     OUT.write_text(json.dumps({"colors": colors.tolist(), "r": r.tolist(), "T": T.tolist(),
-                               "ids": ids.tolist(), "files": files}) + "\n")
+                               "ids": ids.tolist(), "files": files,
+                               "cluster_colors": cluster_colors.tolist(),
+                               "files_cluster_palette": files_rc}) + "\n")
     print(f"wrote {OUT} ({len(files)} files)")
 
 
