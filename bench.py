@@ -11,10 +11,12 @@ weak scaling; time = max over ranks of the CUDA-event time.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-`--impl reference` times the reference algorithm on the host CPU (the
-numpy oracle port, oracle/lumisplit_oracle.py -- the reference package is
-pure Python and cannot travel to the GPU box) on a bounded strip of the same
-workload, extrapolated to frames/sec at 1080p.
+`--impl reference` times the reference algorithm on the host CPU: the
+compiled fp64 restatement of the reference solver (oracle/ls_oracle.c,
+pinned to the reference's own outputs by tests/test_oracle_c.py; the
+reference package is pure Python/NumPy at ~390 s per 1080p frame and
+cannot travel to the GPU box) on full-size frames of the same workload,
+every host thread.
 """
 
 from __future__ import annotations
@@ -34,7 +36,6 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "decomposed frames/sec at 1080p"
 UNIT = "frames/s"
-STRIP_ROWS = 16          # CPU sample: a 1920 x 16 strip of the same frames
 
 
 def parse():
@@ -147,39 +148,10 @@ def traffic_from_profiles(kernel: str):
 
 
 # ---------------------------------------------------------------------------
-# CPU reference leg: the oracle port on a bounded strip of the same frames
+# CPU legs: the compiled restatement of the reference (oracle/ls_oracle.c,
+# pinned to the reference's outputs by tests/test_oracle_c.py) on FULL-SIZE
+# frames of the same synthetic workload, all host threads (OpenMP over rows)
 # ---------------------------------------------------------------------------
-def cpu_sample(frames_np, colors, prev_state, strip_rows, seed):
-    """One streaming frame of the reference algorithm (segment, build_aux,
-    2 outer x 2 GN, pipeline.py:139-156) on rows [0, strip_rows) of the
-    frame, warm-started from `prev_state` (r, T) of the same strip.
-    Returns (seconds, new state)."""
-    from dataclasses import replace
-    from oracle import lumisplit_oracle as O
-    img_prev, img = frames_np
-    sl = slice(0, strip_rows)
-    img = img[sl]
-    img_prev = img_prev[sl]
-    r_prev, T_prev = prev_state
-    t0 = time.perf_counter()
-    ids = O.segment(img, colors)
-    aux = O.build_aux(img, ids, seed, O.chromaticity(img_prev)[0], r_prev)
-    cfg = replace(O.Config(tol_rel=0.0), refine=False, outer_iterations=2)
-    st = O.State(image=img, colors=colors, r=r_prev.copy(), T=T_prev.copy(), aux=aux,
-                 weights=O.Weights(), config=cfg)
-    O.flip_flop(st)
-    return time.perf_counter() - t0, (st.r, st.T)
-
-
-def limit_threads():
-    try:
-        from threadpoolctl import threadpool_limits
-        return threadpool_limits(1)
-    except ImportError:
-        os.environ["OPENBLAS_NUM_THREADS"] = "1"
-        return None
-
-
 def cpu_model():
     try:
         for ln in open("/proc/cpuinfo"):
@@ -190,42 +162,6 @@ def cpu_model():
     return "unknown"
 
 
-def make_cpu_inputs(H, W, K, strip_rows, n):
-    """Frames + a warm start for the CPU sample, generated on the host
-    (same generator and seed as the GPU leg)."""
-    import numpy as np
-    from paper_1908_01961_b200 import synth
-    clip = synth.make_clip(strip_rows, W, K, n + 1, seed=0, device="cpu")
-    frames = [f.double().numpy() for f in clip.frames]
-    from oracle import lumisplit_oracle as O
-    ids = O.segment(frames[0], clip.colors)
-    r, T = O.initialize(frames[0], ids, clip.colors)
-    return frames, clip.colors, (r, T)
-
-
-def _reference_worker(job):
-    """One host core: warm-up + timed streaming frames of the oracle port on
-    its own 16-row strip (a different synthetic clip per worker)."""
-    H, W, K, warmup, steps, wid = job
-    import torch
-    torch.set_num_threads(1)
-    guard = limit_threads()
-    from oracle import lumisplit_oracle as O
-    from paper_1908_01961_b200 import synth
-    n = warmup + steps
-    clip = synth.make_clip(STRIP_ROWS, W, K, n + 1, seed=wid, device="cpu")
-    frames = [f.double().numpy() for f in clip.frames]
-    ids = O.segment(frames[0], clip.colors)
-    state = O.initialize(frames[0], ids, clip.colors)
-    t_timed = 0.0
-    for i in range(n):
-        dt, state = cpu_sample((frames[i], frames[i + 1]), clip.colors, state, STRIP_ROWS, seed=i + 1)
-        if i >= warmup:
-            t_timed += dt
-    del guard
-    return t_timed
-
-
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -233,36 +169,72 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
+class CpuClip:
+    """Host frames of the bench clip (same generator and seed as the GPU
+    leg) and the streaming loop of pipeline.py:136-166 run by the C oracle."""
+
+    def __init__(self, H, W, K, n_frames, seed=0, threads=None):
+        import torch
+        from oracle import c_oracle as CO
+        from paper_1908_01961_b200 import synth
+        self.CO = CO
+        torch.set_num_threads(max(1, host_cores()))
+        clip = synth.make_clip(H, W, K, n_frames, seed=seed, device="cpu")
+        self.frames = [f.double().numpy() for f in clip.frames]
+        self.colors = clip.colors
+        self.seed = seed
+        self.threads = threads or host_cores()
+        CO.set_threads(self.threads)
+        ids = CO.segment(self.frames[0], self.colors)
+        r, T = CO.initialize(self.frames[0], ids, self.colors)
+        self.prev = _Prev(r, T)
+
+    def frame(self, i):
+        """Streaming frame i (segment + aux + 2 outer x 2 GN x 16 PCG), warm
+        started from frame i-1's result.  Returns the seconds it took."""
+        from dataclasses import replace
+        from oracle import lumisplit_oracle as O
+        cfg = replace(O.Config(tol_rel=0.0), refine=False, outer_iterations=2)
+        t0 = time.perf_counter()
+        st = self.CO.stream_frame(self.frames[i], self.colors, self.prev, self.frames[i - 1], O.Weights(),
+                                  cfg, self.seed + i)
+        dt = time.perf_counter() - t0
+        self.prev = _Prev(st.r, st.T)
+        return dt
+
+
+class _Prev:
+    def __init__(self, r, T):
+        self.r, self.T = r, T
+
+
 def run_reference(args):
-    """The reference arm: the oracle port (the reference is Python and cannot
-    travel to the GPU box) on every host core at once -- one process per core,
-    each solving streaming frames of its own 1920x16 strip -- so the line is
-    the host's aggregate throughput, scaled per pixel to the frame size."""
-    import multiprocessing as mp
+    """The reference arm: the compiled restatement of the reference solver
+    (oracle/ls_oracle.c; the reference package itself is pure Python/NumPy,
+    ~390 s per 1080p streaming frame) on full-size frames of the
+    same workload with every host thread: W warm-up + K timed streaming
+    frames, each a whole frame (no strips, no extrapolation)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     H, W, K = args.height, args.width, args.K
     cores = host_cores()
-    import torch  # noqa: F401  (imported once here, inherited by the forked workers)
-    from oracle import lumisplit_oracle  # noqa: F401
-    from paper_1908_01961_b200 import synth  # noqa: F401
-    jobs = [(H, W, K, args.warmup, args.steps, w) for w in range(cores)]
-    with mp.get_context("fork").Pool(cores) as pool:
-        times = pool.map(_reference_worker, jobs)
-    strips_per_s = cores * args.steps / max(times)          # all cores, slowest worker's clock
-    px_per_s = strips_per_s * STRIP_ROWS * W
-    value = px_per_s / (H * W)
-    sec_per_frame = 1.0 / value
-    sample = (f"{args.steps} streaming frames (segment + aux + 2x2 GN x 16 PCG) of the oracle port on a "
-              f"{W}x{STRIP_ROWS} strip per host core ({cores} processes, one thread each, different "
-              f"synthetic K={K} clips); aggregate pixel throughput scaled to {W}x{H}")
+    cc = CpuClip(H, W, K, 1 + args.warmup + args.steps, seed=0, threads=cores)
+    for i in range(args.warmup):
+        cc.frame(1 + i)
+    times = [cc.frame(1 + args.warmup + i) for i in range(args.steps)]
+    t = sum(times)
+    value = args.steps / t
+    sample = (f"{args.steps} full {W}x{H} K={K} streaming frames (segment + aux + 2x2 GN x 16 PCG, fp64) of "
+              f"the compiled reference restatement (oracle/ls_oracle.c, OpenMP, {cores} threads), after "
+              f"{args.warmup} warm-up frames; same synthetic clip as the GPU arm")
     line = {"metric": metric_for(args), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": sec_per_frame * 1e3, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{W}x{H} K={K} streaming frames (BASELINE configs[2])",
-                       "H": H, "W": W, "K": K, "gn_steps_per_frame": 4, "pcg_iterations": 16},
+                       "H": H, "W": W, "K": K, "gn_steps_per_frame": 4, "pcg_iterations": 16,
+                       "frame_seconds": times},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": sample, "cpu": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -499,22 +471,19 @@ def run_ours(args):
                "api": "pipeline.StreamingDecomposer.step (reference decompose_frames loop); "
                       "frame i+1's H2D and frame i's D2H on copy streams beside frame i's / i+1's solve"}
 
-    # --- CPU baseline (rank 0, N = 1 only) ---
+    # --- CPU baseline (rank 0, N = 1 only): 2 full streaming frames of the
+    #     compiled reference restatement on every host thread, the 2nd timed ---
     cpu = None
     if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.profile_only):
-        guard = limit_threads()
-        cf, ccol, cstate = make_cpu_inputs(H, W, K, STRIP_ROWS, 2)
-        ts = []
-        for i in range(2):
-            dt, cstate = cpu_sample((cf[i], cf[i + 1]), ccol, cstate, STRIP_ROWS, seed=i + 1)
-            ts.append(dt)
-        scale = (H * W) / (STRIP_ROWS * W)
-        cpu_fps = 1.0 / (ts[-1] * scale)
-        cpu = {"value": cpu_fps, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"1 streaming frame (segment + aux + 2x2 GN x 16 PCG) of the oracle port on a "
-                         f"{W}x{STRIP_ROWS} strip, per-pixel time x{scale:.1f} to {W}x{H}",
+        cores = host_cores()
+        cc = CpuClip(H, W, K, 3, seed=0, threads=cores)
+        cc.frame(1)
+        dt = cc.frame(2)
+        cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"1 full {W}x{H} K={K} streaming frame (segment + aux + 2x2 GN x 16 PCG, fp64) of the "
+                         f"compiled reference restatement (oracle/ls_oracle.c, OpenMP over rows, {cores} "
+                         f"threads), after 1 untimed frame",
                "cpu": cpu_model()}
-        del guard
 
     if rank == 0:
         line = {"metric": metric_for(args), "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,

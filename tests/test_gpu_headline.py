@@ -1,0 +1,174 @@
+"""Parity at the headline configuration (BASELINE configs[2]: 1920x1080, K=8)
+and at configs[1] (640x480, K=6): the exact kernel instantiations bench.py
+times (NT = K+1 = 9: k_energy<9,*>, k_pcg_apply<9>, k_pcg_update, the
+CUDA-graph flip-flop) against the compiled CPU restatement of the reference
+(oracle/ls_oracle.c, pinned to the reference's outputs by
+tests/test_oracle_c.py).
+
+Gates (BASELINE.json north_star):
+* operators: per-term energies 1e-5 relative, b / diag(J^T J) 1e-5 and
+  J^T J p 2e-5 relative to the largest entry, PCG(16) 1e-3;
+* GN steps and whole streaming frames, teacher-forced (both sides start
+  from the same previous state, aux and seed): per-layer max-abs <= 1e-3 on
+  R = exp(r), T_0 and every T_k, relative reconstruction energy <= 1e-4.
+"""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import c_oracle as CO
+from oracle import lumisplit_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+LAYER_TOL = 1e-3
+RECON_TOL = 1e-4
+
+
+def _clip(H, W, K, n=2, seed=0):
+    from paper_1908_01961_b200 import synth
+    return synth.make_clip(H, W, K, n, seed=seed, device="cpu")
+
+
+def _host(t):
+    return t.double().cpu().numpy()
+
+
+def recon_energy(image, r, T, colors):
+    """sum (I - exp(r) * T B)^2: the reconstruction energy of SURVEY 8c."""
+    B = O.palette_matrix(colors)
+    return float(np.sum((image - np.exp(r) * (T @ B)) ** 2))
+
+
+def assert_layers_close(image, colors, r_dev, T_dev, r_ref, T_ref, what=""):
+    dR = np.abs(np.exp(r_dev) - np.exp(r_ref)).max(axis=(0, 1))
+    dT = np.abs(T_dev - T_ref).max(axis=(0, 1))
+    assert dR.max() <= LAYER_TOL, (what, "R", dR)
+    assert dT.max() <= LAYER_TOL, (what, "T", dT)
+    ea = recon_energy(image, r_dev, T_dev, colors)
+    eb = recon_energy(image, r_ref, T_ref, colors)
+    assert abs(ea - eb) <= RECON_TOL * eb, (what, ea, eb)
+    return float(dR.max()), float(dT.max())
+
+
+def _streaming_setup(H, W, K, seed):
+    """Frame 0 solved on the device (no refinement, one outer iteration) is
+    the previous frame; frame 1 is the streaming frame under test."""
+    from paper_1908_01961_b200.energy import EnergyWeights
+    from paper_1908_01961_b200.palette import BaseColorPalette
+    from paper_1908_01961_b200.pipeline import StreamingDecomposer
+    from paper_1908_01961_b200.solver import SolveConfig
+    clip = _clip(H, W, K, 2, seed=seed)
+    dec = StreamingDecomposer(BaseColorPalette(colors=clip.colors), EnergyWeights(),
+                              SolveConfig(tol_rel=0.0, refine=False, outer_iterations=1), seed=seed,
+                              streaming_outer=2)
+    s0 = dec.first(clip.frames[0].cuda())
+    torch.cuda.synchronize()
+    return clip, dec, s0
+
+
+def _frame1_state(clip, s0, seed):
+    """Device SolverState of the streaming frame (warm start from s0) plus
+    the matching oracle aux (partners checked bit-exact)."""
+    from paper_1908_01961_b200.energy import EnergyWeights
+    from paper_1908_01961_b200.imaging import Frame, chromaticity
+    from paper_1908_01961_b200.palette import BaseColorPalette, segment
+    from paper_1908_01961_b200.solver import SolveConfig, SolverState, build_aux, initialize
+    frame = Frame(clip.frames[1].cuda())
+    pal = BaseColorPalette(colors=clip.colors)
+    cm = segment(frame, pal)
+    aux = build_aux(frame, cm, seed, prev_chroma=chromaticity(s0.frame), prev_r=s0.layers.r)
+    layers = initialize(frame, cm, pal, previous=s0.layers)
+    st = SolverState(frame=frame, palette=pal, layers=layers, aux=aux, weights=EnergyWeights(),
+                     config=SolveConfig(tol_rel=0.0))
+    img0, img1 = (f.double().numpy() for f in clip.frames)
+    ids = cm.ids.cpu().numpy()
+    assert np.array_equal(ids, CO.segment(img1, clip.colors))
+    oaux = CO.build_aux(img1, ids, seed, CO.chromaticity(img0)[0], _host(s0.layers.r))
+    s = aux.samples
+    assert np.array_equal(s.src.cpu().numpy(), oaux.pairs.src)
+    assert np.array_equal(s.dst.cpu().numpy(), oaux.pairs.dst)
+    assert np.array_equal(s.temporal.cpu().numpy(), oaux.pairs.temporal)
+    return st, img1, oaux
+
+
+def test_headline_1080p_k8_operators_vs_oracle():
+    """Energies, -J^T F, diag(J^T J), J^T J p and PCG(16) of the NT=9 kernels
+    at 1920x1080 with temporal partners."""
+    from paper_1908_01961_b200.energy import assemble_blocks, to_reference_vector
+    clip, dec, s0 = _streaming_setup(1080, 1920, 8, seed=0)
+    st, img1, oaux = _frame1_state(clip, s0, seed=1)
+    r0, T0 = _host(st.layers.r), _host(st.layers.T)
+    sysm = CO.System(img1, clip.colors, oaux, O.Weights())
+    sysm.linearize(r0, T0)
+    blocks = assemble_blocks(st.frame, st.palette, st.layers, st.aux, st.weights)
+    e_dev = blocks.energies()
+    e_ref = sysm.terms(r0, T0)
+    for k in O.TERM_NAMES:
+        assert abs(e_dev[k] - e_ref[k]) <= 1e-5 * max(abs(e_ref[k]), 1e-3 * sum(e_ref.values())), k
+    b_dev, d_dev = blocks.gradient_and_diag()
+    b_ref, d_ref = sysm.grad_diag()
+    b_dev, d_dev = _host(to_reference_vector(b_dev)), _host(to_reference_vector(d_dev))
+    assert np.abs(b_dev - b_ref).max() <= 1e-5 * np.abs(b_ref).max()
+    assert np.abs(d_dev - d_ref).max() <= 1e-5 * np.abs(d_ref).max()
+    g = torch.Generator(device="cuda").manual_seed(7)
+    p = torch.randn(st.layers.X.shape, generator=g, device="cuda", dtype=torch.float32)
+    Ap_dev = _host(to_reference_vector(blocks.apply_normal(p)))
+    Ap_ref = sysm.apply(_host(to_reference_vector(p)))
+    assert np.abs(Ap_dev - Ap_ref).max() <= 2e-5 * np.abs(Ap_ref).max()
+    x_dev, info_dev = blocks.pcg(16)
+    x_ref, info_ref = sysm.pcg(b_ref, d_ref, 16)
+    x_dev = _host(to_reference_vector(x_dev))
+    assert info_dev["iterations"] == info_ref["iterations"] == 16
+    assert np.abs(x_dev - x_ref).max() <= 1e-3 * np.abs(x_ref).max()
+    assert abs(info_dev["final_residual"] - info_ref["final_residual"]) <= 1e-3 * info_ref["initial_residual"]
+
+
+def test_headline_1080p_k8_gn_steps_teacher_forced():
+    """Two streaming GN steps at 1920x1080, K=8, each started from the
+    oracle's previous result (teacher forcing)."""
+    from paper_1908_01961_b200.solver import gn_step_sparse
+    clip, dec, s0 = _streaming_setup(1080, 1920, 8, seed=0)
+    st, img1, oaux = _frame1_state(clip, s0, seed=1)
+    sysm = CO.System(img1, clip.colors, oaux, O.Weights())
+    for step in range(2):
+        r0, T0 = _host(st.layers.r), _host(st.layers.T)
+        ost = O.State(image=img1, colors=np.asarray(clip.colors, dtype=np.float64), r=r0, T=T0, aux=oaux,
+                      weights=O.Weights(), config=O.Config(tol_rel=0.0))
+        orec = CO.gn_step_sparse(ost, sysm)
+        rec = gn_step_sparse(st)
+        assert rec["accepted"] == orec["accepted"] and rec["alpha"] == orec["alpha"]
+        assert rec["pcg"]["iterations"] == orec["pcg"]["iterations"]
+        assert np.isclose(rec["energy_before"], orec["energy_before"], rtol=1e-5)
+        assert np.isclose(rec["energy_after"], orec["energy_after"], rtol=1e-4)
+        assert_layers_close(img1, clip.colors, _host(st.layers.r), _host(st.layers.T), ost.r, ost.T,
+                            f"GN step {step}")
+        st.layers.X.copy_(torch.as_tensor(np.concatenate([ost.r.transpose(2, 0, 1), ost.T.transpose(2, 0, 1)]),
+                                          dtype=torch.float32, device="cuda"))
+
+
+@pytest.mark.parametrize("H,W,K", [(480, 640, 6), (1080, 1920, 8)])
+def test_streaming_frame_teacher_forced_through_product_path(H, W, K):
+    """One whole streaming frame (segment, aux, warm start, 2 outer x 2 GN x
+    16 PCG) through StreamingDecomposer.step -- the CUDA-graph flip-flop the
+    bench times -- against the oracle's streaming frame from the same
+    previous state (configs[1] and configs[2])."""
+    clip, dec, s0 = _streaming_setup(H, W, K, seed=2)
+    prev = O.State(image=None, colors=clip.colors, r=_host(s0.layers.r), T=_host(s0.layers.T), aux=None,
+                   weights=None, config=None)
+    img0, img1 = (f.double().numpy() for f in clip.frames)
+    st = dec.step(clip.frames[1].cuda())
+    torch.cuda.synchronize()
+    cfg = replace(O.Config(tol_rel=0.0), outer_iterations=2)
+    ost = CO.stream_frame(img1, clip.colors, prev, img0, O.Weights(), cfg, 2 + 1)
+    assert np.array_equal(st.cluster_map.ids.cpu().numpy(), CO.segment(img1, clip.colors))
+    assert len(st.records) == len(ost.records) == 4
+    for a, b in zip(st.records, ost.records):
+        assert a["accepted"] == b["accepted"] and a["alpha"] == b["alpha"]
+        assert a["pcg"]["iterations"] == b["pcg"]["iterations"]
+        assert np.isclose(a["energy_after"], b["energy_after"], rtol=1e-4)
+    assert st.status == ost.status
+    assert_layers_close(img1, clip.colors, _host(st.layers.r), _host(st.layers.T), ost.r, ost.T,
+                        f"{W}x{H} K={K} streaming frame")
