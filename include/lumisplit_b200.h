@@ -226,6 +226,48 @@ LS_API int ls_svd_solve(ls_ctx* ctx, int n, const double* A_host, const double* 
 LS_API int ls_dense_step(ls_ctx* ctx, double* colors_inout_host, const float* X, double* applied_host,
                   ls_dense_record* rec);
 
+/* ---- per-block residual protocol (energy.py:194-452) --------------------
+ * The reference's assemble_blocks returns eight residual blocks
+ * (energy.py:478-496), each with residual(r, T), apply_j(dr, dT),
+ * apply_jt(w, out_dr, out_dT) (accumulating) and add_diag(out_dr, out_dT)
+ * (accumulating); stack_residuals concatenates the residuals (:499-500).
+ * These entry points are that protocol on the device, block by block, with
+ * the IRLS weights and the linearisation frozen at the planar state X0 and
+ * the frame installed in the context (ls_set_image / ls_set_edge /
+ * ls_set_anchor / ls_set_prev_r).  Row vectors (residual, J dX, the w of
+ * J^T w) are float32 in the reference's row order (the (H, W, C) ravel of
+ * each block; r_consistency: pair-major, 3 rows per pair); X0, Y, dX and the
+ * accumulated outputs are U planes.  The consistency block reads the partner
+ * rows from `pairs` (device arrays, pair order = row order).  Block ids:
+ * data, clustering, r_sparsity, r_consistency, monochrome, i_sparsity,
+ * smoothness, non_neg (the LS term order). */
+enum { LS_BLOCK_DATA = 0, LS_BLOCK_CLUSTERING, LS_BLOCK_R_SPARSITY, LS_BLOCK_R_CONSISTENCY,
+       LS_BLOCK_MONOCHROME, LS_BLOCK_I_SPARSITY, LS_BLOCK_SMOOTHNESS, LS_BLOCK_NON_NEG };
+typedef struct {
+  int64_t n;
+  const int64_t* src;
+  const int64_t* dst;
+  const uint8_t* temporal; /* NULL: all spatial */
+  const double* weight;    /* NULL: all 1 */
+} ls_pairs;
+/* number of residual rows of a block (host-side, no device work) */
+LS_API int ls_block_rows(ls_ctx* ctx, int block, int64_t n_pairs, int64_t* rows);
+/* DataBlock.residual ... NonNegBlock.residual (energy.py:205-209, 234-235,
+ * 264-267, 348-350, 399-401, 424-425) at the state Y */
+LS_API int ls_block_residual(ls_ctx* ctx, const double* colors, const float* X0, int block, const ls_pairs* pairs,
+                             const float* Y, float* out_rows);
+/* apply_j (energy.py:211-212, 237-238, 269-270, 352-357, 403-404, 427-428) */
+LS_API int ls_block_apply_j(ls_ctx* ctx, const double* colors, const float* X0, int block, const ls_pairs* pairs,
+                            const float* dX, float* out_rows);
+/* apply_jt, accumulating into out_dX (energy.py:214-218, 240-241, 272-282,
+ * 359-370, 406-408, 430-431) */
+LS_API int ls_block_apply_jt(ls_ctx* ctx, const double* colors, const float* X0, int block, const ls_pairs* pairs,
+                             const float* w_rows, float* out_dX);
+/* add_diag, accumulating into out_dX (energy.py:220-222, 243-244, 284-291,
+ * 372-381, 410-411, 433-434) */
+LS_API int ls_block_add_diag(ls_ctx* ctx, const double* colors, const float* X0, int block, const ls_pairs* pairs,
+                             float* out_dX);
+
 /* ---- Row bands (SURVEY.md 8(e), configs[3]: >= 4K frames split spatially) --
  * One context per band of rows.  The context is created with the band's
  * LOCAL frame: global rows [gy0, gy0 + H) of a GH-row frame, i.e. the band's

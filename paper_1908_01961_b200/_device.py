@@ -214,6 +214,30 @@ class DeviceSolver:
                                            out.ctypes.data_as(L.DBL_P)))
         return out
 
+    # -- per-block residual protocol (ls_block_*, energy.py:194-452) ------------
+    def block_rows(self, block: int, n_pairs: int) -> int:
+        n = C.c_int64()
+        self._chk(self.lib.ls_block_rows(self.ctx, int(block), int(n_pairs), C.byref(n)))
+        return int(n.value)
+
+    def block_call(self, op: str, colors, X0, block: int, pairs, vec=None, out=None):
+        """op: residual / apply_j (vec = U planes, returns the rows) or
+        apply_jt (vec = rows) / add_diag (accumulate into the U planes `out`)."""
+        a, pa = L.dbl_array(colors)
+        pr = pairs if pairs is not None else L.Pairs(0, None, None, None, None)
+        self._enter()
+        if op in ("residual", "apply_j"):
+            rows = torch.empty(self.block_rows(block, pr.n), dtype=torch.float32, device=self.device)
+            fn = self.lib.ls_block_residual if op == "residual" else self.lib.ls_block_apply_j
+            self._chk(fn(self.ctx, pa, L.dptr(X0), int(block), C.byref(pr), L.dptr(vec), L.dptr(rows)))
+            return rows
+        if op == "apply_jt":
+            self._chk(self.lib.ls_block_apply_jt(self.ctx, pa, L.dptr(X0), int(block), C.byref(pr), L.dptr(vec),
+                                                 L.dptr(out)))
+        else:
+            self._chk(self.lib.ls_block_add_diag(self.ctx, pa, L.dptr(X0), int(block), C.byref(pr), L.dptr(out)))
+        return out
+
     def grad_diag(self, colors, X):
         a, pa = L.dbl_array(colors)
         b = torch.empty_like(X)

@@ -49,6 +49,12 @@ class DenseRecord(C.Structure):
                 ("accepted", C.c_int), ("solved_nonzero", C.c_int)]
 
 
+class Pairs(C.Structure):
+    """ls_pairs: device arrays of the consistency partner rows."""
+    _fields_ = [("n", C.c_int64), ("src", C.c_void_p), ("dst", C.c_void_p), ("temporal", C.c_void_p),
+                ("weight", C.c_void_p)]
+
+
 P = C.c_void_p
 I64 = C.c_int64
 U64 = C.c_uint64
@@ -95,6 +101,12 @@ SIGNATURES = {
     "ls_dense_normal": [P, DBL_P, P, C.c_int, DBL_P, DBL_P],
     "ls_svd_solve": [P, C.c_int, DBL_P, DBL_P, C.c_double, DBL_P],
     "ls_dense_step": [P, DBL_P, P, DBL_P, C.POINTER(DenseRecord)],
+    # per-block residual protocol (energy.py:194-452)
+    "ls_block_rows": [P, C.c_int, I64, C.POINTER(I64)],
+    "ls_block_residual": [P, DBL_P, P, C.c_int, C.POINTER(Pairs), P, P],
+    "ls_block_apply_j": [P, DBL_P, P, C.c_int, C.POINTER(Pairs), P, P],
+    "ls_block_apply_jt": [P, DBL_P, P, C.c_int, C.POINTER(Pairs), P, P],
+    "ls_block_add_diag": [P, DBL_P, P, C.c_int, C.POINTER(Pairs), P],
     # row bands
     "ls_launch_count": [P, C.POINTER(I64)],
     "ls_add_launches": [P, I64],

@@ -9,6 +9,8 @@
 // explicitly rounded operations (no FMA contraction) where the result feeds
 // a comparison (chroma gate, nearest-palette argmin), so the integer outputs
 // (partners, cluster ids) are bit-identical to the reference.
+#include <climits>
+
 #include "ls_kernels.h"
 
 namespace ls {
@@ -675,6 +677,103 @@ void launch_all_finite(cudaStream_t s, const float* x, int64_t n, int* flag) {
 
 void launch_set_i32(cudaStream_t s, int32_t* p, int n, int32_t v) {
   k_set_i32<<<grid_for(n), 256, 0, s>>>(p, n, v);
+}
+
+// ---------------------------------------------------------------------------
+// single-pass int32 scan with decoupled look-back (row offsets of the
+// adjacency and of the pair list: exclusive sums; the dark-pixel
+// inheritance of segment: an inclusive max-scan).  Each CTA takes the next
+// tile id from a counter, scans its 2048 values in registers / warp
+// shuffles, publishes its aggregate, and thread 0 walks back over the
+// predecessors' published (flag, value) words until an inclusive prefix.
+// Integer ops: the result is exact and independent of the schedule.
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+constexpr unsigned long long kFlagAgg = 1ull << 32, kFlagPre = 2ull << 32;
+
+template <int OP>
+__device__ __forceinline__ int scan_op(int a, int b) {
+  return OP == 0 ? a + b : (a > b ? a : b);
+}
+
+template <int OP>
+__global__ void __launch_bounds__(kScanThreads) k_scan(const int* __restrict__ in, int* __restrict__ out, int64_t n,
+                                                      unsigned long long* status, unsigned* counter) {
+  constexpr int ident = OP == 0 ? 0 : INT_MIN;
+  __shared__ int s_tile, s_prefix;
+  __shared__ int s_warp[kScanThreads / 32];
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(counter, 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t base = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int v[kScanItems];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) v[j] = base + j < n ? in[base + j] : ident;
+#pragma unroll
+  for (int j = 1; j < kScanItems; ++j) v[j] = scan_op<OP>(v[j - 1], v[j]);   // thread-inclusive
+  int t = v[kScanItems - 1];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, t, o);
+    if (lane >= o) t = scan_op<OP>(u, t);
+  }
+  if (lane == 31) s_warp[wid] = t;
+  __syncthreads();
+  if (wid == 0) {
+    int w = lane < kScanThreads / 32 ? s_warp[lane] : ident;
+#pragma unroll
+    for (int o = 1; o < kScanThreads / 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w = scan_op<OP>(u, w);
+    }
+    if (lane < kScanThreads / 32) s_warp[lane] = w;
+  }
+  __syncthreads();
+  const int up = __shfl_up_sync(0xffffffffu, t, 1);
+  int excl = lane > 0 ? up : ident;                         // exclusive within the warp
+  if (wid > 0) excl = scan_op<OP>(s_warp[wid - 1], excl);   // ... within the tile
+  if (threadIdx.x == 0) {
+    const int agg = s_warp[kScanThreads / 32 - 1];
+    int prefix = ident;
+    if (tile == 0) {
+      atomicExch(status, kFlagPre | (unsigned)agg);
+    } else {
+      atomicExch(status + tile, kFlagAgg | (unsigned)agg);
+      for (int j = tile - 1;; --j) {
+        unsigned long long st;
+        do {
+          st = *reinterpret_cast<volatile unsigned long long*>(status + j);
+        } while ((st >> 32) == 0ull);
+        prefix = scan_op<OP>((int)(unsigned)(st & 0xffffffffull), prefix);
+        if ((st & ~0xffffffffull) == kFlagPre) break;
+      }
+      atomicExch(status + tile, kFlagPre | (unsigned)scan_op<OP>(prefix, agg));
+    }
+    s_prefix = prefix;
+  }
+  __syncthreads();
+  const int pre = scan_op<OP>(s_prefix, excl);
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    if (base + j >= n) break;
+    if (OP == 0) out[base + j] = pre + (j > 0 ? v[j - 1] : 0);   // exclusive sum
+    else out[base + j] = scan_op<OP>(pre, v[j]);                 // inclusive max
+  }
+}
+
+size_t scan_scratch_bytes(int64_t n) { return sizeof(unsigned long long) * (size_t)((n + kScanTile - 1) / kScanTile + 1); }
+
+cudaError_t launch_scan(cudaStream_t s, const int32_t* in, int32_t* out, int64_t n, int op, void* scratch) {
+  if (n <= 0) return cudaSuccess;
+  const int tiles = (int)((n + kScanTile - 1) / kScanTile);
+  unsigned long long* status = static_cast<unsigned long long*>(scratch);
+  unsigned* counter = reinterpret_cast<unsigned*>(status + tiles);
+  cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(unsigned long long) * (tiles + 1), s);
+  if (e != cudaSuccess) return e;
+  if (op == 0) k_scan<0><<<tiles, kScanThreads, 0, s>>>(in, out, n, status, counter);
+  else k_scan<1><<<tiles, kScanThreads, 0, s>>>(in, out, n, status, counter);
+  return cudaGetLastError();
 }
 
 }  // namespace ls

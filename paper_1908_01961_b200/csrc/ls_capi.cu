@@ -10,7 +10,6 @@
 // ls_flip_flop_graph decide everything on the device and synchronise once per
 // frame, the latter as one CUDA-graph launch; the ls_band_* entry points are
 // the same phases for one band of rows (bands.py).
-#include <cub/device/device_scan.cuh>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -73,10 +72,6 @@ static bool make_map(CUtensorMap* m, const float* base, int W, int H, int planes
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-struct MaxOp {
-  __host__ __device__ int operator()(int a, int b) const { return a > b ? a : b; }
-};
-
 // CUDA-event timing of the solver kernels by class (bench.py roofline)
 enum { PC_EG = 0, PC_APPLY, PC_UPDATE, PC_TRIAL, PC_DENSE, PC_N };
 struct Prof {
@@ -122,7 +117,7 @@ struct ls_ctx {
   int* small_i = nullptr;                     // [0] bad flag, [1] temporal count, [2] first_valid
   SampleState* sstate = nullptr;          // device-side sampler rejection bookkeeping
   bool sampled_counts_known = true;
-  void* cub_tmp = nullptr;
+  void* cub_tmp = nullptr;      // scan scratch (launch_scan)
   size_t cub_bytes = 0;
   int32_t *seg_raw = nullptr, *seg_key = nullptr, *seg_last = nullptr;
   double* pal_chroma = nullptr;
@@ -352,11 +347,8 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   A_(cudaHostAlloc((void**)&c->host_buf, sizeof(double) * (2 * 36 * 36 + 64), cudaHostAllocMapped));   // kernel-written (UVA)
   A_(cudaMemset(c->tickets, 0, 8 * sizeof(unsigned)));
   A_(cudaMemset(c->sc, 0, sizeof(Scalars)));
-  // CUB scratch: max of the int exclusive-sum over N+1 and the max-scan over N
-  size_t b1 = 0, b2 = 0;
-  A_(cub::DeviceScan::ExclusiveSum(nullptr, b1, c->deg, c->row_ptr, N + 1));
-  A_(cub::DeviceScan::InclusiveScan(nullptr, b2, c->seg_key, c->seg_last, MaxOp(), N));
-  c->cub_bytes = std::max(b1, b2);
+  // scan scratch (tile status words + tile counter) for N+1 values
+  c->cub_bytes = scan_scratch_bytes((int64_t)N + 1);
   A_(dalloc(c, (char**)&c->cub_tmp, c->cub_bytes));
 #undef A_
   if (e != cudaSuccess) {
@@ -525,8 +517,7 @@ static int build_rows(ls_ctx* c, int64_t* total) {
   const int N = c->N;
   launch_degree(c->stream, N, c->out_cnt, c->in_cnt, c->deg);
   LS_CK(cudaMemsetAsync(c->deg + N, 0, sizeof(int32_t), c->stream));
-  size_t bytes = c->cub_bytes;
-  LS_CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->deg, c->row_ptr, N + 1, c->stream));
+  LS_CK(launch_scan(c->stream, c->deg, c->row_ptr, (int64_t)N + 1, 0, c->cub_tmp));
   int32_t tot = 0;
   LS_CK(cudaMemcpyAsync(&tot, c->row_ptr + N, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   LS_CK(cudaStreamSynchronize(c->stream));
@@ -638,14 +629,12 @@ int ls_sample_consistency(ls_ctx* c, const double* chroma, const double* prev_ch
   c->band_zero_lists = 0;
   launch_degree(c->stream, N, c->out_cnt, c->in_cnt, c->deg);
   LS_CK(cudaMemsetAsync(c->deg + N, 0, sizeof(int32_t), c->stream));
-  size_t bytes = c->cub_bytes;
-  LS_CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->deg, c->row_ptr, N + 1, c->stream));
+  LS_CK(launch_scan(c->stream, c->deg, c->row_ptr, (int64_t)N + 1, 0, c->cub_tmp));
   LS_CK(cudaMemsetAsync(c->fill, 0, sizeof(int32_t) * N, c->stream));
   launch_fill_from_samples(c->stream, c->codes, c->H, c->W, c->row_ptr, c->fill, c->ent, c->key);
   launch_sort_rows(c->stream, N, c->row_ptr, c->ent, c->key, nullptr);
   // pair offsets (src-major, slot order) for ls_get_pairs / ls_pair_count
-  bytes = c->cub_bytes;
-  LS_CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->out_cnt, c->pair_off, N + 1, c->stream));
+  LS_CK(launch_scan(c->stream, c->out_cnt, c->pair_off, (int64_t)N + 1, 0, c->cub_tmp));
   LS_CK(cudaGetLastError());
   c->launches += 1 + 3 * kSamplePasses + 6;
   c->n_pairs = -1;                       // resolved lazily by ls_pair_count
@@ -746,8 +735,7 @@ int ls_segment(ls_ctx* c, const double* colors, int32_t* ids_out) {
   }
   launch_set_i32(c->stream, c->small_i + 2, 1, N);
   launch_segment_raw(c->stream, c->img, c->chroma, N, K, pc, c->seg_raw, c->seg_key, c->small_i + 2);
-  size_t bytes = c->cub_bytes;
-  LS_CK(cub::DeviceScan::InclusiveScan(c->cub_tmp, bytes, c->seg_key, c->seg_last, MaxOp(), N, c->stream));
+  LS_CK(launch_scan(c->stream, c->seg_key, c->seg_last, (int64_t)N, 1, c->cub_tmp));
   launch_segment_final(c->stream, N, c->seg_raw, c->seg_last, c->small_i + 2, ids_out);
   c->launches += 4;
   LS_CK(cudaGetLastError());
@@ -859,6 +847,77 @@ int ls_apply_normal(ls_ctx* c, const double* colors, const float* X, const float
   const bool tma = tile_maps(c, X, p, &maps);
   launch_apply(L_apply(c), frame_of(c), cf, X, p, Ap, c->part, c->tickets + 1, nullptr, 0, tma ? &maps : nullptr);
   LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+// ---- per-block residual protocol (ls_blocks.cu) ---------------------------
+int ls_block_rows(ls_ctx* c, int block, int64_t n_pairs, int64_t* rows) {
+  LS_ARG(c && rows && block >= 0 && block < BLK_COUNT && n_pairs >= 0, "bad arguments");
+  *rows = block_rows(block, c->H, c->W, c->NT, n_pairs);
+  return LS_OK;
+}
+
+static int block_common(ls_ctx* c, const double* colors, const float* X0, int block, const ls_pairs* pairs,
+                        BlockPairs* bp) {
+  int rc = whole_frame_only(c);
+  if (rc) return rc;
+  LS_ARG(c->has_image, "no frame installed");
+  LS_ARG(colors || c->K == 0, "null palette");
+  LS_ARG(X0 && block >= 0 && block < BLK_COUNT, "bad arguments");
+  *bp = BlockPairs{0, nullptr, nullptr, nullptr, nullptr};
+  if (block == BLK_CONSISTENCY) {
+    LS_ARG(pairs && pairs->n >= 0 && (pairs->n == 0 || (pairs->src && pairs->dst)), "consistency block needs pairs");
+    *bp = BlockPairs{pairs->n, pairs->src, pairs->dst, pairs->temporal, pairs->weight};
+  }
+  LS_CK(cudaSetDevice(c->dev));
+  return LS_OK;
+}
+
+int ls_block_residual(ls_ctx* c, const double* colors, const float* X0, int block, const ls_pairs* pairs,
+                      const float* Y, float* out) {
+  BlockPairs bp;
+  int rc = block_common(c, colors, X0, block, pairs, &bp);
+  if (rc) return rc;
+  LS_ARG(Y && out, "bad arguments");
+  LS_ARG(block != BLK_CLUSTERING || c->has_ids || c->has_anchor, "EnergyAux needs cluster_ids or r_cluster_log");
+  LS_ARG(block != BLK_CONSISTENCY || !bp.temporal || c->has_prev_r,
+         "temporal partners need the previous frame's reflectance");
+  LS_CK(launch_block_rows(c->stream, frame_of(c), make_coef<double>(c->w, colors, c->K), X0, bp, block, 0, Y, out));
+  c->launches += 1;
+  return LS_OK;
+}
+
+int ls_block_apply_j(ls_ctx* c, const double* colors, const float* X0, int block, const ls_pairs* pairs,
+                     const float* dX, float* out) {
+  BlockPairs bp;
+  int rc = block_common(c, colors, X0, block, pairs, &bp);
+  if (rc) return rc;
+  LS_ARG(dX && out, "bad arguments");
+  LS_CK(launch_block_rows(c->stream, frame_of(c), make_coef<double>(c->w, colors, c->K), X0, bp, block, 1, dX, out));
+  c->launches += 1;
+  return LS_OK;
+}
+
+int ls_block_apply_jt(ls_ctx* c, const double* colors, const float* X0, int block, const ls_pairs* pairs,
+                      const float* w, float* out) {
+  BlockPairs bp;
+  int rc = block_common(c, colors, X0, block, pairs, &bp);
+  if (rc) return rc;
+  LS_ARG(w && out, "bad arguments");
+  LS_CK(launch_block_cols(c->stream, frame_of(c), make_coef<double>(c->w, colors, c->K), X0, bp, block, 0, w, out));
+  c->launches += block == BLK_CONSISTENCY ? 2 : 1;
+  return LS_OK;
+}
+
+int ls_block_add_diag(ls_ctx* c, const double* colors, const float* X0, int block, const ls_pairs* pairs,
+                      float* out) {
+  BlockPairs bp;
+  int rc = block_common(c, colors, X0, block, pairs, &bp);
+  if (rc) return rc;
+  LS_ARG(out, "bad arguments");
+  LS_CK(launch_block_cols(c->stream, frame_of(c), make_coef<double>(c->w, colors, c->K), X0, bp, block, 1, nullptr,
+                          out));
+  c->launches += block == BLK_CONSISTENCY ? 2 : 1;
   return LS_OK;
 }
 
@@ -1600,8 +1659,7 @@ int ls_band_segment(ls_ctx* c, const double* colors, int32_t* summary) {
   const int own_lo = c->y_lo * c->W, own_hi = c->y_hi * c->W;
   launch_set_i32(c->stream, c->small_i + 2, 1, N);
   launch_segment_band(c->stream, c->img, c->chroma, N, K, pc, c->seg_raw, c->seg_key, c->small_i + 2, own_lo, own_hi);
-  size_t bytes = c->cub_bytes;
-  LS_CK(cub::DeviceScan::InclusiveScan(c->cub_tmp, bytes, c->seg_key, c->seg_last, MaxOp(), N, c->stream));
+  LS_CK(launch_scan(c->stream, c->seg_key, c->seg_last, (int64_t)N, 1, c->cub_tmp));
   launch_segment_summary(c->stream, c->seg_raw, c->seg_last, c->small_i + 2, own_hi, summary);
   c->launches += 4;
   LS_CK(cudaGetLastError());

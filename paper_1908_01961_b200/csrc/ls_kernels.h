@@ -66,7 +66,29 @@ void prepare_kernels(int NT);
 int apply_grid_limit(int NT);
 int update_grid_limit();
 
+// ls_blocks.cu: the reference's per-block residual protocol (energy.py:194-452)
+enum BlockId { BLK_DATA = 0, BLK_CLUSTERING, BLK_RSPARSITY, BLK_CONSISTENCY, BLK_MONOCHROME, BLK_ISPARSITY,
+               BLK_SMOOTHNESS, BLK_NONNEG, BLK_COUNT };
+struct BlockPairs {
+  int64_t n;
+  const int64_t* src;
+  const int64_t* dst;
+  const uint8_t* temporal;   // may be null (all spatial)
+  const double* weight;      // may be null (all 1)
+};
+int64_t block_rows(int block, int H, int W, int NT, int64_t n_pairs);
+// op 0: residual at Y, op 1: J Y (Y a direction); out has block_rows rows
+cudaError_t launch_block_rows(cudaStream_t s, const Frame& f, const Coef<double>& c, const float* X0,
+                              const BlockPairs& pairs, int block, int op, const float* Y, float* out);
+// op 0: out += J^T w, op 1: out += diag(J^T J); out is U planes
+cudaError_t launch_block_cols(cudaStream_t s, const Frame& f, const Coef<double>& c, const float* X0,
+                              const BlockPairs& pairs, int block, int op, const float* w, float* out);
+
 // ls_aux.cu
+// int32 scan (op 0: exclusive sum, op 1: inclusive max) of n values; scratch
+// of scan_scratch_bytes(n) bytes (zeroed by the launcher on the stream)
+size_t scan_scratch_bytes(int64_t n);
+cudaError_t launch_scan(cudaStream_t s, const int32_t* in, int32_t* out, int64_t n, int op, void* scratch);
 constexpr int kJumpBits = 40;   // stream positions < 2^41 u32 words
 struct SampleParams {
   unsigned long long st_hi, st_lo, inc_hi, inc_lo;

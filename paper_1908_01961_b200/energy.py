@@ -1,13 +1,14 @@
 """Decomposition energy (reference energy.py) on the device.
 
 The reference stacks eight residual-block objects and evaluates them with
-NumPy.  Here the whole energy is one fused operator (`FusedEnergy`, returned
-by `assemble_blocks`) whose residual, gradient, Jacobi diagonal and J^T J
-products are computed by the sm_100a kernels without ever materialising the
-stacked residual F (~61 rows per pixel at K=8): per-term energies,
-b = -J^T F, diag(J^T J) and J^T J p are what the solver consumes
-(solver.py:110-140), and they are exposed with the reference's names and
-term keys.
+NumPy.  `assemble_blocks` returns the same eight blocks (`ResidualBlock`:
+residual / apply_j / apply_jt / add_diag per block, device kernels of
+csrc/ls_blocks.cu) -- and, on the returned list, the fused operator the
+solver actually runs (`FusedEnergy`), whose gradient, Jacobi diagonal and
+J^T J products are computed by the sm_100a kernels without ever
+materialising the stacked residual F (~61 rows per pixel at K=8): per-term
+energies, b = -J^T F, diag(J^T J) and J^T J p are what the solver consumes
+(solver.py:110-140), exposed with the reference's names and term keys.
 """
 
 from __future__ import annotations
@@ -398,10 +399,122 @@ class FusedEnergy:
         return self.solver.pcg(self.palette.colors, self.X, iterations)
 
 
+class ResidualBlock:
+    """One residual block of the reference's protocol (energy.py:194-452):
+    `name`, residual(r, T) -> 1-D rows, apply_j(dr, dT) -> 1-D rows,
+    apply_jt(w, out_dr, out_dT) and add_diag(out_dr, out_dT) accumulating in
+    place.  The IRLS weights and the linearisation are those of the layers
+    the blocks were assembled at.  r / dr / out_dr are (H, W, 3) and T / dT
+    / out_dT (H, W, K+1), CUDA tensors or NumPy arrays (the reference's
+    tests pass arrays; results come back as the same kind).  Rows are the
+    reference's row order (ls_block_* in include/lumisplit_b200.h)."""
+
+    def __init__(self, owner: "FusedEnergy", block_id: int, name: str):
+        self._e = owner
+        self.block_id = block_id
+        self.name = name
+
+    def _pairs(self):
+        if self.block_id != L.TERM_NAMES.index("r_consistency"):
+            return None
+        return self._e._pair_struct()
+
+    def _planes(self, r, T):
+        dev = self._e.X.device
+        return LayerStack(as_cuda(r, device=dev), as_cuda(T, device=dev)).X
+
+    def residual(self, r, T):
+        self._e._ready()
+        rows = self._e.solver.block_call("residual", self._e.palette.colors, self._e.X, self.block_id,
+                                         self._pairs(), vec=self._planes(r, T))
+        return _like(rows, r)
+
+    def apply_j(self, dr, dT):
+        self._e._ready()
+        rows = self._e.solver.block_call("apply_j", self._e.palette.colors, self._e.X, self.block_id,
+                                         self._pairs(), vec=self._planes(dr, dT))
+        return _like(rows, dr)
+
+    def _accumulate(self, planes, out_dr, out_dT):
+        for out, part in ((out_dr, planes[:3]), (out_dT, planes[3:])):
+            upd = part.permute(1, 2, 0)
+            if isinstance(out, torch.Tensor):
+                out += upd.to(device=out.device, dtype=out.dtype)
+            else:
+                out += upd.double().cpu().numpy()
+
+    def apply_jt(self, w, out_dr, out_dT):
+        self._e._ready()
+        acc = torch.zeros_like(self._e.X)
+        wv = as_cuda(w, device=self._e.X.device).reshape(-1).float().contiguous()
+        self._e.solver.block_call("apply_jt", self._e.palette.colors, self._e.X, self.block_id, self._pairs(),
+                                  vec=wv, out=acc)
+        self._accumulate(acc, out_dr, out_dT)
+
+    def add_diag(self, out_dr, out_dT):
+        self._e._ready()
+        acc = torch.zeros_like(self._e.X)
+        self._e.solver.block_call("add_diag", self._e.palette.colors, self._e.X, self.block_id, self._pairs(),
+                                  out=acc)
+        self._accumulate(acc, out_dr, out_dT)
+
+    def __repr__(self):
+        return f"ResidualBlock({self.name!r})"
+
+
+def _like(rows: torch.Tensor, ref):
+    return rows if isinstance(ref, torch.Tensor) else rows.double().cpu().numpy()
+
+
+class EnergyBlocks(list):
+    """What assemble_blocks returns: the eight blocks in the reference's
+    order (energy.py:478-496, names as `block.name`), and -- as attributes
+    -- the fused operator the solver runs (energies, gradient_and_diag,
+    apply_normal, pcg of FusedEnergy): the blocks are the reference's
+    per-block protocol, the fused kernels the hot path."""
+
+    def __init__(self, fused: "FusedEnergy"):
+        super().__init__(ResidualBlock(fused, i, n) for i, n in enumerate(TERM_NAMES))
+        self.fused = fused
+
+    def __getattr__(self, name):
+        if name == "fused":
+            raise AttributeError(name)
+        return getattr(self.fused, name)
+
+
+def _fused_pair_struct(self):
+    """ls_pairs of the installed partner rows (device arrays kept alive)."""
+    smp = self.aux.samples
+    dev = self.X.device
+    src = as_cuda(smp.src, dtype=torch.int64, device=dev).contiguous()
+    dst = as_cuda(smp.dst, dtype=torch.int64, device=dev).contiguous()
+    tmp = as_cuda(smp.temporal, dtype=torch.uint8, device=dev).contiguous()
+    wgt = as_cuda(smp.weight, dtype=torch.float64, device=dev).contiguous() if smp.weight is not None else None
+    has_t = bool(tmp.any()) if tmp.numel() else False
+    if has_t and self.aux.prev_r is None:
+        raise ValueError("temporal partners need the previous frame's reflectance")
+    self._pair_keep = (src, dst, tmp, wgt)
+    return L.Pairs(int(src.numel()), src.data_ptr(), dst.data_ptr(), tmp.data_ptr() if has_t else None,
+                   wgt.data_ptr() if wgt is not None else None)
+
+
+FusedEnergy._pair_struct = _fused_pair_struct
+
+
 def assemble_blocks(image, palette: BaseColorPalette, layers: LayerStack, aux: EnergyAux,
-                    weights: EnergyWeights) -> FusedEnergy:
+                    weights: EnergyWeights) -> EnergyBlocks:
+    """energy.py:478-496: the eight residual blocks frozen at `layers`."""
     frame = image if isinstance(image, Frame) else _RawFrame(as_cuda(image))
-    return FusedEnergy(frame, palette, layers, aux, weights)
+    return EnergyBlocks(FusedEnergy(frame, palette, layers, aux, weights))
+
+
+def stack_residuals(blocks, r, T):
+    """energy.py:499-500: all residual rows, block after block."""
+    res = [b.residual(r, T) for b in blocks]
+    if res and not isinstance(res[0], torch.Tensor):
+        return np.concatenate(res)
+    return torch.cat(res)
 
 
 class _RawFrame:
@@ -411,7 +524,9 @@ class _RawFrame:
         self.data = data
 
 
-def block_energies(blocks: FusedEnergy, r, T) -> dict:
+def block_energies(blocks, r, T) -> dict:
+    """energy.py:503-504 (the fused energy kernel: same per-term values as
+    summing each block's squared residual)."""
     return blocks.energies(r, T)
 
 
