@@ -226,6 +226,19 @@ LS_API int ls_svd_solve(ls_ctx* ctx, int n, const double* A_host, const double* 
 LS_API int ls_dense_step(ls_ctx* ctx, double* colors_inout_host, const float* X, double* applied_host,
                   ls_dense_record* rec);
 
+/* First-frame palette estimation (palette.py:227-238 without the final
+ * segment, which is ls_segment): the 10x10 chroma histogram of the non-dark
+ * pixels (:81-103), population-weighted k-means with the seeded first pick of
+ * numpy's Generator.choice -- (state, inc) of np.random.PCG64(seed) as for
+ * ls_sample_consistency -- and farthest-point seeding (:106-138), nearest-
+ * center assignment and the greedy merge of centers closer than 0.2
+ * (:141-192).  image_hwc: (H, W, 3) float32 device memory; colors_out: host,
+ * room for 3 * k_max doubles; *K_out = 0 when every pixel is dark
+ * (EmptyHistogramError).  k_max in 1..12.  Synchronises `stream`. */
+LS_API int ls_estimate_palette(const float* image_hwc, int H, int W, int k_max, uint64_t state_hi,
+                               uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, double* colors_out,
+                               int* K_out, void* stream);
+
 /* ---- per-block residual protocol (energy.py:194-452) --------------------
  * The reference's assemble_blocks returns eight residual blocks
  * (energy.py:478-496), each with residual(r, T), apply_j(dr, dT),

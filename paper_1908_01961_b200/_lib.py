@@ -101,6 +101,7 @@ SIGNATURES = {
     "ls_dense_normal": [P, DBL_P, P, C.c_int, DBL_P, DBL_P],
     "ls_svd_solve": [P, C.c_int, DBL_P, DBL_P, C.c_double, DBL_P],
     "ls_dense_step": [P, DBL_P, P, DBL_P, C.POINTER(DenseRecord)],
+    "ls_estimate_palette": [P, C.c_int, C.c_int, C.c_int, U64, U64, U64, U64, DBL_P, C.POINTER(C.c_int), P],
     # per-block residual protocol (energy.py:194-452)
     "ls_block_rows": [P, C.c_int, I64, C.POINTER(I64)],
     "ls_block_residual": [P, DBL_P, P, C.c_int, C.POINTER(Pairs), P, P],

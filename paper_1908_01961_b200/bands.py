@@ -46,7 +46,9 @@ import torch
 from . import _device
 from . import _lib as L
 
-HALO = 8
+HALO = 8        # rows of halo each band keeps (consistency 7 + stencil 1)
+R_HALO = 7      # rows of the 3 r planes a kernel reads across a boundary (energy.py:23)
+T_HALO = 1      # rows of the T planes (gradient stencils, energy.py:272-291)
 
 
 # ---------------------------------------------------------------------------
@@ -106,6 +108,17 @@ def halo_moves(bands: list[BandSpec]):
     return moves
 
 
+def halo_pieces(move, r_planes: int = 3):
+    """The parts of a halo move the kernels read: the R_HALO rows of the r
+    planes and the T_HALO rows of the T planes nearest the boundary (the
+    r planes' partner window reaches 7 rows, every stencil 1).  Returns
+    [(plane0, plane1, g0, g1)] (plane1 None = to the last plane)."""
+    s, d, g0, g1 = move
+    if s < d:   # the upper band's last own rows -> the lower band's top halo
+        return [(0, r_planes, max(g0, g1 - R_HALO), g1), (r_planes, None, max(g0, g1 - T_HALO), g1)]
+    return [(0, r_planes, g0, min(g1, g0 + R_HALO)), (r_planes, None, g0, min(g1, g0 + T_HALO))]
+
+
 def zero_scan_range(GH: int, W: int, n: int, b: int) -> tuple[int, int]:
     """Stream positions band b scans for rejections: the bands split
     [0, 12 N + 64) (dx, dy, temporal sections of energy.py:162-171 plus the
@@ -142,17 +155,23 @@ class LocalExchange:
         g = torch.stack([p.to(parts[0].device) for p in parts]).contiguous()
         return [g if p.device == g.device else g.to(p.device) for p in parts]
 
-    def halo(self, tensors: list[torch.Tensor]):
-        """tensors[i]: (C, H_loc, W) local tensor of band i."""
-        for s, d, g0, g1 in halo_moves(self.bands):
-            src, dst = self.bands[s], self.bands[d]
-            piece = tensors[s][:, g0 - src.ya:g1 - src.ya]
-            tensors[d][:, g0 - dst.ya:g1 - dst.ya].copy_(piece, non_blocking=True)
+    def halo(self, tensors: list[torch.Tensor], full: bool = False):
+        """tensors[i]: (U, H_loc, W) local tensor of band i.  Refreshes the
+        halo rows the kernels read (halo_pieces); full=True copies the whole
+        HALO rows of every plane."""
+        for mv in halo_moves(self.bands):
+            src, dst = self.bands[mv[0]], self.bands[mv[1]]
+            pieces = [(0, None, mv[2], mv[3])] if full else halo_pieces(mv)
+            for p0, p1, g0, g1 in pieces:
+                piece = tensors[mv[0]][p0:p1, g0 - src.ya:g1 - src.ya]
+                tensors[mv[1]][p0:p1, g0 - dst.ya:g1 - dst.ya].copy_(piece, non_blocking=True)
 
 
 class DistExchange:
     """One band per rank of a torch.distributed process group (rank r owns
-    band r)."""
+    band r).  With NCCL the buffers stay on the device (NVLink P2P, all-
+    gather); with gloo (CPU tests, or several ranks sharing one GPU) they are
+    staged through host memory."""
 
     def __init__(self, bands: list[BandSpec], group=None):
         import torch.distributed as dist
@@ -164,32 +183,47 @@ class DistExchange:
         self.bands = bands
         self.local = [self.rank]
         self.nbands = len(bands)
+        self.host = dist.get_backend(group) == "gloo"
+
+    def _stage(self, t: torch.Tensor) -> torch.Tensor:
+        return t.cpu() if self.host and t.is_cuda else t
 
     def gather(self, parts: list[torch.Tensor]) -> list[torch.Tensor]:
         (p,) = parts
-        flat = p.contiguous().view(-1)
-        out = torch.empty(self.nbands * flat.numel(), dtype=p.dtype, device=p.device)
+        flat = self._stage(p.contiguous().view(-1))
+        out = torch.empty(self.nbands * flat.numel(), dtype=p.dtype, device=flat.device)
         self.dist.all_gather_into_tensor(out, flat, group=self.group)
-        return [out.view((self.nbands,) + tuple(p.shape))]
+        return [out.to(p.device).view((self.nbands,) + tuple(p.shape))]
 
-    def halo(self, tensors: list[torch.Tensor]):
+    def halo(self, tensors: list[torch.Tensor], full: bool = False):
+        """Each move is one message: the r-plane rows and the T-plane rows the
+        kernels read (halo_pieces), packed; full=True sends whole halos."""
         (t,) = tensors
         me = self.bands[self.rank]
         ops, recvs = [], []
         peer = lambda b: self.dist.get_global_rank(self.group, b) if self.group is not None else b
-        for s, d, g0, g1 in halo_moves(self.bands):
+        for mv in halo_moves(self.bands):
+            s, d = mv[0], mv[1]
+            if self.rank not in (s, d):
+                continue
+            pieces = [(0, None, mv[2], mv[3])] if full else halo_pieces(mv)
+            views = [t[p0:p1, g0 - me.ya:g1 - me.ya] for p0, p1, g0, g1 in pieces]
             if s == self.rank:
-                buf = t[:, g0 - me.ya:g1 - me.ya].contiguous()
+                buf = self._stage(torch.cat([v.reshape(-1) for v in views]))
                 ops.append(self.dist.P2POp(self.dist.isend, buf, peer(d), self.group))
-            elif d == self.rank:
-                buf = torch.empty_like(t[:, g0 - me.ya:g1 - me.ya])
+            else:
+                buf = torch.empty(sum(v.numel() for v in views), dtype=t.dtype,
+                                  device="cpu" if self.host else t.device)
                 ops.append(self.dist.P2POp(self.dist.irecv, buf, peer(s), self.group))
-                recvs.append((buf, g0 - me.ya, g1 - me.ya))
+                recvs.append((buf, views))
         if ops:
             for w in self.dist.batch_isend_irecv(ops):
                 w.wait()
-        for buf, a, b in recvs:
-            t[:, a:b].copy_(buf)
+        for buf, views in recvs:
+            off = 0
+            for v in views:
+                v.copy_(buf[off:off + v.numel()].view(v.shape))
+                off += v.numel()
 
 
 # ---------------------------------------------------------------------------

@@ -228,7 +228,7 @@ static void set_geometry(ls_ctx* c) {
   const int64_t M = (int64_t)c->U * rows * c->W;
   const int64_t upd_blocks = (M / 4 + kThreads - 1) / kThreads;
   c->grid_update = (int)std::max<int64_t>(1, std::min<int64_t>({upd_blocks, (int64_t)c->nsm * std::max(1, update_grid_limit()), (int64_t)kMaxBlocks}));
-  c->grid_dense = std::max(1, std::min(c->nsm * 4, (rows * c->W + 127) / 128));
+  c->grid_dense = std::max(1, std::min(c->nsm * 8, (rows * c->W + 63) / 64));
 }
 
 // the whole-frame entry points finalise inside their kernels
@@ -847,6 +847,39 @@ int ls_apply_normal(ls_ctx* c, const double* colors, const float* X, const float
   const bool tma = tile_maps(c, X, p, &maps);
   launch_apply(L_apply(c), frame_of(c), cf, X, p, Ap, c->part, c->tickets + 1, nullptr, 0, tma ? &maps : nullptr);
   LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+// ---- first-frame palette estimation (ls_palette.cu) ------------------------
+int ls_estimate_palette(const float* image_hwc, int H, int W, int k_max, uint64_t st_hi, uint64_t st_lo,
+                        uint64_t inc_hi, uint64_t inc_lo, double* colors_out, int* K_out, void* stream) {
+  LS_ARG(image_hwc && colors_out && K_out && H > 0 && W > 0, "bad arguments");
+  LS_ARG(k_max >= 1, "k_max must be >= 1");
+  LS_ARG(k_max <= LS_MAX_K, "k_max above the supported palette size (12)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int N = H * W;
+  float* img = nullptr;
+  double* chroma = nullptr;
+  char* scratch = nullptr;
+  double* cols = nullptr;
+  const size_t sb = palette_scratch_bytes();
+  LS_CK(cudaMallocAsync((void**)&img, sizeof(float) * 3 * (size_t)N, s));
+  LS_CK(cudaMallocAsync((void**)&chroma, sizeof(double) * 2 * (size_t)N, s));
+  LS_CK(cudaMallocAsync((void**)&scratch, sb + sizeof(double) * 3 * LS_MAX_K + 64, s));
+  cols = reinterpret_cast<double*>(scratch + sb);
+  int* kdev = reinterpret_cast<int*>(scratch + sb + sizeof(double) * 3 * LS_MAX_K);
+  launch_image(s, image_hwc, N, img, chroma);
+  LS_CK(cudaGetLastError());
+  LS_CK(launch_estimate_palette(s, img, chroma, N, k_max, PalRng{st_hi, st_lo, inc_hi, inc_lo}, scratch, cols,
+                                kdev));
+  int K = 0;
+  LS_CK(cudaMemcpyAsync(&K, kdev, sizeof(int), cudaMemcpyDeviceToHost, s));
+  LS_CK(cudaMemcpyAsync(colors_out, cols, sizeof(double) * 3 * k_max, cudaMemcpyDeviceToHost, s));
+  LS_CK(cudaFreeAsync(img, s));
+  LS_CK(cudaFreeAsync(chroma, s));
+  LS_CK(cudaFreeAsync(scratch, s));
+  LS_CK(cudaStreamSynchronize(s));
+  *K_out = K;
   return LS_OK;
 }
 

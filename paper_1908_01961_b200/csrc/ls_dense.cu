@@ -126,6 +126,125 @@ __global__ void __launch_bounds__(128) k_dense_accum(Frame f, const double* __re
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
+// ---- k_dense_accum2: the same sums with per-thread register accumulation --
+// A CTA of 128 threads takes chunks of 64 pixels.  Phase 1: threads 0..63
+// compute their pixel's values -- v_c[k] = R_c T_{k+1} (3K), the data
+// residual res_c (3), r_c (3) and the cluster id -- into shared memory.
+// Phase 2: thread t runs job t % 64 over half (t / 64) of the chunk's pixels:
+// jobs 0..3K-1 are one row (c, k) of the data block, accumulating
+// v_c[k] v_c[j] for every j (the lower part is dropped at the end) and
+// v_c[k] res_c; jobs 3K..4K-1 are cluster k's count and r sums.  All
+// accumulation is in registers; one fixed-order reduction per CTA, then the
+// last CTA sums the CTA partials in CTA order.
+constexpr int kDa2Threads = 128, kDa2Chunk = 64;
+
+template <int K>
+__global__ void __launch_bounds__(kDa2Threads) k_dense_accum2(Frame f, const double* __restrict__ colors,
+                                                              const float* __restrict__ X, int use_ids,
+                                                              double* part, unsigned* ticket, double* sums) {
+  constexpr int NT = K + 1, NV = 3 * K + 7;   // per pixel: v (3K), res (3), r (3), id
+  constexpr int NS = 3 * (K * (K + 1) / 2) + 7 * K, NM = 3 * (K * (K + 1) / 2);
+  constexpr int NA = K + 1 > 4 ? K + 1 : 4;   // accumulators: a data row + rhs, or 4 cluster sums
+  __shared__ double pix[kDa2Chunk][NV + 1];
+  __shared__ double red[kDa2Threads][NA];
+  __shared__ double B[NT][3];
+  if (threadIdx.x < NT * 3) {
+    const int k = threadIdx.x / 3, c = threadIdx.x % 3;
+    B[k][c] = k == 0 ? 1.0 : colors[3 * (k - 1) + c];
+  }
+  const int N = f.N;
+  const int i0 = f.y_lo * f.W, npx = (f.y_hi - f.y_lo) * f.W;
+  const int job = threadIdx.x % kDa2Chunk, half = threadIdx.x / kDa2Chunk;
+  const bool row_job = job < 3 * K, cl_job = job >= 3 * K && job < 4 * K;
+  const int jc = row_job ? job / K : 0, jk = row_job ? job % K : (cl_job ? job - 3 * K : 0);
+  double acc[NA];
+#pragma unroll
+  for (int j = 0; j < NA; ++j) acc[j] = 0.0;
+  __syncthreads();
+  for (int c0 = blockIdx.x * kDa2Chunk; c0 < npx; c0 += gridDim.x * kDa2Chunk) {
+    if (threadIdx.x < kDa2Chunk) {
+      double* pv = pix[threadIdx.x];
+      const int q = c0 + threadIdx.x;
+      if (q < npx) {
+        const int i = i0 + q;
+        double t[NT];
+#pragma unroll
+        for (int k = 0; k < NT; ++k) t[k] = (double)X[(size_t)(3 + k) * N + i];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double S = 0.0;
+#pragma unroll
+          for (int k = 0; k < NT; ++k) S += t[k] * B[k][c];
+          const double r = (double)X[(size_t)c * N + i];
+          const double R = exp(r);
+#pragma unroll
+          for (int k = 0; k < K; ++k) pv[c * K + k] = R * t[k + 1];
+          pv[3 * K + c] = (double)f.img[(size_t)c * N + i] - R * S;
+          pv[3 * K + 3 + c] = r;
+        }
+        pv[3 * K + 6] = (use_ids && f.ids) ? (double)f.ids[i] : 0.0;
+      } else {
+        for (int v = 0; v < NV; ++v) pv[v] = 0.0;
+      }
+    }
+    __syncthreads();
+    const int qn = min(kDa2Chunk / 2, max(0, npx - c0 - half * (kDa2Chunk / 2)));
+    const double* base = pix[half * (kDa2Chunk / 2)];
+    if (row_job) {
+      for (int q = 0; q < qn; ++q) {
+        const double* pv = base + q * (NV + 1);
+        const double a = pv[jc * K + jk];
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[j] = fma(a, pv[jc * K + j], acc[j]);
+        acc[K] = fma(a, pv[3 * K + jc], acc[K]);
+      }
+    } else if (cl_job) {
+      const double id = (double)(jk + 1);
+      for (int q = 0; q < qn; ++q) {
+        const double* pv = base + q * (NV + 1);
+        if (pv[3 * K + 6] == id) {
+          acc[0] += 1.0;
+          acc[1] += pv[3 * K + 3];
+          acc[2] += pv[3 * K + 4];
+          acc[3] += pv[3 * K + 5];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // CTA reduction: the two halves of each job, then the sums layout of
+  // dense_ns (M_c upper triangle, rhs_c, n_k, sum r_c over cluster k)
+#pragma unroll
+  for (int j = 0; j < NA; ++j) red[threadIdx.x][j] = acc[j];
+  __syncthreads();
+  if (threadIdx.x < kDa2Chunk) {
+    double* out = part + (size_t)blockIdx.x * NS;
+    if (row_job) {
+      int off = 0;
+      for (int kk = 0; kk < jk; ++kk) off += K - kk;
+      for (int j = jk; j < K; ++j)
+        out[jc * (K * (K + 1) / 2) + off + (j - jk)] = red[job][j] + red[job + kDa2Chunk][j];
+      out[NM + jc * K + jk] = red[job][K] + red[job + kDa2Chunk][K];
+    } else if (cl_job) {
+      out[NM + 3 * K + jk] = red[job][0] + red[job + kDa2Chunk][0];
+      for (int c = 0; c < 3; ++c) out[NM + 4 * K + 3 * jk + c] = red[job][1 + c] + red[job + kDa2Chunk][1 + c];
+    }
+  }
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int e = threadIdx.x; e < NS; e += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) s += ((volatile double*)part)[(size_t)b * NS + e];
+    sums[e] = s;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
 // band-ordered sum of gathered per-band partial sums [nbands][nv]
 __global__ void k_band_sum(const double* __restrict__ g, int nbands, int nv, double* out) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nv; j += gridDim.x * blockDim.x) {
@@ -309,7 +428,14 @@ __global__ void __launch_bounds__(32 * kSvdWarps) k_dense_solve(const double* __
 
 void launch_dense_accum(cudaStream_t s, int grid, const Frame& f, const double* colors_dev, int K, const float* X,
                         int use_ids, double* part, unsigned* ticket, double* sums) {
-  k_dense_accum<<<grid, 128, 0, s>>>(f, colors_dev, K, X, use_ids, part, ticket, sums);
+  switch (K) {   // register-accumulating kernel for K = 1..12 (4K jobs <= 64 threads)
+#define LS_DA2(KV) \
+    case KV: k_dense_accum2<KV><<<grid, kDa2Threads, 0, s>>>(f, colors_dev, X, use_ids, part, ticket, sums); break;
+    LS_DA2(1) LS_DA2(2) LS_DA2(3) LS_DA2(4) LS_DA2(5) LS_DA2(6) LS_DA2(7) LS_DA2(8) LS_DA2(9) LS_DA2(10)
+    LS_DA2(11) LS_DA2(12)
+#undef LS_DA2
+    default: k_dense_accum<<<grid, 128, 0, s>>>(f, colors_dev, K, X, use_ids, part, ticket, sums); break;
+  }
 }
 void launch_dense_assemble_solve(cudaStream_t s, const double* sums, int K, const double* colors_dev, int use_ids,
                                  double lam_d, double lam_cl, double lam_ir, double lam_cr, int chroma_identity,

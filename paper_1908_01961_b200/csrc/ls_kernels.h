@@ -84,6 +84,14 @@ cudaError_t launch_block_rows(cudaStream_t s, const Frame& f, const Coef<double>
 cudaError_t launch_block_cols(cudaStream_t s, const Frame& f, const Coef<double>& c, const float* X0,
                               const BlockPairs& pairs, int block, int op, const float* w, float* out);
 
+// ls_palette.cu: first-frame palette estimation (palette.py:81-238)
+struct PalRng {   // numpy PCG64 state of default_rng(seed) (Generator.choice draw)
+  unsigned long long st_hi, st_lo, inc_hi, inc_lo;
+};
+size_t palette_scratch_bytes();
+cudaError_t launch_estimate_palette(cudaStream_t s, const float* img, const double* chroma, int N, int k_max,
+                                    const PalRng& rng, void* scratch, double* out_colors, int* out_k);
+
 // ls_aux.cu
 // int32 scan (op 0: exclusive sum, op 1: inclusive max) of n values; scratch
 // of scan_scratch_bytes(n) bytes (zeroed by the launcher on the stream)

@@ -2,9 +2,9 @@
 (reference palette.py).
 
 `segment` (per streaming frame) runs on the device kernel, bit-identical to
-palette.py:195-224.  `estimate_palette` is the first-frame histogram k-means
-(palette.py:81-238) -- outside the solver hot path (SURVEY.md section 2,
-row 6): ~100 histogram bins, so it runs on the host after one device copy.
+palette.py:195-224.  `estimate_palette`, the first-frame histogram k-means
+and merge (palette.py:81-238), runs on the device too (csrc/ls_palette.cu):
+integer histogram, bit-exact k-means centers, merge in the last CTA.
 """
 
 from __future__ import annotations
@@ -18,7 +18,7 @@ import torch
 from . import _device
 from .imaging import Frame, chroma_of_color, chromaticity, as_cuda
 
-HIST_BINS = 10
+HIST_BINS = 10            # palette.py:19-21 (the kernels' constants)
 MERGE_DISTANCE = 0.2
 KMEANS_MAX_ITERS = 100
 
@@ -104,120 +104,68 @@ def segment(frame: Frame, palette: BaseColorPalette, chroma=None) -> ClusterMap:
     return ClusterMap(ids=ids, colors=np.array(palette.colors, dtype=np.float64))
 
 
-# ---- first-frame palette estimation (host; out of the hot path) -------------
-
-def _histogram(chroma_np, inten_np, dark_np):
-    valid = ~dark_np
-    if not np.any(valid):
-        raise EmptyHistogramError("all pixels are dark; nothing to cluster")
-    c = chroma_np[valid]
-    rb = np.clip((c[:, 0] * HIST_BINS).astype(np.int64), 0, HIST_BINS - 1)
-    gb = np.clip((c[:, 1] * HIST_BINS).astype(np.int64), 0, HIST_BINS - 1)
-    flat = gb * HIST_BINS + rb
-    pop = np.bincount(flat, minlength=HIST_BINS * HIST_BINS)
-    return pop.reshape(HIST_BINS, HIST_BINS)
-
-
-def _kmeans(pop, k_max, seed):
-    """palette.py:81-120: population-weighted farthest-point seeding + Lloyd."""
-    if k_max < 1:
-        raise ValueError("k_max must be >= 1")
-    gb, rb = np.nonzero(pop)
-    mids = np.stack([(rb + 0.5) / HIST_BINS, (gb + 0.5) / HIST_BINS], axis=-1)
-    pops = pop[gb, rb]
-    n = mids.shape[0]
-    k = min(k_max, n)
-    rng = np.random.default_rng(seed)
-    chosen = [rng.choice(n, p=pops / pops.sum())]
-    while len(chosen) < k:
-        d = np.min(np.linalg.norm(mids[:, None, :] - mids[chosen][None, :, :], axis=2), axis=1)
-        chosen.append(int(np.argmax(d)))
-    centers = mids[chosen].copy()
-    prev = None
-    for _ in range(KMEANS_MAX_ITERS):
-        assign = np.argmin(np.linalg.norm(mids[:, None, :] - centers[None], axis=2), axis=1)
-        if prev is not None and np.array_equal(assign, prev):
-            break
-        prev = assign
-        for j in range(k):
-            sel = assign == j
-            if np.any(sel):
-                centers[j] = np.average(mids[sel], axis=0, weights=pops[sel])
-    return centers
-
-
-def _merge(centers, image_np, assign, dark_np):
-    """palette.py:148-192: merge centers closer than 0.2, smaller into larger."""
-    centers = centers.copy()
-    valid = ~dark_np
-    k = centers.shape[0]
-    pops = np.array([np.count_nonzero((assign == j) & valid) for j in range(k)], dtype=np.int64)
-    alive = list(range(k))
-    while len(alive) > 1:
-        best = None
-        for ai in range(len(alive)):
-            for bi in range(ai + 1, len(alive)):
-                a, b = alive[ai], alive[bi]
-                d = float(np.linalg.norm(centers[a] - centers[b]))
-                if d < MERGE_DISTANCE and (best is None or d < best[0]):
-                    best = (d, a, b)
-        if best is None:
-            break
-        _, a, b = best
-        small, large = (a, b) if pops[a] <= pops[b] else (b, a)
-        assign[assign == small] = large
-        pops[large] += pops[small]
-        pops[small] = 0
-        alive.remove(small)
-    colors = []
-    for j in alive:
-        sel = (assign == j) & valid
-        if np.any(sel):
-            colors.append(image_np[sel].mean(axis=0))
-        else:
-            r, g = centers[j]
-            colors.append(np.array([r, g, max(0.0, 1.0 - r - g)]))
-    return BaseColorPalette(colors=np.array(colors))
-
+# ---- first-frame palette estimation (device, csrc/ls_palette.cu) ----------
 
 def estimate_palette(frame: Frame, k_max: int = 10, seed: int = 0):
-    """palette.py:227-238 -> (palette, cluster_map)."""
-    ch = chromaticity(frame)
-    chroma_np = ch.chroma.cpu().numpy()
-    dark_np = ch.dark.cpu().numpy()
-    image_np = frame.data.double().cpu().numpy()
-    centers = _kmeans(_histogram(chroma_np, None, dark_np), k_max, seed)
-    flat = chroma_np.reshape(-1, 2)
-    assign = np.argmin(np.linalg.norm(flat[:, None, :] - centers[None], axis=2), axis=1)
-    pal = _merge(centers, image_np, assign.reshape(chroma_np.shape[:2]), dark_np)
+    """palette.py:227-238 -> (palette, cluster_map).  Histogram, weighted
+    k-means (the first pick drawn from default_rng(seed) exactly as
+    Generator.choice does) and the merge run on the device
+    (ls_estimate_palette); the cluster map is `segment` with the result."""
+    from . import _lib as L
+    import ctypes as C
+    if k_max < 1:
+        raise ValueError("k_max must be >= 1")
+    img = frame.data
+    if not img.is_cuda:
+        raise ValueError("estimate_palette needs a CUDA frame")
+    H, W = int(img.shape[0]), int(img.shape[1])
+    st = np.random.PCG64(seed).state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m64 = (1 << 64) - 1
+    kk = min(int(k_max), L.MAX_K)
+    out = np.zeros(3 * kk)
+    K = C.c_int()
+    lib = L.load()
+    with torch.cuda.device(img.device):
+        stream = torch.cuda.current_stream(img.device)
+        rc = lib.ls_estimate_palette(C.c_void_p(img.contiguous().data_ptr()), H, W, kk, s >> 64, s & m64,
+                                     inc >> 64, inc & m64, out.ctypes.data_as(L.DBL_P), C.byref(K),
+                                     C.c_void_p(stream.cuda_stream))
+    if rc != L.LS_OK:
+        raise (ValueError if rc == L.LS_ERR_ARG else L.NativeError)(L.last_error())
+    if K.value == 0:
+        raise EmptyHistogramError("all pixels are dark; nothing to cluster")
+    pal = BaseColorPalette(colors=out[:3 * K.value].reshape(K.value, 3).copy())
     return pal, segment(frame, pal)
 
 
+# palette file format (palette.py:241-265): {"K", "colors"[, "refined",
+# "previous"]}, indented two spaces, trailing newline
 def palette_to_json(palette: BaseColorPalette) -> dict:
-    doc = {"K": palette.K, "colors": [[float(v) for v in c] for c in palette.colors]}
+    rows = lambda a: np.asarray(a, dtype=np.float64).tolist()     # noqa: E731
+    doc = dict(K=palette.K, colors=rows(palette.colors))
     if palette.refined:
-        doc["refined"] = True
+        doc.update(refined=True)
         if palette.previous is not None:
-            doc["previous"] = [[float(v) for v in c] for c in palette.previous]
+            doc.update(previous=rows(palette.previous))
     return doc
 
 
 def palette_from_json(doc: dict) -> BaseColorPalette:
     prev = doc.get("previous")
-    return BaseColorPalette(colors=np.array(doc["colors"], dtype=np.float64),
+    return BaseColorPalette(colors=np.asarray(doc["colors"], dtype=np.float64),
                             refined=bool(doc.get("refined", False)),
-                            previous=None if prev is None else np.array(prev))
+                            previous=np.asarray(prev) if prev is not None else None)
 
 
 def save_palette(path, palette: BaseColorPalette) -> None:
-    with open(path, "w") as fh:
-        json.dump(palette_to_json(palette), fh, indent=2)
-        fh.write("\n")
+    from pathlib import Path
+    Path(path).write_text(json.dumps(palette_to_json(palette), indent=2) + "\n")
 
 
 def load_palette(path) -> BaseColorPalette:
-    with open(path) as fh:
-        return palette_from_json(json.load(fh))
+    from pathlib import Path
+    return palette_from_json(json.loads(Path(path).read_text()))
 
 
 def cluster_map_from_ids(ids, palette: BaseColorPalette, device=None) -> ClusterMap:

@@ -35,19 +35,48 @@ def _full(H, W, C=5, seed=0):
     return torch.rand(C, H, W, generator=g, dtype=torch.float64)
 
 
-def test_local_exchange_refreshes_every_halo():
+def _needed(s, H):
+    """Mask of the halo cells the kernels read: R_HALO rows of the r planes
+    and T_HALO rows of the T planes next to each band boundary."""
+    m = torch.zeros(5, s.height, dtype=torch.bool)
+    m[:, s.y_lo:s.y_hi] = True
+    for planes, rows in ((slice(0, 3), B.R_HALO), (slice(3, None), B.T_HALO)):
+        m[planes, max(0, s.y_lo - rows):s.y_lo] = True
+        m[planes, s.y_hi:min(s.height, s.y_hi + rows)] = True
+    return m
+
+
+@pytest.mark.parametrize("full", [False, True])
+def test_local_exchange_refreshes_every_halo(full):
     H, W = 70, 12
     specs = B.plan_bands(H, 4)
-    full = _full(H, W)
+    ref = _full(H, W)
     locs = []
     for s in specs:
-        t = full[:, s.ya:s.yb].clone()
+        t = ref[:, s.ya:s.yb].clone()
         t[:, :s.y_lo] = -1.0          # stale halos
         t[:, s.y_hi:] = -2.0
         locs.append(t)
-    B.LocalExchange(specs).halo(locs)
+    B.LocalExchange(specs).halo(locs, full=full)
     for s, t in zip(specs, locs):
-        assert torch.equal(t, full[:, s.ya:s.yb])
+        want = ref[:, s.ya:s.yb]
+        if full:
+            assert torch.equal(t, want)
+        else:
+            m = _needed(s, H)[:, :, None].expand_as(t)
+            assert torch.equal(t[m], want[m])
+            assert (t[~m] < 0).all()        # rows nobody reads are not moved
+
+
+def test_halo_pieces_cut_bytes():
+    """r planes: 7 rows, T planes: 1 row per boundary instead of 8 rows of
+    all U planes (U = 12 at K = 8: 30 / 96 of the rows)."""
+    specs = B.plan_bands(2160, 4)
+    for mv in B.halo_moves(specs):
+        (a0, a1, r0, r1), (b0, b1, t0, t1) = B.halo_pieces(mv)
+        assert (a0, a1, b0, b1) == (0, 3, 3, None)
+        assert r1 - r0 == B.R_HALO and t1 - t0 == B.T_HALO
+        assert (r0 <= t0 < t1 <= r1) and (t1 == r1 if mv[0] < mv[1] else t0 == r0)
 
 
 def test_local_exchange_gather_is_band_ordered():
@@ -79,7 +108,11 @@ def _worker(rank, world, port, H, W, q):
         t[:, :me.y_lo] = float("nan")
         t[:, me.y_hi:] = float("nan")
         ex.halo([t])
-        ok_halo = torch.equal(t, full[:, me.ya:me.yb])
+        m = _needed(me, H)[:, :, None].expand_as(t)
+        ok_halo = torch.equal(t[m], full[:, me.ya:me.yb][m]) and bool(torch.isnan(t[~m]).all())
+        t2 = t.clone()
+        ex.halo([t2], full=True)
+        ok_halo = ok_halo and torch.equal(t2, full[:, me.ya:me.yb])
         part = torch.tensor([rank * 10.0 + j for j in range(3)], dtype=torch.float64)
         (g,) = ex.gather([part])
         ok_gather = torch.equal(g, torch.tensor([[r * 10.0 + j for j in range(3)] for r in range(world)],
