@@ -180,6 +180,9 @@ static Coef<R> make_coef(const ls_weights& w, const double* colors, int K) {
       c.G[k][ch] = (R)(b[ch] - mean);
       c.anchor[k][ch] = (k == 0) ? R(0) : (R)std::log(std::max(b[ch], 1e-4));
     }
+    R g2 = R(0);
+    for (int ch = 0; ch < 3; ++ch) g2 = std::fma(c.G[k][ch], c.G[k][ch], g2);
+    c.g2[k] = g2;
   }
   c.lam_d = (R)w.lambda_data;
   c.lam_cl = (R)w.lambda_clustering;
@@ -988,10 +991,12 @@ static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, f
                      it, tma ? &maps[it & 1] : nullptr, x);
     prof_end(c, PC_APPLY, pi);
     pi = prof_begin(c);
-    launch_pcg_update(L_update(c), M, c->r, c->wv, c->d, c->u, pbuf[it & 1], x, c->part, c->tickets + 2, c->sc, it);
+    launch_pcg_update(L_update(c), M, c->r, c->wv, c->d, c->u, pbuf[it & 1], x, c->part, c->tickets + 2, c->sc, it,
+                      nullptr, it == iters - 1);
     prof_end(c, PC_UPDATE, pi);
   }
-  // the last x += alpha p (the applies fold in the earlier ones)
+  // the last x += alpha p when the loop broke early (the applies fold in the
+  // earlier ones, the final update the last one; otherwise a no-op)
   launch_pcg_xfinal(L_update(c), M, x, pbuf[0], pbuf[1], c->sc, c->tickets + 4);
   c->launches += 2 + 2LL * iters;
   LS_CK(cudaGetLastError());

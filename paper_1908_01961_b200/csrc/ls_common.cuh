@@ -53,6 +53,7 @@ struct Coef {
   R B[kMaxNT][3];      // palette matrix, row 0 white (palette.py:64-66)
   R G[kMaxNT][3];      // B - rowmean(B) (energy.py:396)
   R anchor[kMaxNT][3]; // log(max(color[id-1], 1e-4)) indexed by id (energy.py:470-472)
+  R g2[kMaxNT];        // sum_c G[k][c]^2 (monochrome diagonal, energy.py:410-411), fma order of the kernels
   R lam_d, lam_cl, lam_rs, p, lam_rc, lam_m, lam_is, lam_sm, lam_nn;
   R eps_nn, eps_irls, inv_eps, floor_rs;
 };

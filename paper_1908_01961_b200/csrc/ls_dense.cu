@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(kDa2Threads) k_dense_accum2(Frame f, const dou
   constexpr int NT = K + 1, NV = 3 * K + 7;   // per pixel: v (3K), res (3), r (3), id
   constexpr int NS = 3 * (K * (K + 1) / 2) + 7 * K, NM = 3 * (K * (K + 1) / 2);
   constexpr int NA = K + 1 > 4 ? K + 1 : 4;   // accumulators: a data row + rhs, or 4 cluster sums
-  __shared__ double pix[kDa2Chunk][NV + 1];
+  constexpr int PS = NV | 1;   // odd row stride (doubles): phase-1 row writes are 2-way, not 32-way, banked
+  __shared__ double pix[kDa2Chunk][PS];
   __shared__ double red[kDa2Threads][NA];
   __shared__ double B[NT][3];
   if (threadIdx.x < NT * 3) {
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(kDa2Threads) k_dense_accum2(Frame f, const dou
     const double* base = pix[half * (kDa2Chunk / 2)];
     if (row_job) {
       for (int q = 0; q < qn; ++q) {
-        const double* pv = base + q * (NV + 1);
+        const double* pv = base + q * PS;
         const double a = pv[jc * K + jk];
 #pragma unroll
         for (int j = 0; j < K; ++j) acc[j] = fma(a, pv[jc * K + j], acc[j]);
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(kDa2Threads) k_dense_accum2(Frame f, const dou
     } else if (cl_job) {
       const double id = (double)(jk + 1);
       for (int q = 0; q < qn; ++q) {
-        const double* pv = base + q * (NV + 1);
+        const double* pv = base + q * PS;
         if (pv[3 * K + 6] == id) {
           acc[0] += 1.0;
           acc[1] += pv[3 * K + 3];

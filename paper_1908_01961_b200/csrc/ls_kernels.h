@@ -50,9 +50,11 @@ int tile_box_rw();
 void launch_pcg_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* z,
                       const float* pprev, float* pnew, float* q, double* part, unsigned* ticket, Scalars* sc,
                       int iter, const PcgMaps* maps, float* x);
+// last = true (whole frames only): the final iteration also folds in the
+// last deferred x += alpha p (p = this iteration's direction) and skips z
 void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
                        const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter,
-                       const Frame* band = nullptr);
+                       const Frame* band = nullptr, bool last = false);
 void launch_pcg_xfinal(const Launch& L, int64_t M, float* xv, const float* p0, const float* p1, Scalars* sc,
                        unsigned* ticket, const Frame* band = nullptr);
 // row bands: phases whose partial sums are gathered across bands

@@ -33,6 +33,9 @@
 #ifndef LS_ABLATE
 #define LS_ABLATE 0
 #endif
+#ifndef LS_XEARLY
+#define LS_XEARLY 0
+#endif
 
 namespace ls {
 
@@ -313,14 +316,14 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
         esm = fmaf(wy * g, g, esm);
       }
       if (MODE == MODE_EG) {
-        float g = 0.f, d = 0.f, gm = 0.f, g2 = 0.f;
+        float g = 0.f, d = 0.f, gm = 0.f;
+        const float g2 = c.g2[k];   // sum_c G_kc^2, precomputed (make_coef)
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
           const float rb = R[ch] * c.B[k][ch];
           g = fmaf(rb, res[ch], g);
           d = fmaf(rb, rb, d);
           gm = fmaf(c.G[k][ch], m[ch], gm);
-          g2 = fmaf(c.G[k][ch], c.G[k][ch], g2);
         }
         const float wdk = wis + wnn;
         g = fmaf(-c.lam_d, g, fmaf(lm, gm, wdk * T0[k]));
@@ -334,7 +337,7 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
         g = fmaf(c.lam_sm, gs, g);
         d = fmaf(c.lam_sm, ds, d);
         const float bf = -g;
-        const float di = __frcp_rn(d > 0.f ? d : 1.f);   // Jacobi preconditioner (solver.py:87)
+        const float di = rcpf(d > 0.f ? d : 1.f);   // Jacobi preconditioner 1/diag (solver.py:87), MUFU
         const float zf = bf * di;
         const size_t o = (size_t)(3 + k) * N + i;
         if (r_out) { r_out[o] = bf; d_out[o] = di; u_out[o] = zf; }
@@ -434,7 +437,7 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
     g += gcons[ch];
     d += dcons;
     const float bf = -g;
-    const float di = __frcp_rn(d > 0.f ? d : 1.f);   // Jacobi preconditioner (solver.py:87)
+    const float di = rcpf(d > 0.f ? d : 1.f);   // Jacobi preconditioner 1/diag (solver.py:87), MUFU
     const float zf = bf * di;
     if (r_out) { r_out[ch * N + i] = bf; d_out[ch * N + i] = di; u_out[ch * N + i] = zf; }
     if (b_raw) { b_raw[ch * N + i] = bf; diag_raw[ch * N + i] = d; }
@@ -994,6 +997,14 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
     else if (own)
       acc += apply_pixel<NT, false>(f, c, sX, sZT, sZR, q, x, y, cx, cy, rx, ry, pre);
     float pold[U];
+#if LS_XEARLY
+    float xo[U];
+    if (xupd && own) {   // x loads issued before the stage barrier (timing experiment)
+      const size_t i = (size_t)y * W + x;
+#pragma unroll
+      for (int u = 0; u < U; ++u) xo[u] = xread ? xv[(size_t)u * N + i] : 0.f;
+    }
+#endif
     if (own) {
       const int i = y * W + x;
       const int sc0 = cy * kSW + cx, rc0 = ry * kRW + rx;
@@ -1023,9 +1034,11 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
     }
     if (xupd && own) {   // x += alpha_{i-1} p_{i-1}, overlapping the next tile's loads
       const size_t i = (size_t)y * W + x;
+#if !LS_XEARLY
       float xo[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) xo[u] = xread ? xv[(size_t)u * N + i] : 0.f;
+#endif
 #pragma unroll
       for (int u = 0; u < U; ++u) xv[(size_t)u * N + i] = fmaf(ax, pold[u], xo[u]);
     }
@@ -1056,12 +1069,19 @@ __device__ __forceinline__ int64_t span_index(const BandSpan& b, int64_t j) {
   return (int64_t)pl * b.plane4 + b.off4 + (j - (int64_t)pl * b.len4);
 }
 
+// LAST (the final iteration of a whole-frame PCG): r_{n} is needed only for
+// the reported |r| (solver.py:106) and z / beta not at all, so the kernel
+// reads r, q and -- instead of dinv -- p and x, folds the last deferred
+// x-update x += alpha p in (what k_pcg_xfinal would do) and writes only x.
+template <bool LAST>
 __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __restrict__ r, const float* __restrict__ q,
                                                          const float* __restrict__ dinv, float* __restrict__ z,
                                                          double* part, unsigned* ticket, Scalars* sc, int iter,
-                                                         BandSpan band, double* bsum) {
+                                                         BandSpan band, double* bsum, const float* __restrict__ p,
+                                                         float* __restrict__ xv) {
   if (sc->stop) return;
   const float a = (float)sc->alpha;
+  const bool xread = LAST && sc->xinit;
   double acc[2] = {0.0, 0.0};
   const bool banded = band.planes > 0;
   const int64_t M4 = banded ? (int64_t)band.planes * band.len4 : (M >> 2);
@@ -1070,20 +1090,31 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
     const int64_t j = banded ? span_index(band, jj) : jj;
     float4 rr = reinterpret_cast<const float4*>(r)[j];
     const float4 qq = __ldg(reinterpret_cast<const float4*>(q) + j);
-    const float4 di = __ldg(reinterpret_cast<const float4*>(dinv) + j);
     rr = make_float4(fmaf(-a, qq.x, rr.x), fmaf(-a, qq.y, rr.y), fmaf(-a, qq.z, rr.z), fmaf(-a, qq.w, rr.w));
-    const float4 zz = make_float4(rr.x * di.x, rr.y * di.y, rr.z * di.z, rr.w * di.w);
-    reinterpret_cast<float4*>(r)[j] = rr;
-    reinterpret_cast<float4*>(z)[j] = zz;
-    acc[0] += (double)fmaf(rr.x, zz.x, fmaf(rr.y, zz.y, fmaf(rr.z, zz.z, rr.w * zz.w)));
+    if (LAST) {
+      const float4 pp = __ldg(reinterpret_cast<const float4*>(p) + j);
+      float4 xx = xread ? reinterpret_cast<const float4*>(xv)[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+      xx = make_float4(fmaf(a, pp.x, xx.x), fmaf(a, pp.y, xx.y), fmaf(a, pp.z, xx.z), fmaf(a, pp.w, xx.w));
+      reinterpret_cast<float4*>(xv)[j] = xx;
+    } else {
+      const float4 di = __ldg(reinterpret_cast<const float4*>(dinv) + j);
+      const float4 zz = make_float4(rr.x * di.x, rr.y * di.y, rr.z * di.z, rr.w * di.w);
+      reinterpret_cast<float4*>(r)[j] = rr;
+      reinterpret_cast<float4*>(z)[j] = zz;
+      acc[0] += (double)fmaf(rr.x, zz.x, fmaf(rr.y, zz.y, fmaf(rr.z, zz.z, rr.w * zz.w)));
+    }
     acc[1] += (double)fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, fmaf(rr.z, rr.z, rr.w * rr.w)));
   }
   for (int64_t j = banded ? M : (M4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride) {
     const float rr = fmaf(-a, q[j], r[j]);
-    const float zz = rr * dinv[j];
-    r[j] = rr;
-    z[j] = zz;
-    acc[0] += (double)rr * zz;
+    if (LAST) {
+      xv[j] = fmaf(a, p[j], xread ? xv[j] : 0.f);
+    } else {
+      const float zz = rr * dinv[j];
+      r[j] = rr;
+      z[j] = zz;
+      acc[0] += (double)rr * zz;
+    }
     acc[1] += (double)rr * rr;
   }
   block_reduce_store<2>(acc, part);
@@ -1094,6 +1125,11 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
     if (bsum) {
       bsum[0] = rz;
       bsum[1] = rn;
+    } else if (LAST) {   // the loop ends here: record the count and |r|, x is complete
+      sc->iterations = iter + 1;
+      sc->rnorm2 = rn;
+      sc->pending = 0;
+      sc->xinit = 1;
     } else {
       fin_pcg_update(rz, rn, sc, iter);
     }
@@ -1130,8 +1166,13 @@ static size_t energy_smem(int mode, bool tma) {
 template <int NT>
 static size_t apply_smem(bool tma) { return sizeof(float) * tile_floats(NT, true) * (tma ? 2 : 1); }
 
+// LS_PCG_PAD (timing experiments only, tools/ablate.py): extra shared memory
+// per CTA to pin the operator kernel's occupancy (e.g. 2 CTAs / SM)
+#ifndef LS_PCG_PAD
+#define LS_PCG_PAD 0
+#endif
 template <int NT>
-static size_t pcg_smem(bool tma) { return sizeof(float) * pcg_stage(NT, tma); }
+static size_t pcg_smem(bool tma) { return sizeof(float) * pcg_stage(NT, tma) + LS_PCG_PAD; }
 
 template <int NT>
 static void prepare_nt() {
@@ -1343,12 +1384,14 @@ void launch_pcg_xfinal(const Launch& L, int64_t M, float* xv, const float* p0, c
 
 void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
                        const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter,
-                       const Frame* band) {
-  (void)p;
-  (void)xv;
+                       const Frame* band, bool last) {
   const BandSpan bs = band_span(band);
   double* bsum = band ? band->bsum : nullptr;
-  k_pcg_update<<<L.grid, kThreads, 0, L.stream>>>(M, r, q, dinv, z, part, ticket, sc, iter, bs, bsum);
+  if (last && !band)
+    k_pcg_update<true><<<L.grid, kThreads, 0, L.stream>>>(M, r, q, dinv, z, part, ticket, sc, iter, bs, bsum, p, xv);
+  else
+    k_pcg_update<false><<<L.grid, kThreads, 0, L.stream>>>(M, r, q, dinv, z, part, ticket, sc, iter, bs, bsum, p,
+                                                           xv);
 }
 
 // band-ordered sum of the gathered partials [nbands][nv], then the same
@@ -1406,7 +1449,7 @@ int tile_box_w() { return kSW; }
 int tile_box_rw() { return kRW; }
 int update_grid_limit() {
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg_update, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg_update<false>, kThreads, 0);
   return nb;
 }
 

@@ -1,6 +1,7 @@
 """Timing ablations of k_pcg_apply: builds liblumisplit_b200 variants with
 -DLS_ABLATE=n into tools/_ablate/ (1: no consistency term, 2: no p formation,
-3: no smoothness, 4: no r-sparsity; n+100: the same with 4 CTAs/SM) and, with --run, times each through
+3: no smoothness, 4: no r-sparsity; n+100: the same with 4 CTAs/SM; 201: 2 CTAs/SM via a
+shared-memory pad; 202: the x-update loads issued before the stage barrier) and, with --run, times each through
 bench.py --profile-only.  Results are wrong by construction; timing only."""
 import json, os, subprocess, sys
 from pathlib import Path
@@ -16,7 +17,7 @@ def build_variant(n, extra=()):
     procs = []
     for src in B.SRC:
         obj = OUT / f"{src.stem}_{n}.o"
-        cmd = [B.NVCC, *B.ARCH, *B.FLAGS, f"-DLS_ABLATE={n % 100}", *extra, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
+        cmd = [B.NVCC, *B.ARCH, *B.FLAGS, f"-DLS_ABLATE={n % 100 if n < 200 else 0}", *extra, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         procs.append(subprocess.Popen(cmd)); objs.append(str(obj))
     assert all(p.wait() == 0 for p in procs)
     so = OUT / f"lib_{n}.so"
@@ -27,7 +28,14 @@ if __name__ == "__main__":
     variants = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 and sys.argv[1] != "--run" else [1, 2, 3, 4]
     if "--run" not in sys.argv:
         for n in variants:
-            build_variant(n, ["-DLS_PCG_MINB=4"] if n >= 100 else [])
+            extra = []
+            if 100 <= n < 200:
+                extra = ["-DLS_PCG_MINB=4"]
+            elif n == 201:      # occupancy pinned to 2 CTAs / SM (smem pad)
+                extra = ["-DLS_PCG_PAD=30000"]
+            elif n == 202:      # x-update loads issued before the stage barrier
+                extra = ["-DLS_XEARLY=1"]
+            build_variant(n, extra)
     else:
         for n in [0] + variants:
             env = dict(os.environ)

@@ -34,10 +34,16 @@ def to_bytes(v, unit):
 
 
 def main():
-    rep, launches, tag = sys.argv[1], sys.argv[2], sys.argv[3]
-    hdr, units, data = raw(rep)
-    ik = hdr.index("Kernel Name")
+    reps, launches, tag = sys.argv[1].split(","), sys.argv[2], sys.argv[3]
     per = defaultdict(list)
+    for rep in reps:
+        hdr, units, data = raw(rep)
+        collect(hdr, units, data, per)
+    finish(",".join(reps), per, launches, tag)
+
+
+def collect(hdr, units, data, per):
+    ik = hdr.index("Kernel Name")
     for r in data:
         name = r[ik].split("(")[0].replace("void ", "").strip()
         d = {}
@@ -56,6 +62,9 @@ def main():
                     except ValueError:
                         d[m] = val
         per[name].append(d)
+
+
+def finish(rep, per, launches, tag):
     summary = {}
     for name, lst in per.items():
         avg = {k: sum(x[k] for x in lst if isinstance(x.get(k), float)) / len(lst) for k in lst[0]}
@@ -93,11 +102,13 @@ def main():
         traffic[base] = avg["dram_bytes_per_launch"]
     (prof / "traffic.json").write_text(json.dumps(traffic, indent=1))
     md = [f"# ncu summary {tag}", "", f"report: `{rep}` (ncu --set full, --clock-control none)", "",
-          "| kernel | launches captured | duration us | DRAM bytes/launch | DRAM % peak | SM % | issue active % | regs |",
-          "|---|---|---|---|---|---|---|---|"]
-    for name, a in summary.items():
+          "| kernel | launches captured | duration us | DRAM bytes/launch | DRAM GB/s | DRAM % peak | SM % | "
+          "issue active % | regs |",
+          "|---|---|---|---|---|---|---|---|---|"]
+    for name, a in sorted(summary.items(), key=lambda kv: -kv[1].get("duration_us", 0)):
+        dur = a.get("duration_us", 0) or 1e-9
         md.append(f"| {name} | {a['captured_launches']} | {a.get('duration_us', 0):.1f} | "
-                  f"{a['dram_bytes_per_launch'] / 1e6:.1f} MB | "
+                  f"{a['dram_bytes_per_launch'] / 1e6:.1f} MB | {a['dram_bytes_per_launch'] / dur / 1e3:.0f} | "
                   f"{a.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 0):.1f} | "
                   f"{a.get('sm__throughput.avg.pct_of_peak_sustained_elapsed', 0):.1f} | "
                   f"{a.get('smsp__issue_active.avg.pct_of_peak_sustained_active', 0):.1f} | "
