@@ -413,7 +413,14 @@ def run_ours(args):
         host = [frames[1 + warmup + 2 * steps + i].cpu().pin_memory() for i in range(steps)]
         # the warm-up frames of the headline pass again, as pinned host frames
         host_warm = [frames[1 + i].cpu().pin_memory() for i in range(warmup)]
-        out_host = [torch.empty(tuple(st.layers.X.shape), dtype=torch.float32).pin_memory() for _ in range(2)]
+        # the step's result as the reference's arrays: r (H, W, 3) and T (H, W, K+1)
+        # (energy.py:74-94), interleaved on the device by the unpack kernel, then D2H
+        from paper_1908_01961_b200.energy import export_reference_layout
+        Hl, Wl = int(st.layers.X.shape[1]), int(st.layers.X.shape[2])
+        dev_r = [torch.empty((Hl, Wl, 3), dtype=torch.float32, device=dev) for _ in range(2)]
+        dev_T = [torch.empty((Hl, Wl, K + 1), dtype=torch.float32, device=dev) for _ in range(2)]
+        out_host = [(torch.empty((Hl, Wl, 3), dtype=torch.float32).pin_memory(),
+                     torch.empty((Hl, Wl, K + 1), dtype=torch.float32).pin_memory()) for _ in range(2)]
         side = torch.cuda.Stream(device=dev)
         main = torch.cuda.current_stream()
         up = torch.cuda.Stream(device=dev)
@@ -434,6 +441,7 @@ def run_ours(args):
                 return t, ev
 
             n = len(hf)
+            copied = [None, None]
             e0.record()
             up.wait_stream(main)
             nxt = upload(0)
@@ -447,13 +455,17 @@ def run_ours(args):
                     nxt = (hf[i + 1].to(dev, non_blocking=True), torch.cuda.Event())
                     nxt[1].record(main)
                 s2 = dec.step(fdev)
+                if copied[i % 2] is not None:       # frame i-2's read-back of this buffer pair
+                    main.wait_event(copied[i % 2])
+                export_reference_layout(s2.layers, dev_r[i % 2], dev_T[i % 2])
                 done = torch.cuda.Event()
                 done.record()
                 side.wait_event(done)
                 with torch.cuda.stream(side):
-                    X = s2.layers.X
-                    X.record_stream(side)
-                    out_host[i % 2].copy_(X, non_blocking=True)
+                    out_host[i % 2][0].copy_(dev_r[i % 2], non_blocking=True)
+                    out_host[i % 2][1].copy_(dev_T[i % 2], non_blocking=True)
+                    copied[i % 2] = torch.cuda.Event()
+                    copied[i % 2].record(side)
             main.wait_stream(side)
             e1.record()
             torch.cuda.synchronize()
@@ -469,8 +481,9 @@ def run_ours(args):
             eth = clips.aggregate(steps if rank == 0 else 0, e_ms / 1e3)
         e2e = {"value": eth.fps, "unit": UNIT,
                "h2d_bytes_per_step": int(host[0].numel() * 4),
-               "d2h_bytes_per_step": int(out_host[0].numel() * 4),
-               "api": "pipeline.StreamingDecomposer.step (reference decompose_frames loop); "
+               "d2h_bytes_per_step": int((out_host[0][0].numel() + out_host[0][1].numel()) * 4),
+               "api": "pipeline.StreamingDecomposer.step (reference decompose_frames loop); the result "
+                      "as the reference's r (H,W,3) and T (H,W,K+1) arrays (unpacked on the device); "
                       "frame i+1's H2D and frame i's D2H on copy streams beside frame i's / i+1's solve"}
 
     # --- a whole 300-frame clip through decompose_frames,

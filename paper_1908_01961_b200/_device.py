@@ -214,6 +214,13 @@ class DeviceSolver:
                                            out.ctypes.data_as(L.DBL_P)))
         return out
 
+    def unpack_hwc(self, planes: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        """(C, H, W) planes -> (H, W, C) interleaved (ls_unpack_hwc), on the
+        current stream."""
+        self._enter()
+        self._chk(self.lib.ls_unpack_hwc(self.ctx, L.dptr(planes), int(planes.shape[0]), L.dptr(out)))
+        return out
+
     # -- per-block residual protocol (ls_block_*, energy.py:194-452) ------------
     def block_rows(self, block: int, n_pairs: int) -> int:
         n = C.c_int64()

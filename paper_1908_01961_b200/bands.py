@@ -157,11 +157,17 @@ class LocalExchange:
 
     def halo(self, tensors: list[torch.Tensor], full: bool = False):
         """tensors[i]: (U, H_loc, W) local tensor of band i.  Refreshes the
-        halo rows the kernels read (halo_pieces); full=True copies the whole
-        HALO rows of every plane."""
+        halo rows the kernels read: on one device a copy costs a launch more
+        than its bytes, so each move is ONE copy of the R_HALO rows next to
+        the boundary in every plane (covering halo_pieces); full=True copies
+        the whole HALO rows."""
         for mv in halo_moves(self.bands):
             src, dst = self.bands[mv[0]], self.bands[mv[1]]
-            pieces = [(0, None, mv[2], mv[3])] if full else halo_pieces(mv)
+            if full:
+                pieces = [(0, None, mv[2], mv[3])]
+            else:
+                rows = halo_pieces(mv)[0]
+                pieces = [(0, None, rows[2], rows[3])]
             for p0, p1, g0, g1 in pieces:
                 piece = tensors[mv[0]][p0:p1, g0 - src.ya:g1 - src.ya]
                 tensors[mv[1]][p0:p1, g0 - dst.ya:g1 - dst.ya].copy_(piece, non_blocking=True)

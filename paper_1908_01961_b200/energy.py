@@ -126,6 +126,21 @@ class LayerStack:
         return LayerStack(planes=self.X.clone())
 
 
+def export_reference_layout(layers: LayerStack, out_r: torch.Tensor | None = None,
+                            out_T: torch.Tensor | None = None):
+    """The reference's arrays of a layer stack -- r (H, W, 3) and T (H, W, K+1),
+    interleaved as NumPy C order (energy.py:74-94) -- written on the device by
+    one unpack kernel per array (contiguous, ready for a host copy)."""
+    X = layers.X
+    H, W = layers.shape
+    out_r = out_r if out_r is not None else torch.empty((H, W, 3), dtype=torch.float32, device=X.device)
+    out_T = out_T if out_T is not None else torch.empty((H, W, layers.K + 1), dtype=torch.float32, device=X.device)
+    s = _device.get_solver(X.device, H, W, layers.K)
+    s.unpack_hwc(X[:3], out_r)
+    s.unpack_hwc(X[3:], out_T)
+    return out_r, out_T
+
+
 def reconstruct(layers: LayerStack, palette: BaseColorPalette) -> torch.Tensor:
     """energy.py:97-99."""
     return layers.reflectance * layers.illumination(palette)

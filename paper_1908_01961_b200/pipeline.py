@@ -215,6 +215,16 @@ def decompose_frames(frames: list, weights: EnergyWeights, config: SolveConfig, 
     return result
 
 
+def decompose_bundle(bundle, weights: EnergyWeights, config: SolveConfig, seed: int = 0, k_max: int = 10,
+                     clicks: list | None = None):
+    """pipeline.py:170-177: decompose_frames over a ground-truth bundle's
+    frames (any object with `.frames`, e.g. the reference's
+    GroundTruthBundle or synth.Clip); returns (reflectances,
+    illuminations, palette, result)."""
+    result = decompose_frames(list(bundle.frames), weights, config, seed=seed, k_max=k_max, clicks=clicks)
+    return result.reflectances(), result.illuminations(), result.palette, result
+
+
 # disk-to-disk pipeline and per-frame outputs (pipeline.py:183-270)
 from .frameio import (find_frames, run_pipeline, write_diagnostics,  # noqa: E402,F401
                       write_frame_outputs)

@@ -40,3 +40,17 @@ def test_estimate_palette_errors():
     img = torch.rand(16, 16, 3, device="cuda")
     with pytest.raises(ValueError):
         estimate_palette(Frame(img), k_max=0)
+
+
+def test_decompose_bundle_returns_layers_and_palette():
+    """pipeline.py:170-177 over a synthetic bundle (palette estimated on the
+    device from frame 1)."""
+    from paper_1908_01961_b200 import synth
+    from paper_1908_01961_b200.energy import EnergyWeights
+    from paper_1908_01961_b200.pipeline import decompose_bundle
+    from paper_1908_01961_b200.solver import SolveConfig
+    clip = synth.make_clip(48, 64, 3, 3, seed=4, device="cuda")
+    refl, illum, pal, res = decompose_bundle(clip, EnergyWeights(), SolveConfig(outer_iterations=3), k_max=4)
+    assert len(refl) == len(illum) == 3 and pal.K >= 1
+    assert tuple(refl[0].shape) == (48, 64, 3) and tuple(illum[0].shape) == (48, 64, 3)
+    assert all(np.isfinite(r["energy_after"]) for rs in res.records for r in rs)
