@@ -123,6 +123,10 @@ struct ls_ctx {
   double* pal_chroma = nullptr;
   // PCG workspace
   float *r = nullptr, *d = nullptr, *u = nullptr, *wv = nullptr, *p = nullptr, *s = nullptr, *x = nullptr;
+  // single-reduction PCG (LS_PCG=cg1 at context creation): two more vectors
+  bool pcg_cg1 = false;
+  int grid_cg = 0;
+  float *cg_m1 = nullptr, *cg_t1 = nullptr;
   double* part = nullptr;
   size_t part_len = 0;
   unsigned* tickets = nullptr;
@@ -301,6 +305,12 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   c->y_hi = H;
   set_geometry(c);
   c->use_tma = (W % 4 == 0) && tma_encode_fn() != nullptr && std::getenv("LS_NO_TMA") == nullptr;
+  {   // opt-in single-reduction PCG (whole frames with TMA only)
+    const char* pv = std::getenv("LS_PCG");
+    c->pcg_cg1 = pv && std::string(pv) == "cg1" && c->use_tma;
+    if (c->pcg_cg1)
+      c->grid_cg = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, cg_grid_limit(c->NT)), kMaxBlocks}));
+  }
   cudaError_t e = cudaSuccess;
 #define A_(expr) \
   if (e == cudaSuccess) e = (expr)
@@ -332,6 +342,10 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   for (float** v : {&c->r, &c->d, &c->u, &c->wv, &c->p, &c->s, &c->x}) A_(dalloc(c, v, (size_t)M));
   c->part_len = std::max<size_t>((size_t)kMaxBlocks * 12, (size_t)c->grid_dense * 320);
   A_(dalloc(c, &c->part, c->part_len));
+  if (c->pcg_cg1) {
+    A_(dalloc(c, &c->cg_m1, (size_t)M));
+    A_(dalloc(c, &c->cg_t1, (size_t)M));
+  }
   A_(dalloc(c, &c->tickets, 8));
   A_(dalloc(c, &c->sc, 1));
   A_(dalloc(c, &c->dense_sums, 512));
@@ -968,10 +982,57 @@ static bool pcg_maps(ls_ctx* c, const float* X, const float* pprev, PcgMaps* m) 
          make_map(&m->PR, pprev, W, H, 3, tile_box_rw(), kTileH + 2 * kHalf);
 }
 
+// single-reduction PCG (k_cg_iter): EG (r, dinv, u_0, gamma_0), then
+// w_0 = A u_0, then one kernel per iteration.  Ping-pong buffers: u {u, r},
+// m {wv, cg_m1}, t {s, cg_t1}; p in place.
+static int run_pcg_cg1(ls_ctx* c, const double* colors, const float* X, int iters, float* x,
+                       const FrameCtl* ctl) {
+  const Frame f = frame_of(c);
+  const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
+  size_t pi = prof_begin(c);
+  EnergyMaps em;
+  const bool etma = energy_maps(c, X, nullptr, &em);
+  launch_energy(0, L_energy(c), f, cd, X, nullptr, 0.f, nullptr, nullptr, c->r, c->d, c->u, nullptr, nullptr,
+                c->part, c->tickets + 0, c->sc, etma ? &em : nullptr, ctl);
+  prof_end(c, PC_EG, pi);
+  const int W = c->W, H = c->H, U = c->U, NT = c->NT;
+  const size_t N = (size_t)c->N;
+  float* ub[2] = {c->u, c->r};
+  float* mb[2] = {c->wv, c->cg_m1};
+  float* tb[2] = {c->s, c->cg_t1};
+  auto maps_for = [&](const float* uin, const float* min, const float* tin, CgMaps* m) {
+    return make_map(&m->X, X, W, H, U, tile_box_w(), kTileH + 2) &&
+           make_map(&m->UT, uin + 3 * N, W, H, NT, tile_box_w(), kTileH + 2) &&
+           make_map(&m->UR, uin, W, H, 3, tile_box_rw(), kTileH + 2 * kHalf) &&
+           make_map(&m->MT, min + 3 * N, W, H, NT, tile_box_w(), kTileH + 2) &&
+           make_map(&m->MR, min, W, H, 3, tile_box_rw(), kTileH + 2 * kHalf) &&
+           make_map(&m->TT, tin + 3 * N, W, H, NT, tile_box_w(), kTileH + 2) &&
+           make_map(&m->TR, tin, W, H, 3, tile_box_rw(), kTileH + 2 * kHalf);
+  };
+  CgMaps maps[2];   // by iteration parity: u_i = ub[i&1], m_i = mb[i&1], t_{i-1} = tb[(i+1)&1]
+  LS_ARG(maps_for(ub[0], mb[0], tb[1], &maps[0]) && maps_for(ub[1], mb[1], tb[0], &maps[1]),
+         "TMA descriptors for the single-reduction PCG");
+  const Launch Lc{c->grid_cg, c->ntiles, c->stream};
+  pi = prof_begin(c);
+  launch_cg(Lc, 0, f, cd, X, c->d, nullptr, mb[0], nullptr, c->p, x, c->part, c->tickets + 1, c->sc, 0, maps[0]);
+  prof_end(c, PC_APPLY, pi);
+  for (int it = 0; it < iters; ++it) {
+    pi = prof_begin(c);
+    launch_cg(Lc, it == iters - 1 ? 2 : 1, f, cd, X, c->d, ub[(it + 1) & 1], mb[(it + 1) & 1], tb[it & 1], c->p, x,
+              c->part, c->tickets + 1, c->sc, it, maps[it & 1]);
+    prof_end(c, PC_APPLY, pi);
+  }
+  launch_pcg_xfinal(L_update(c), (int64_t)U * c->N, x, c->p, c->s, c->sc, c->tickets + 4);   // no-op (pending = 0)
+  c->launches += 3 + iters;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
 // fused energy/gradient + textbook PCG loop (solver.py:79-107); x receives the step.
 // Buffers: r, d = 1/diag, u = z = r/diag, wv = q = A p, p / s = ping-pong p.
 static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, float* x,
                    const FrameCtl* ctl = nullptr) {
+  if (c->pcg_cg1 && !c->band_partial) return run_pcg_cg1(c, colors, X, iters, x, ctl);
   const Frame f = frame_of(c);
   const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
   size_t pi = prof_begin(c);

@@ -127,45 +127,50 @@ __global__ void __launch_bounds__(128) k_dense_accum(Frame f, const double* __re
 }
 
 // ---- k_dense_accum2: the same sums with per-thread register accumulation --
-// A CTA of 128 threads takes chunks of 64 pixels.  Phase 1: threads 0..63
-// compute their pixel's values -- v_c[k] = R_c T_{k+1} (3K), the data
-// residual res_c (3), r_c (3) and the cluster id -- into shared memory.
-// Phase 2: thread t runs job t % 64 over half (t / 64) of the chunk's pixels:
-// jobs 0..3K-1 are one row (c, k) of the data block, accumulating
+// Every warp works alone (no CTA barrier inside the loop): it takes 32
+// pixels at a time; lane l computes pixel l's values -- v_c[k] = R_c T_{k+1}
+// (3K), the data residual res_c (3), r_c (3) and the cluster id -- into the
+// warp's shared-memory rows; then lane l runs job(s) l (+32) over the 32
+// pixels: jobs 0..3K-1 are one row (c, k) of the data block, accumulating
 // v_c[k] v_c[j] for every j (the lower part is dropped at the end) and
 // v_c[k] res_c; jobs 3K..4K-1 are cluster k's count and r sums.  All
-// accumulation is in registers; one fixed-order reduction per CTA, then the
-// last CTA sums the CTA partials in CTA order.
-constexpr int kDa2Threads = 128, kDa2Chunk = 64;
+// accumulation is in registers (fp64); one fixed-order reduction per CTA,
+// then the last CTA sums the CTA partials in CTA order.
+constexpr int kDa2Threads = 128, kDa2Warps = kDa2Threads / 32;
 
 template <int K>
-__global__ void __launch_bounds__(kDa2Threads) k_dense_accum2(Frame f, const double* __restrict__ colors,
+__global__ void __launch_bounds__(kDa2Threads, 4) k_dense_accum2(Frame f, const double* __restrict__ colors,
                                                               const float* __restrict__ X, int use_ids,
                                                               double* part, unsigned* ticket, double* sums) {
   constexpr int NT = K + 1, NV = 3 * K + 7;   // per pixel: v (3K), res (3), r (3), id
   constexpr int NS = 3 * (K * (K + 1) / 2) + 7 * K, NM = 3 * (K * (K + 1) / 2);
   constexpr int NA = K + 1 > 4 ? K + 1 : 4;   // accumulators: a data row + rhs, or 4 cluster sums
-  constexpr int PS = NV | 1;   // odd row stride (doubles): phase-1 row writes are 2-way, not 32-way, banked
-  __shared__ double pix[kDa2Chunk][PS];
-  __shared__ double red[kDa2Threads][NA];
+  constexpr int NJ = 4 * K, JPL = (NJ + 31) / 32;   // jobs, jobs per lane
+  constexpr int PS = NV | 1;   // odd row stride (doubles): the row writes are 2-way, not 32-way, banked
+  // the pixel rows and, after the loop, the per-warp job sums share storage
+  constexpr int kPixD = kDa2Warps * 32 * PS, kRedD = kDa2Warps * NJ * NA;
+  __shared__ double shm[kPixD > kRedD ? kPixD : kRedD];
+  double (*pix)[32][PS] = reinterpret_cast<double (*)[32][PS]>(shm);
   __shared__ double B[NT][3];
   if (threadIdx.x < NT * 3) {
     const int k = threadIdx.x / 3, c = threadIdx.x % 3;
     B[k][c] = k == 0 ? 1.0 : colors[3 * (k - 1) + c];
   }
-  const int N = f.N;
-  const int i0 = f.y_lo * f.W, npx = (f.y_hi - f.y_lo) * f.W;
-  const int job = threadIdx.x % kDa2Chunk, half = threadIdx.x / kDa2Chunk;
-  const bool row_job = job < 3 * K, cl_job = job >= 3 * K && job < 4 * K;
-  const int jc = row_job ? job / K : 0, jk = row_job ? job % K : (cl_job ? job - 3 * K : 0);
-  double acc[NA];
-#pragma unroll
-  for (int j = 0; j < NA; ++j) acc[j] = 0.0;
   __syncthreads();
-  for (int c0 = blockIdx.x * kDa2Chunk; c0 < npx; c0 += gridDim.x * kDa2Chunk) {
-    if (threadIdx.x < kDa2Chunk) {
-      double* pv = pix[threadIdx.x];
-      const int q = c0 + threadIdx.x;
+  const int N = f.N;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int i0 = f.y_lo * f.W, npx = (f.y_hi - f.y_lo) * f.W;
+  double acc[JPL][NA];
+#pragma unroll
+  for (int q = 0; q < JPL; ++q)
+#pragma unroll
+    for (int j = 0; j < NA; ++j) acc[q][j] = 0.0;
+  double (*wp)[PS] = pix[wid];
+  const int gw = blockIdx.x * kDa2Warps + wid, nw = gridDim.x * kDa2Warps;
+  for (int c0 = gw * 32; c0 < npx; c0 += nw * 32) {
+    {   // lane = pixel
+      double* pv = wp[lane];
+      const int q = c0 + lane;
       if (q < npx) {
         const int i = i0 + q;
         double t[NT];
@@ -185,50 +190,70 @@ __global__ void __launch_bounds__(kDa2Threads) k_dense_accum2(Frame f, const dou
         }
         pv[3 * K + 6] = (use_ids && f.ids) ? (double)f.ids[i] : 0.0;
       } else {
+#pragma unroll
         for (int v = 0; v < NV; ++v) pv[v] = 0.0;
       }
     }
-    __syncthreads();
-    const int qn = min(kDa2Chunk / 2, max(0, npx - c0 - half * (kDa2Chunk / 2)));
-    const double* base = pix[half * (kDa2Chunk / 2)];
-    if (row_job) {
-      for (int q = 0; q < qn; ++q) {
-        const double* pv = base + q * PS;
-        const double a = pv[jc * K + jk];
+    __syncwarp();
+    const int qn = min(32, npx - c0);
 #pragma unroll
-        for (int j = 0; j < K; ++j) acc[j] = fma(a, pv[jc * K + j], acc[j]);
-        acc[K] = fma(a, pv[3 * K + jc], acc[K]);
-      }
-    } else if (cl_job) {
-      const double id = (double)(jk + 1);
-      for (int q = 0; q < qn; ++q) {
-        const double* pv = base + q * PS;
-        if (pv[3 * K + 6] == id) {
-          acc[0] += 1.0;
-          acc[1] += pv[3 * K + 3];
-          acc[2] += pv[3 * K + 4];
-          acc[3] += pv[3 * K + 5];
+    for (int qj = 0; qj < JPL; ++qj) {   // lane = job
+      const int job = lane + 32 * qj;
+      if (job < 3 * K) {
+        const int jc = job / K, jk = job % K;
+        for (int q = 0; q < qn; ++q) {
+          const double* pv = wp[q];
+          const double a = pv[jc * K + jk];
+#pragma unroll
+          for (int j = 0; j < K; ++j) acc[qj][j] = fma(a, pv[jc * K + j], acc[qj][j]);
+          acc[qj][K] = fma(a, pv[3 * K + jc], acc[qj][K]);
+        }
+      } else if (job < NJ) {
+        const double id = (double)(job - 3 * K + 1);
+        for (int q = 0; q < qn; ++q) {
+          const double* pv = wp[q];
+          if (pv[3 * K + 6] == id) {
+            acc[qj][0] += 1.0;
+            acc[qj][1] += pv[3 * K + 3];
+            acc[qj][2] += pv[3 * K + 4];
+            acc[qj][3] += pv[3 * K + 5];
+          }
         }
       }
     }
-    __syncthreads();
+    __syncwarp();
   }
-  // CTA reduction: the two halves of each job, then the sums layout of
-  // dense_ns (M_c upper triangle, rhs_c, n_k, sum r_c over cluster k)
+  // CTA reduction (warps in order) into the sums layout of dense_ns
+  // (M_c upper triangle, rhs_c, n_k, sum r_c over cluster k)
+  double (*red)[NJ][NA] = reinterpret_cast<double (*)[NJ][NA]>(shm);
+  __syncthreads();   // every warp is done with its pixel rows
 #pragma unroll
-  for (int j = 0; j < NA; ++j) red[threadIdx.x][j] = acc[j];
+  for (int qj = 0; qj < JPL; ++qj) {
+    const int job = lane + 32 * qj;
+    if (job < NJ)
+#pragma unroll
+      for (int j = 0; j < NA; ++j) red[wid][job][j] = acc[qj][j];
+  }
   __syncthreads();
-  if (threadIdx.x < kDa2Chunk) {
-    double* out = part + (size_t)blockIdx.x * NS;
-    if (row_job) {
+  double* out = part + (size_t)blockIdx.x * NS;
+  for (int job = threadIdx.x; job < NJ; job += kDa2Threads) {
+    double v[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+      double sacc = 0.0;
+      for (int w = 0; w < kDa2Warps; ++w) sacc += red[w][job][j];
+      v[j] = sacc;
+    }
+    if (job < 3 * K) {
+      const int jc = job / K, jk = job % K;
       int off = 0;
       for (int kk = 0; kk < jk; ++kk) off += K - kk;
-      for (int j = jk; j < K; ++j)
-        out[jc * (K * (K + 1) / 2) + off + (j - jk)] = red[job][j] + red[job + kDa2Chunk][j];
-      out[NM + jc * K + jk] = red[job][K] + red[job + kDa2Chunk][K];
-    } else if (cl_job) {
-      out[NM + 3 * K + jk] = red[job][0] + red[job + kDa2Chunk][0];
-      for (int c = 0; c < 3; ++c) out[NM + 4 * K + 3 * jk + c] = red[job][1 + c] + red[job + kDa2Chunk][1 + c];
+      for (int j = jk; j < K; ++j) out[jc * (K * (K + 1) / 2) + off + (j - jk)] = v[j];
+      out[NM + jc * K + jk] = v[K];
+    } else {
+      const int jk = job - 3 * K;
+      out[NM + 3 * K + jk] = v[0];
+      for (int c = 0; c < 3; ++c) out[NM + 4 * K + 3 * jk + c] = v[1 + c];
     }
   }
   __shared__ bool is_last;
@@ -239,9 +264,9 @@ __global__ void __launch_bounds__(kDa2Threads) k_dense_accum2(Frame f, const dou
   if (!is_last) return;
   __threadfence();
   for (int e = threadIdx.x; e < NS; e += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) s += ((volatile double*)part)[(size_t)b * NS + e];
-    sums[e] = s;
+    double s2 = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) s2 += ((volatile double*)part)[(size_t)b * NS + e];
+    sums[e] = s2;
   }
   if (threadIdx.x == 0) *ticket = 0u;
 }

@@ -28,6 +28,12 @@ struct PcgMaps {
   CUtensorMap X, ZT, ZR, PT, PR;
 };
 
+// single-reduction PCG (k_cg_iter): state X, operands u (T 1 halo, r 7 halo),
+// m and t (same boxes)
+struct CgMaps {
+  CUtensorMap X, UT, UR, MT, MR, TT, TR;
+};
+
 struct Launch {
   int grid;
   int ntiles;
@@ -57,6 +63,11 @@ void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, con
                        const Frame* band = nullptr, bool last = false);
 void launch_pcg_xfinal(const Launch& L, int64_t M, float* xv, const float* p0, const float* p1, Scalars* sc,
                        unsigned* ticket, const Frame* band = nullptr);
+// single-reduction PCG: mode 0 init (w_0 = A u_0), 1 iteration, 2 last iteration
+void launch_cg(const Launch& L, int mode, const Frame& f, const Coef<float>& c, const float* X, const float* dinv,
+               float* u_out, float* m_out, float* t_out, float* p, float* xv, double* part, unsigned* ticket,
+               Scalars* sc, int iter, const CgMaps& maps);
+int cg_grid_limit(int NT);
 // row bands: phases whose partial sums are gathered across bands
 enum BandPhase { BAND_EG = 0, BAND_APPLY = 1, BAND_UPDATE = 2, BAND_TRIAL = 3, BAND_DENSE = 4 };
 void launch_band_sum(cudaStream_t s, const double* gathered, int nbands, int nv, double* out);

@@ -653,10 +653,13 @@ __device__ __forceinline__ PixPre pix_prefetch(const Frame& f, int x, int y, boo
   return p;
 }
 
-template <int NT, bool IN>
+// SCALE (the single-reduction PCG, k_cg_iter): the stored value is w * dinv
+// (the preconditioned product M w); the returned <w, u> is of the unscaled w
+template <int NT, bool IN, bool SCALE = false>
 __device__ __forceinline__ float apply_pixel(const Frame& f, const Coef<float>& c, const float* sX, const float* sT,
                                              const float* sR, float* __restrict__ w, int x, int y, int cx, int cy,
-                                             int rx, int ry, const PixPre& pre) {
+                                             int rx, int ry, const PixPre& pre,
+                                             const float* __restrict__ dinv = nullptr) {
   const int W = f.W, H = f.H, N = f.N;
   const int i = y * W + x;
   const bool hx = IN || x < W - 1, hy = IN || y < H - 1, hl = IN || x > 0, hu = IN || y > 0;
@@ -715,7 +718,7 @@ __device__ __forceinline__ float apply_pixel(const Frame& f, const Coef<float>& 
     if (hu) sm = fmaf(irls1f(v - P[-kSW], c), uv - Q[-kSW], sm);
     }
     a = fmaf(c.lam_sm, sm, a);
-    w[(size_t)(3 + k) * N + i] = a;
+    w[(size_t)(3 + k) * N + i] = SCALE ? a * __ldg(dinv + (size_t)(3 + k) * N + i) : a;
     dot = fmaf(a, uv, dot);
   }
   // r-sparsity D^T W D u_r, one weight per pixel shared by the channels
@@ -789,7 +792,7 @@ __device__ __forceinline__ float apply_pixel(const Frame& f, const Coef<float>& 
   }
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
-    w[(size_t)ch * N + i] = outr[ch];
+    w[(size_t)ch * N + i] = SCALE ? outr[ch] * __ldg(dinv + (size_t)ch * N + i) : outr[ch];
     dot = fmaf(outr[ch], ur[ch], dot);
   }
   return dot;
@@ -1052,6 +1055,208 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
   if (threadIdx.x == 0) {
     if (f.bsum) f.bsum[0] = pap;
     else fin_pcg_apply(pap, sc);
+    *ticket = 0u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Single-reduction PCG (Chronopoulos-Gear form of solver.py:79-107, the
+// north star's "one grid-level reduction per PCG step"), ONE kernel per
+// iteration, in preconditioned variables (M = diag^-1 = dinv):
+//   u = M r,  m = M w (w = A u),  t = M s (s = w + beta s)
+//   iteration i:  t_i = m_i + beta_i t_{i-1};  u_{i+1} = u_i - alpha_i t_i
+//                 p_i = u_i + beta_i p_{i-1};   x += alpha_i p_i
+//                 w_{i+1} = A u_{i+1},  m_{i+1} = M w_{i+1}
+//                 gamma = (r, u) = sum u^2 / dinv,  delta = (w, u),  |r|^2
+//   last CTA:     beta = gamma_{i+1} / gamma_i,
+//                 pAp = delta - beta gamma_{i+1} / alpha_i,  alpha = gamma_{i+1} / pAp
+// The three operands u_i, m_i, t_{i-1} are staged over tile + halo (t and
+// u_{i+1} are formed over the whole window), so the stencil of u_{i+1} needs
+// no second pass: 12U HBM words per pixel per iteration -- the same as the
+// two-kernel textbook loop -- and one fp64 reduction of (delta, gamma, |r|^2).
+// The textbook loop's breaks map one to one: gamma_{i+1} <= 0 is its
+// rz_new <= 0 after update i, pAp_{i+1} <= 0 its pAp <= 0 before update i+1.
+// Three operand windows are 100 KB of shared memory per CTA (2 CTAs / SM).
+// CG_INIT: w_0 = A u_0, m_0 = M w_0, delta_0 (gamma_0 comes from EG).
+// ---------------------------------------------------------------------------
+enum { CG_INIT = 0, CG_ITER = 1, CG_LAST = 2 };
+__host__ __device__ constexpr int cg_stage(int NT) { return pad32((NT + 3) * kSP) + 3 * op_floats(NT); }
+
+template <int NT>
+__device__ __forceinline__ void tma_issue_cg(float* stage, const CgMaps& m, uint64_t* bar, int tx0, int ty0,
+                                             int mode, bool with_t) {
+  constexpr uint32_t xb = sizeof(float) * (NT + 3) * kSP;
+  constexpr uint32_t ob = sizeof(float) * (NT * kSP + 3 * kRP);
+  const int nop = mode == CG_INIT ? 1 : (with_t ? 3 : 2);
+  mbar_expect_tx(bar, xb + nop * ob);
+  float* o = stage + pad32((NT + 3) * kSP);
+  tma_load_3d(stage, &m.X, bar, tx0 - kSX, ty0 - 1, 0);
+  tma_load_3d(o, &m.UT, bar, tx0 - kSX, ty0 - 1, 0);
+  tma_load_3d(o + pad32(NT * kSP), &m.UR, bar, tx0 - kRX, ty0 - kHalf, 0);
+  if (mode != CG_INIT) {
+    o += op_floats(NT);
+    tma_load_3d(o, &m.MT, bar, tx0 - kSX, ty0 - 1, 0);
+    tma_load_3d(o + pad32(NT * kSP), &m.MR, bar, tx0 - kRX, ty0 - kHalf, 0);
+    if (with_t) {
+      o += op_floats(NT);
+      tma_load_3d(o, &m.TT, bar, tx0 - kSX, ty0 - 1, 0);
+      tma_load_3d(o + pad32(NT * kSP), &m.TR, bar, tx0 - kRX, ty0 - kHalf, 0);
+    }
+  }
+}
+
+template <int NT, int MODE>
+__global__ void __launch_bounds__(kThreads, 2) k_cg_iter(Frame f, Coef<float> c, const float* __restrict__ X,
+                                                         const float* __restrict__ dinv, float* __restrict__ u_out,
+                                                         float* __restrict__ m_out, float* __restrict__ t_out,
+                                                         float* __restrict__ p, float* __restrict__ xv, double* part,
+                                                         unsigned* ticket, Scalars* sc, int iter, int ntiles,
+                                                         const __grid_constant__ CgMaps maps) {
+  constexpr int U = NT + 3;
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t bar;
+  if (sc->stop) return;
+  const int W = f.W, N = f.N;
+  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+  const int cx = lx + kSX, cy = ly + 1, rx = lx + kRX, ry = ly + kHalf;
+  const int ntx = (W + kTileW - 1) / kTileW;
+  const bool with_t = MODE != CG_INIT && iter > 0;
+  const float alpha = (float)sc->alpha, beta = (float)sc->beta;
+  const bool xread = sc->xinit;
+  float* sX = smem;
+  float* sUT = smem + pad32(U * kSP);
+  float* sUR = sUT + pad32(NT * kSP);
+  float* sMT = sUT + op_floats(NT);
+  float* sTT = sMT + op_floats(NT);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+    if ((int)blockIdx.x < ntiles) {
+      const int t = blockIdx.x;
+      tma_issue_cg<NT>(smem, maps, &bar, (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH, MODE, with_t);
+    }
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  double acc[3] = {0.0, 0.0, 0.0};   // delta = <w, u>, gamma = <r, u>, |r|^2
+  for (int j = 0;; ++j) {
+    const int tile = blockIdx.x + j * gridDim.x;
+    if (tile >= ntiles) break;
+    const int tx0 = (tile % ntx) * kTileW, ty0 = f.y_lo + (tile / ntx) * kTileH;
+    const int x = tx0 + lx, y = ty0 + ly;
+    const bool own = x < W && y < f.y_hi;
+    const size_t i = (size_t)y * W + x;
+    const PixPre pre = pix_prefetch(f, x, y, own);
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+    const int sc0 = cy * kSW + cx, rc0 = ry * kRW + rx;
+    if (MODE != CG_INIT) {
+      float ui[U];     // u_i of the own pixel, before the window is advanced
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) ui[ch] = sUR[ch * kRP + rc0];
+#pragma unroll
+      for (int k = 0; k < NT; ++k) ui[3 + k] = sUT[k * kSP + sc0];
+      __syncthreads();
+      // t_i = m_i + beta t_{i-1};  u_{i+1} = u_i - alpha t_i  over tile + halo
+      static_assert((NT * kSP) % 4 == 0 && (3 * kRP) % 4 == 0, "float4 formation");
+      constexpr int n4 = op_floats(NT) / 4;
+      float4* u4 = reinterpret_cast<float4*>(sUT);
+      float4* m4 = reinterpret_cast<float4*>(sMT);
+      const float4* t4 = reinterpret_cast<const float4*>(sTT);
+      for (int e = threadIdx.x; e < n4; e += kThreads) {
+        float4 tt = m4[e];
+        if (with_t) {
+          const float4 tp = t4[e];
+          tt.x = fmaf(beta, tp.x, tt.x); tt.y = fmaf(beta, tp.y, tt.y);
+          tt.z = fmaf(beta, tp.z, tt.z); tt.w = fmaf(beta, tp.w, tt.w);
+        }
+        float4 uu = u4[e];
+        uu.x = fmaf(-alpha, tt.x, uu.x); uu.y = fmaf(-alpha, tt.y, uu.y);
+        uu.z = fmaf(-alpha, tt.z, uu.z); uu.w = fmaf(-alpha, tt.w, uu.w);
+        m4[e] = tt;     // t_i now lives in the m region
+        u4[e] = uu;
+      }
+      __syncthreads();
+      if (own) {   // p_i = u_i + beta p_{i-1};  x += alpha p_i;  t_i, u_{i+1} out
+        float pv[U], xo[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          pv[u] = iter > 0 ? __ldg(p + (size_t)u * N + i) : 0.f;
+          xo[u] = xread ? xv[(size_t)u * N + i] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float pn = iter > 0 ? fmaf(beta, pv[u], ui[u]) : ui[u];
+          p[(size_t)u * N + i] = pn;
+          xv[(size_t)u * N + i] = fmaf(alpha, pn, xo[u]);
+        }
+        double gm = 0.0, rn = 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool isr = u < 3;
+          const float tv = isr ? sMT[pad32(NT * kSP) + u * kRP + rc0] : sMT[(u - 3) * kSP + sc0];
+          const float uv = isr ? sUR[u * kRP + rc0] : sUT[(u - 3) * kSP + sc0];
+          if (MODE == CG_ITER) {
+            t_out[(size_t)u * N + i] = tv;
+            u_out[(size_t)u * N + i] = uv;
+          }
+          const float rv = __fdividef(uv, __ldg(dinv + (size_t)u * N + i));   // r = u / dinv
+          gm += (double)(rv * uv);
+          rn += (double)(rv * rv);
+        }
+        acc[1] += gm;
+        acc[2] += rn;
+      }
+    }
+    if (MODE != CG_LAST) {   // w = A u (u_{i+1}, or u_0 in CG_INIT); m = dinv w written
+      const bool interior = tx0 > 0 && ty0 > 0 && tx0 + kTileW < W && ty0 + kTileH < f.H && ty0 + kTileH <= f.y_hi;
+      float d = 0.f;
+      if (interior)
+        d = apply_pixel<NT, true, true>(f, c, sX, sUT, sUR, m_out, x, y, cx, cy, rx, ry, pre, dinv);
+      else if (own)
+        d = apply_pixel<NT, false, true>(f, c, sX, sUT, sUR, m_out, x, y, cx, cy, rx, ry, pre, dinv);
+      acc[0] += (double)d;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int t = blockIdx.x + (j + 1) * gridDim.x;
+      if (t < ntiles) tma_issue_cg<NT>(smem, maps, &bar, (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH, MODE, with_t);
+    }
+  }
+  block_reduce_store<3>(acc, part);
+  if (!last_block(ticket)) return;
+  const double delta = sum_partials<3>(part, gridDim.x, 0);
+  const double gamma = sum_partials<3>(part, gridDim.x, 1);
+  const double rn = sum_partials<3>(part, gridDim.x, 2);
+  if (threadIdx.x == 0) {
+    if (MODE == CG_INIT) {   // p_0 = u_0: pAp_0 = delta_0 (solver.py:94-96)
+      sc->delta = delta;
+      if (!(delta > 0.0) || !isfinite(delta)) sc->stop = 1;
+      else { sc->alpha = sc->gamma / delta; sc->beta = 0.0; }
+    } else {
+      sc->iterations = iter + 1;   // x now holds iteration i's update
+      sc->xinit = 1;
+      sc->pending = 0;
+      sc->rnorm2 = rn;
+      if (MODE == CG_ITER) {
+        if (gamma <= 0.0) {
+          sc->stop = 1;              // rz_new <= 0 (solver.py:101-103)
+        } else {
+          const double b = gamma / sc->gamma;
+          const double pap = delta - b * gamma / sc->alpha;
+          sc->delta = pap;
+          if (!(pap > 0.0) || !isfinite(pap)) {
+            sc->stop = 1;            // the next iteration's pAp <= 0 (solver.py:95-96)
+          } else {
+            sc->beta = b;
+            sc->alpha_prev = sc->alpha;
+            sc->alpha = gamma / pap;
+            sc->gamma_prev = sc->gamma;
+            sc->gamma = gamma;
+          }
+        }
+      }
+    }
     *ticket = 0u;
   }
 }
@@ -1334,6 +1539,49 @@ void launch_pcg_apply(const Launch& L, const Frame& f, const Coef<float>& c, con
                       const float* pprev, float* pnew, float* q, double* part, unsigned* ticket, Scalars* sc,
                       int iter, const PcgMaps* maps, float* x) {
   LS_DISPATCH_NT(f.NT, (launch_pcg_apply_nt<NT_>(L, f, c, X, z, pprev, pnew, q, part, ticket, sc, iter, maps, x)));
+}
+
+template <int NT>
+static size_t cg_smem() { return sizeof(float) * cg_stage(NT); }
+
+template <int NT>
+static void launch_cg_nt(const Launch& L, int mode, const Frame& f, const Coef<float>& c, const float* X,
+                         const float* dinv, float* u_out, float* m_out, float* t_out, float* p, float* xv,
+                         double* part, unsigned* ticket, Scalars* sc, int iter, const CgMaps& maps) {
+  const size_t sm = cg_smem<NT>();
+  switch (mode) {
+    case CG_INIT:
+      cudaFuncSetAttribute(k_cg_iter<NT, CG_INIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_cg_iter<NT, CG_INIT><<<L.grid, kThreads, sm, L.stream>>>(f, c, X, dinv, u_out, m_out, t_out, p, xv, part,
+                                                                 ticket, sc, iter, L.ntiles, maps);
+      break;
+    case CG_ITER:
+      cudaFuncSetAttribute(k_cg_iter<NT, CG_ITER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_cg_iter<NT, CG_ITER><<<L.grid, kThreads, sm, L.stream>>>(f, c, X, dinv, u_out, m_out, t_out, p, xv, part,
+                                                                 ticket, sc, iter, L.ntiles, maps);
+      break;
+    default:
+      cudaFuncSetAttribute(k_cg_iter<NT, CG_LAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_cg_iter<NT, CG_LAST><<<L.grid, kThreads, sm, L.stream>>>(f, c, X, dinv, u_out, m_out, t_out, p, xv, part,
+                                                                 ticket, sc, iter, L.ntiles, maps);
+      break;
+  }
+}
+
+void launch_cg(const Launch& L, int mode, const Frame& f, const Coef<float>& c, const float* X, const float* dinv,
+               float* u_out, float* m_out, float* t_out, float* p, float* xv, double* part, unsigned* ticket,
+               Scalars* sc, int iter, const CgMaps& maps) {
+  LS_DISPATCH_NT(f.NT, (launch_cg_nt<NT_>(L, mode, f, c, X, dinv, u_out, m_out, t_out, p, xv, part, ticket, sc, iter,
+                                          maps)));
+}
+
+int cg_grid_limit(int NT) {
+  int nb = 0;
+  LS_DISPATCH_NT(NT, (cudaFuncSetAttribute(k_cg_iter<NT_, CG_ITER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)cg_smem<NT_>()),
+                      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg_iter<NT_, CG_ITER>, kThreads,
+                                                                    cg_smem<NT_>())));
+  return nb;
 }
 
 // the last deferred x-update after the PCG loop: x += alpha_j p_j for the
