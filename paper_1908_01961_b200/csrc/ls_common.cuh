@@ -120,6 +120,16 @@ struct StepRecord {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may be scheduled before its
+// predecessor finishes; pdl_wait() blocks until the predecessor grid has
+// completed and its writes are visible (a no-op without the attribute), and
+// pdl_trigger() lets this grid's successor be scheduled onto SMs as this
+// grid's CTAs retire -- hiding the launch latency and the tail of every
+// kernel boundary of the solver's graph.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 template <typename R>
 __device__ __forceinline__ R irls1(R mag, R eps, R inv_eps) {
   // energy.py:102-112 with p = 1: 1/|m| above the floor eps, else 1/eps

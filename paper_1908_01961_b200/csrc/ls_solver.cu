@@ -26,6 +26,10 @@
 // from sX (cheaper than storing 2K+3 weight planes).  Per-pixel arithmetic is
 // fp32 (the data residual exactly rounded via fp64 FMA); reductions are fp64,
 // fixed order, finished by the last block (no float atomics).
+#include <cstdlib>
+#include <string>
+#include <utility>
+
 #include "ls_common.cuh"
 #include "ls_kernels.h"
 
@@ -38,6 +42,31 @@
 #endif
 
 namespace ls {
+
+// LS_PDL=1: launches of the solver's kernel sequence carry the programmatic-
+// serialization attribute (PDL, see pdl_wait in ls_common.cuh).  Off by
+// default: measured in the captured frame graph at 1080p K=8, 52.0 vs 54.6
+// frames/s with it -- the kernels' own times are
+// unchanged, the graph's kernel boundaries got slower.
+static bool pdl_on() {
+  static const bool on = std::getenv("LS_PDL") != nullptr && std::string(std::getenv("LS_PDL")) == "1";
+  return on;
+}
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 enum { MODE_EG = 0, MODE_TRIAL = 1 };
 
@@ -533,6 +562,8 @@ __global__ void __launch_bounds__(kThreads, kStencilMinBlocks) k_energy(Frame f,
                                                      const __grid_constant__ EnergyMaps maps) {
   constexpr int U = NT + 3;
   constexpr bool TRIAL = MODE == MODE_TRIAL;
+  pdl_wait();
+  pdl_trigger();
   // device-resident flip-flop: skip finished frames / decided line searches
   if (ctl && ctl->done) {
     if (!TRIAL && blockIdx.x == 0 && threadIdx.x == 0) sc->stop = 1;
@@ -919,6 +950,8 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
   constexpr int U = NT + 3;
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bars[2];
+  pdl_wait();
+  pdl_trigger();
   if (sc->stop) return;
   const int W = f.W, H = f.H, N = f.N;
   const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
@@ -1284,6 +1317,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
                                                          double* part, unsigned* ticket, Scalars* sc, int iter,
                                                          BandSpan band, double* bsum, const float* __restrict__ p,
                                                          float* __restrict__ xv) {
+  pdl_wait();
+  pdl_trigger();
   if (sc->stop) return;
   const float a = (float)sc->alpha;
   const bool xread = LAST && sc->xinit;
@@ -1403,9 +1438,9 @@ static void launch_energy_mt(const Launch& L, const Frame& f, const Coef<float>&
                              float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc,
                              const EnergyMaps* maps, const FrameCtl* ctl, int dev_ls, int last_trial) {
   if (maps)
-    k_energy<NT, MODE, true><<<L.grid, kThreads, energy_smem<NT>(MODE, true), L.stream>>>(
-        f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, ctl, dev_ls,
-        last_trial, *maps);
+    launch_pdl(k_energy<NT, MODE, true>, L.grid, kThreads, energy_smem<NT>(MODE, true), L.stream,
+               f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, ctl,
+               dev_ls, last_trial, *maps);
   else
     k_energy<NT, MODE, false><<<L.grid, kThreads, energy_smem<NT>(MODE, false), L.stream>>>(
         f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, ctl, dev_ls,
@@ -1448,6 +1483,8 @@ void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<float>&
 // device-resident flip-flop bookkeeping (solver.py:311-338, refine = False)
 // ---------------------------------------------------------------------------
 __global__ void k_frame_init(FrameCtl* ctl) {
+  pdl_wait();
+  pdl_trigger();
   ctl->done = ctl->converged = ctl->stalled = ctl->has_hist = ctl->e_prev_valid = 0;
   ctl->n_exec = 0;
   ctl->cur = 0;
@@ -1459,6 +1496,8 @@ __global__ void k_frame_init(FrameCtl* ctl) {
 // rejected step, solver.py:169-178 leaves it unchanged); record + bookkeeping
 __global__ void k_step_end(FrameCtl* ctl, const Scalars* sc, const float* __restrict__ Xin, float* __restrict__ Xout,
                            int64_t M, int out_id, StepRecord* recs) {
+  pdl_wait();
+  pdl_trigger();
   if (ctl->done) return;
   const bool fault = sc->fault;
   const bool acc = sc->accepted && !fault;
@@ -1497,6 +1536,8 @@ __global__ void k_step_end(FrameCtl* ctl, const Scalars* sc, const float* __rest
 
 // end of one outer iteration: relative-decrease convergence (solver.py:328-336)
 __global__ void k_outer_end(FrameCtl* ctl, double tol_rel) {
+  pdl_wait();
+  pdl_trigger();
   if (ctl->done || !ctl->has_hist) return;
   const double e_now = ctl->e_last;
   if (ctl->e_prev_valid && ctl->e_prev > 0.0) {
@@ -1511,12 +1552,12 @@ __global__ void k_outer_end(FrameCtl* ctl, double tol_rel) {
   ctl->e_prev_valid = 1;
 }
 
-void launch_frame_init(cudaStream_t s, FrameCtl* ctl) { k_frame_init<<<1, 1, 0, s>>>(ctl); }
+void launch_frame_init(cudaStream_t s, FrameCtl* ctl) { launch_pdl(k_frame_init, 1, 1, 0, s, ctl); }
 void launch_step_end(cudaStream_t s, int grid, FrameCtl* ctl, const Scalars* sc, const float* Xin, float* Xout,
                      int64_t M, int out_id, StepRecord* recs) {
-  k_step_end<<<grid, kThreads, 0, s>>>(ctl, sc, Xin, Xout, M, out_id, recs);
+  launch_pdl(k_step_end, grid, kThreads, 0, s, ctl, sc, Xin, Xout, M, out_id, recs);
 }
-void launch_outer_end(cudaStream_t s, FrameCtl* ctl, double tol_rel) { k_outer_end<<<1, 1, 0, s>>>(ctl, tol_rel); }
+void launch_outer_end(cudaStream_t s, FrameCtl* ctl, double tol_rel) { launch_pdl(k_outer_end, 1, 1, 0, s, ctl, tol_rel); }
 
 void launch_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* u,
                   float* w, double* part, unsigned* ticket, Scalars* sc, int iter, const TileMaps* maps) {
@@ -1528,8 +1569,8 @@ static void launch_pcg_apply_nt(const Launch& L, const Frame& f, const Coef<floa
                                 const float* pprev, float* pnew, float* q, double* part, unsigned* ticket,
                                 Scalars* sc, int iter, const PcgMaps* maps, float* x) {
   if (maps)
-    k_pcg_apply<NT, true><<<L.grid, kThreads, pcg_smem<NT>(true), L.stream>>>(f, c, X, z, pprev, pnew, q, part, ticket,
-                                                                         sc, iter, L.ntiles, *maps, x);
+    launch_pdl(k_pcg_apply<NT, true>, L.grid, kThreads, pcg_smem<NT>(true), L.stream, f, c, X, z, pprev, pnew, q,
+               part, ticket, sc, iter, L.ntiles, *maps, x);
   else
     k_pcg_apply<NT, false><<<L.grid, kThreads, pcg_smem<NT>(false), L.stream>>>(f, c, X, z, pprev, pnew, q, part, ticket,
                                                                           sc, iter, L.ntiles, PcgMaps{}, x);
@@ -1590,6 +1631,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_xfinal(int64_t M, float* __res
                                                          const float* __restrict__ p0,
                                                          const float* __restrict__ p1, Scalars* sc,
                                                          unsigned* ticket, BandSpan band) {
+  pdl_wait();
+  pdl_trigger();
   if (!sc->pending) return;
   const float a = (float)sc->alpha;
   const float* __restrict__ p = ((sc->iterations - 1) & 1) ? p1 : p0;
@@ -1627,7 +1670,7 @@ static BandSpan band_span(const Frame* band) {
 
 void launch_pcg_xfinal(const Launch& L, int64_t M, float* xv, const float* p0, const float* p1, Scalars* sc,
                        unsigned* ticket, const Frame* band) {
-  k_pcg_xfinal<<<L.grid, kThreads, 0, L.stream>>>(M, xv, p0, p1, sc, ticket, band_span(band));
+  launch_pdl(k_pcg_xfinal, L.grid, kThreads, 0, L.stream, M, xv, p0, p1, sc, ticket, band_span(band));
 }
 
 void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
@@ -1636,10 +1679,11 @@ void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, con
   const BandSpan bs = band_span(band);
   double* bsum = band ? band->bsum : nullptr;
   if (last && !band)
-    k_pcg_update<true><<<L.grid, kThreads, 0, L.stream>>>(M, r, q, dinv, z, part, ticket, sc, iter, bs, bsum, p, xv);
+    launch_pdl(k_pcg_update<true>, L.grid, kThreads, 0, L.stream, M, r, q, dinv, z, part, ticket, sc, iter, bs, bsum,
+               p, xv);
   else
-    k_pcg_update<false><<<L.grid, kThreads, 0, L.stream>>>(M, r, q, dinv, z, part, ticket, sc, iter, bs, bsum, p,
-                                                           xv);
+    launch_pdl(k_pcg_update<false>, L.grid, kThreads, 0, L.stream, M, r, q, dinv, z, part, ticket, sc, iter, bs, bsum,
+               p, xv);
 }
 
 // band-ordered sum of the gathered partials [nbands][nv], then the same
