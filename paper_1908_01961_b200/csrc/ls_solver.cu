@@ -40,6 +40,9 @@
 #ifndef LS_XEARLY
 #define LS_XEARLY 0
 #endif
+#ifndef LS_XDEFER
+#define LS_XDEFER 0
+#endif
 
 namespace ls {
 
@@ -551,7 +554,10 @@ __device__ void fin_pcg_update(double rz, double rn, Scalars* sc, int iter) {
 }
 
 template <int NT, int MODE, bool TMA>
-__global__ void __launch_bounds__(kThreads, kStencilMinBlocks) k_energy(Frame f, Coef<float> c, const float* __restrict__ X,
+#ifndef LS_EG_MINB
+#define LS_EG_MINB kStencilMinBlocks
+#endif
+__global__ void __launch_bounds__(kThreads, LS_EG_MINB) k_energy(Frame f, Coef<float> c, const float* __restrict__ X,
                                                      const float* __restrict__ dx, float alpha,
                                                      const float* __restrict__ Yext, float* __restrict__ Xout,
                                                      float* __restrict__ r_out, float* __restrict__ d_out,
@@ -985,6 +991,13 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
   uint32_t phase = 0;
   float acc = 0.f;
   double accd = 0.0;
+#if LS_XDEFER
+  // the previous tile's x-update: loads issued after the TMA issue, the
+  // fma + stores after the next tile's operand wait (latency hidden by it)
+  float xo_d[U], pold_d[U];
+  bool pend = false;
+  size_t pend_i = 0;
+#endif
   for (int j = 0;; ++j) {
     const int tile = blockIdx.x + j * gridDim.x;
     if (tile >= ntiles) break;
@@ -993,6 +1006,13 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
     const bool own = x < W && y < f.y_hi;
     const PixPre pre = pix_prefetch(f, x, y, own);
     if (TMA) mbar_wait(&bars[0], phase);   // operand windows
+#if LS_XDEFER
+    if (pend) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[(size_t)u * N + pend_i] = fmaf(ax, pold_d[u], xo_d[u]);
+      pend = false;
+    }
+#endif
     else {
       __syncthreads();
       load_halo1<U>(sX, X, N, W, H, tx0, ty0);
@@ -1070,6 +1090,15 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
     }
     if (xupd && own) {   // x += alpha_{i-1} p_{i-1}, overlapping the next tile's loads
       const size_t i = (size_t)y * W + x;
+#if LS_XDEFER
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        xo_d[u] = xread ? xv[(size_t)u * N + i] : 0.f;
+        pold_d[u] = pold[u];
+      }
+      pend = true;
+      pend_i = i;
+#else
 #if !LS_XEARLY
       float xo[U];
 #pragma unroll
@@ -1077,10 +1106,17 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
 #endif
 #pragma unroll
       for (int u = 0; u < U; ++u) xv[(size_t)u * N + i] = fmaf(ax, pold[u], xo[u]);
+#endif
     }
     accd += (double)acc;
     acc = 0.f;
   }
+#if LS_XDEFER
+  if (pend) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[(size_t)u * N + pend_i] = fmaf(ax, pold_d[u], xo_d[u]);
+  }
+#endif
   double accv[1] = {accd};
   block_reduce_store<1>(accv, part);
   if (!last_block(ticket)) return;

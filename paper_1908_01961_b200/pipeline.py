@@ -107,7 +107,12 @@ class StreamingDecomposer:
             self.regions = tracked
         aux = build_aux(frame, cmap, seed=self.seed + self.index, prev_chroma=self.prev_chroma,
                         prev_r=self.prev_layers.r)
-        layers = initialize(frame, cmap, self.palette, previous=self.prev_layers)
+        # warm start (solver.py:295-300): the reference deep-copies the previous
+        # layers; the streaming flip-flop never writes its input state (the
+        # graph copies it into its own ring and returns a new tensor), so the
+        # previous frame's planes are passed as they are -- one 100 MB copy
+        # per 1080p frame less
+        layers = LayerStack(planes=self.prev_layers.X)
         state = SolverState(frame=frame, palette=self.palette, layers=layers, aux=aux,
                             weights=self.weights, config=self.stream_cfg)
         flip_flop(state)

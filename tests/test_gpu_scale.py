@@ -309,3 +309,30 @@ def test_streaming_fault_raises_with_dump(graph):
         assert ok.records and all(np.isfinite(r["energy_after"]) for r in ok.records)
     finally:
         os.environ.pop("LS_NO_GRAPH", None)
+
+
+@pytest.mark.parametrize("no_graph", ["", "1"])
+def test_streaming_step_leaves_previous_frame_untouched(no_graph):
+    """StreamingDecomposer.step warm-starts from the previous frame's planes
+    without a copy: the previous frame's layers must come out unchanged and
+    the new frame must own a new tensor (graph and eager flip-flops)."""
+    from paper_1908_01961_b200.energy import EnergyWeights
+    from paper_1908_01961_b200.palette import BaseColorPalette
+    from paper_1908_01961_b200.pipeline import StreamingDecomposer
+    from paper_1908_01961_b200.solver import SolveConfig
+    clip = _clip(64, 96, 3, n=3, seed=19)
+    os.environ["LS_NO_GRAPH"] = no_graph
+    try:
+        dec = StreamingDecomposer(BaseColorPalette(colors=clip.colors), EnergyWeights(),
+                                  SolveConfig(tol_rel=0.0, outer_iterations=2))
+        s0 = dec.first(clip.frames[0].cuda())
+        X0 = s0.layers.X.clone()
+        s1 = dec.step(clip.frames[1].cuda())
+        X1 = s1.layers.X.clone()
+        s2 = dec.step(clip.frames[2].cuda())
+        torch.cuda.synchronize()
+        assert torch.equal(s0.layers.X, X0) and torch.equal(s1.layers.X, X1)
+        assert s1.layers.X.data_ptr() != s0.layers.X.data_ptr()
+        assert s2.layers.X.data_ptr() != s1.layers.X.data_ptr()
+    finally:
+        os.environ.pop("LS_NO_GRAPH", None)

@@ -35,6 +35,10 @@ if __name__ == "__main__":
                 extra = ["-DLS_PCG_PAD=30000"]
             elif n == 202:      # x-update loads issued before the stage barrier
                 extra = ["-DLS_XEARLY=1"]
+            elif n == 204:      # x-update fma/stores deferred past the next tile's operand wait
+                extra = ["-DLS_XDEFER=1"]
+            elif n == 205:      # energy kernel at 2 CTAs/SM (more registers, no rematerialisation)
+                extra = ["-DLS_EG_MINB=2"]
             build_variant(n, extra)
     else:
         for n in [0] + variants:
