@@ -353,9 +353,12 @@ def run_ours(args):
     N = H * W // nb_total
     U = K + 4
     ent_per_px = prof["adjacency_entries"] / N
-    # k_pcg_apply: reads X, z, p_prev, x (4U), edge, row_ptr, entries; writes p, q, x (3U)
-    # (the x-update of the previous iteration is folded in; 15 of 16 launches)
-    bytes_apply = N * (4 * (7 * U + 2) + 2 * ent_per_px)
+    # k_pcg_apply: reads X, z, p_prev (3U), edge, row_ptr, entries; writes p, q (2U).
+    # (With LS_X_DEFERRED=1 -- round 1's layout -- it also reads and writes x for
+    # the deferred x-update: 7U.  By default every search direction is kept and
+    # x = sum alpha_i p_i is formed once after the loop, k_pcg_combine.)
+    x_deferred = os.environ.get("LS_X_DEFERRED") == "1"
+    bytes_apply = N * (4 * ((7 if x_deferred else 5) * U + 2) + 2 * ent_per_px)
     # k_pcg_update: reads r, q, dinv (3U); writes r, z (2U)
     bytes_update = N * 4 * 5 * U
     kern = {
@@ -381,6 +384,9 @@ def run_ours(args):
                 "frac": achieved / peak, "traffic": traffic_from_profiles(kname[dom]),
                 "kernel": kname[dom], "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bpl, "avg_launch_us": avg_ms * 1e3,
+                "pcg_x_update": ("deferred into the operator (7U per launch)" if x_deferred else
+                                 "directions stored, x = sum alpha_i p_i in one pass after the loop "
+                                 "(operator 5U per launch)"),
                 "per_kernel": per_kernel,
                 "timing": f"per-kernel CUDA events over a second timed pass of {steps} frames "
                           f"({prof_t_ms / steps:.2f} ms/frame with the events)",

@@ -164,7 +164,10 @@ __global__ void k_edge(const double* __restrict__ ch, int H, int W, float* __res
 // stream by one word: positions already known are in S.z; a new one is
 // reported through S.new_zero and the pass is repeated on the device
 // (k_sample_fix / redo) -- no host round trip.
-constexpr int kSamplePix = 8;
+#ifndef LS_SAMPLE_PIX
+#define LS_SAMPLE_PIX 8
+#endif
+constexpr int kSamplePix = LS_SAMPLE_PIX;
 
 __global__ void k_sample(const __grid_constant__ SampleParams P, const SampleState* __restrict__ Sg, const double* __restrict__ ch,
                          const double* __restrict__ pch, int H, int W, int16_t* __restrict__ codes,

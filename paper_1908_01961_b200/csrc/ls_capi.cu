@@ -123,6 +123,11 @@ struct ls_ctx {
   double* pal_chroma = nullptr;
   // PCG workspace
   float *r = nullptr, *d = nullptr, *u = nullptr, *wv = nullptr, *p = nullptr, *s = nullptr, *x = nullptr;
+  // stored search directions p_0 .. p_{n-1} of the whole-frame PCG (x is
+  // combined from them once after the loop); LS_X_DEFERRED=1 keeps round 1's
+  // per-iteration deferred x-update instead
+  std::vector<float*> pdirs;
+  bool x_deferred = false;
   // single-reduction PCG (LS_PCG=cg1 at context creation): two more vectors
   bool pcg_cg1 = false;
   int grid_cg = 0;
@@ -305,6 +310,7 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   c->y_hi = H;
   set_geometry(c);
   c->use_tma = (W % 4 == 0) && tma_encode_fn() != nullptr && std::getenv("LS_NO_TMA") == nullptr;
+  c->x_deferred = std::getenv("LS_X_DEFERRED") != nullptr && std::string(std::getenv("LS_X_DEFERRED")) == "1";
   {   // opt-in single-reduction PCG (whole frames with TMA only)
     const char* pv = std::getenv("LS_PCG");
     c->pcg_cg1 = pv && std::string(pv) == "cg1" && c->use_tma;
@@ -1030,9 +1036,75 @@ static int run_pcg_cg1(ls_ctx* c, const double* colors, const float* X, int iter
 
 // fused energy/gradient + textbook PCG loop (solver.py:79-107); x receives the step.
 // Buffers: r, d = 1/diag, u = z = r/diag, wv = q = A p, p / s = ping-pong p.
+// the stored-direction buffers for a loop of `iters` iterations (outside captures)
+static int ensure_pdirs(ls_ctx* c, int iters) {
+  if (c->x_deferred || c->band_partial || c->pcg_cg1 || iters < 1 || iters > kMaxStoredDirs) return LS_OK;
+  const size_t M = (size_t)c->U * c->N;
+  while ((int)c->pdirs.size() < iters) {
+    float* b = nullptr;
+    LS_CK(dalloc(c, &b, M));
+    c->pdirs.push_back(b);
+  }
+  return LS_OK;
+}
+
+// the textbook loop with every search direction kept (p_i in its own
+// buffer, 1.6 GB at 1080p K=8 for 16 iterations -- HBM is 180 GB): the
+// operator kernel no longer carries the deferred x-update (the x read and
+// write of every iteration and their exposed load latency), the last
+// update computes only |r|, and one streaming pass k_pcg_combine forms
+// x = sum alpha_i p_i in iteration order (the same fmaf chain, the same bits)
+static int run_pcg_stored(ls_ctx* c, const double* colors, const float* X, int iters, float* x,
+                          const FrameCtl* ctl) {
+  const Frame f = frame_of(c);
+  const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
+  const int64_t M = (int64_t)c->U * c->N;
+  if ((int)c->pdirs.size() < iters) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    LS_CK(cudaStreamIsCapturing(c->stream, &cs));
+    LS_ARG(cs == cudaStreamCaptureStatusNone, "PCG direction buffers must exist before a graph capture");
+    while ((int)c->pdirs.size() < iters) {
+      float* b = nullptr;
+      LS_CK(dalloc(c, &b, (size_t)M));
+      c->pdirs.push_back(b);
+    }
+  }
+  size_t pi = prof_begin(c);
+  EnergyMaps em;
+  const bool etma = energy_maps(c, X, nullptr, &em);
+  launch_energy(0, L_energy(c), f, cd, X, nullptr, 0.f, nullptr, nullptr, c->r, c->d, c->u, nullptr, nullptr,
+                c->part, c->tickets + 0, c->sc, etma ? &em : nullptr, ctl);
+  prof_end(c, PC_EG, pi);
+  const Launch La{c->grid_pcg, c->ntiles, c->stream};
+  DirList dl;
+  std::memset(&dl, 0, sizeof(dl));
+  dl.n = iters;
+  for (int it = 0; it < iters; ++it) {
+    float* pprev = c->pdirs[it > 0 ? it - 1 : 0];
+    float* pnew = c->pdirs[it];
+    dl.p[it] = pnew;
+    PcgMaps maps;
+    const bool tma = pcg_maps(c, X, pprev, &maps);
+    pi = prof_begin(c);
+    launch_pcg_apply(La, f, cd, X, c->u, pprev, pnew, c->wv, c->part, c->tickets + 1, c->sc, it,
+                     tma ? &maps : nullptr, nullptr);
+    prof_end(c, PC_APPLY, pi);
+    pi = prof_begin(c);
+    launch_pcg_update(L_update(c), M, c->r, c->wv, c->d, c->u, pnew, nullptr, c->part, c->tickets + 2, c->sc, it,
+                      nullptr, it == iters - 1 ? 2 : 0);
+    prof_end(c, PC_UPDATE, pi);
+  }
+  launch_pcg_combine(L_update(c), M, dl, x, c->sc);
+  c->launches += 2 + 2LL * iters;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
 static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, float* x,
                    const FrameCtl* ctl = nullptr) {
   if (c->pcg_cg1 && !c->band_partial) return run_pcg_cg1(c, colors, X, iters, x, ctl);
+  if (!c->x_deferred && !c->band_partial && iters >= 1 && iters <= kMaxStoredDirs)
+    return run_pcg_stored(c, colors, X, iters, x, ctl);
   const Frame f = frame_of(c);
   const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
   size_t pi = prof_begin(c);
@@ -1053,7 +1125,7 @@ static int run_pcg(ls_ctx* c, const double* colors, const float* X, int iters, f
     prof_end(c, PC_APPLY, pi);
     pi = prof_begin(c);
     launch_pcg_update(L_update(c), M, c->r, c->wv, c->d, c->u, pbuf[it & 1], x, c->part, c->tickets + 2, c->sc, it,
-                      nullptr, it == iters - 1);
+                      nullptr, it == iters - 1 ? 1 : 0);
     prof_end(c, PC_UPDATE, pi);
   }
   // the last x += alpha p when the loop broke early (the applies fold in the
@@ -1271,6 +1343,8 @@ extern "C" int ls_flip_flop_graph(ls_ctx* c, const double* colors, const float* 
   const size_t bytes = sizeof(float) * (size_t)c->U * c->N;
   if (!c->ring[0])
     for (float*& r : c->ring) LS_CK(dalloc(c, &r, (size_t)c->U * c->N));
+  rc = ensure_pdirs(c, c->cfg.pcg_iterations);
+  if (rc) return rc;
   GraphKey key;
   std::memset(&key, 0, sizeof(key));
   for (int i = 0; i < 3 * c->K; ++i) key.colors[i] = colors[i];

@@ -96,7 +96,9 @@ struct Scalars {
   int fault;                  // non-finite energy at the linearisation point
   double alpha_ls;            // accepted step length
   double e0, e1;              // Python-sum order of terms0 / terms1 (solver.py:139-140)
+  double alpha_hist[64];      // alpha_i of every iteration (x = sum alpha_i p_i, k_pcg_combine)
 };
+constexpr int kMaxStoredDirs = 64;
 
 // device-resident flip-flop of a streaming frame (solver.py:311-338 with
 // refine = False): convergence test and step bookkeeping on the GPU

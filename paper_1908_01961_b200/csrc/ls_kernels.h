@@ -56,11 +56,19 @@ int tile_box_rw();
 void launch_pcg_apply(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* z,
                       const float* pprev, float* pnew, float* q, double* part, unsigned* ticket, Scalars* sc,
                       int iter, const PcgMaps* maps, float* x);
-// last = true (whole frames only): the final iteration also folds in the
-// last deferred x += alpha p (p = this iteration's direction) and skips z
+// last (whole frames only): 1 = the final iteration also folds in the last
+// deferred x += alpha p (p = this iteration's direction) and skips z;
+// 2 = the final iteration computes only |r| (the stored directions are
+// combined into x by launch_pcg_combine)
 void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
                        const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter,
-                       const Frame* band = nullptr, bool last = false);
+                       const Frame* band = nullptr, int last = 0);
+// the stored search directions p_0 .. p_{n-1} of one PCG loop
+struct DirList {
+  const float* p[kMaxStoredDirs];
+  int n;
+};
+void launch_pcg_combine(const Launch& L, int64_t M, const DirList& dl, float* xv, Scalars* sc);
 void launch_pcg_xfinal(const Launch& L, int64_t M, float* xv, const float* p0, const float* p1, Scalars* sc,
                        unsigned* ticket, const Frame* band = nullptr);
 // single-reduction PCG: mode 0 init (w_0 = A u_0), 1 iteration, 2 last iteration

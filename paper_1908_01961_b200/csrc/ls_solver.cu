@@ -529,7 +529,7 @@ __device__ void fin_energy_trial(const double* tot, Scalars* sc, float alpha, in
   }
 }
 
-__device__ void fin_pcg_apply(double pap, Scalars* sc) {
+__device__ void fin_pcg_apply(double pap, Scalars* sc, int iter) {
   if (sc->pending) {      // this apply folded alpha_{i-1} p_{i-1} into x
     sc->pending = 0;
     sc->xinit = 1;
@@ -540,6 +540,7 @@ __device__ void fin_pcg_apply(double pap, Scalars* sc) {
   } else {
     sc->alpha_prev = sc->alpha;
     sc->alpha = sc->gamma / pap;
+    if (iter >= 0 && iter < kMaxStoredDirs) sc->alpha_hist[iter] = sc->alpha;
   }
 }
 
@@ -968,7 +969,7 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
   // deferred PCG x-update (solver.py:98): x += alpha_{i-1} p_{i-1} for the own
   // pixels, p_{i-1} taken from the staged window -- k_pcg_update then streams
   // only r, q, dinv -> r, z
-  const bool xupd = with_p && sc->pending;
+  const bool xupd = with_p && sc->pending && xv != nullptr;
   const bool xread = sc->xinit;
   const float ax = (float)sc->alpha;
   float* sX = smem;
@@ -1123,7 +1124,7 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
   const double pap = sum_partials<1>(part, gridDim.x, 0);
   if (threadIdx.x == 0) {
     if (f.bsum) f.bsum[0] = pap;
-    else fin_pcg_apply(pap, sc);
+    else fin_pcg_apply(pap, sc, iter);
     *ticket = 0u;
   }
 }
@@ -1347,7 +1348,9 @@ __device__ __forceinline__ int64_t span_index(const BandSpan& b, int64_t j) {
 // the reported |r| (solver.py:106) and z / beta not at all, so the kernel
 // reads r, q and -- instead of dinv -- p and x, folds the last deferred
 // x-update x += alpha p in (what k_pcg_xfinal would do) and writes only x.
-template <bool LAST>
+// LAST_NORM (the last iteration when the directions are stored and combined
+// by k_pcg_combine): only |r|^2 is needed -- reads r and q, writes nothing.
+template <bool LAST, bool NORM = false>
 __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __restrict__ r, const float* __restrict__ q,
                                                          const float* __restrict__ dinv, float* __restrict__ z,
                                                          double* part, unsigned* ticket, Scalars* sc, int iter,
@@ -1367,7 +1370,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
     float4 rr = reinterpret_cast<const float4*>(r)[j];
     const float4 qq = __ldg(reinterpret_cast<const float4*>(q) + j);
     rr = make_float4(fmaf(-a, qq.x, rr.x), fmaf(-a, qq.y, rr.y), fmaf(-a, qq.z, rr.z), fmaf(-a, qq.w, rr.w));
-    if (LAST) {
+    if (NORM) {
+    } else if (LAST) {
       const float4 pp = __ldg(reinterpret_cast<const float4*>(p) + j);
       float4 xx = xread ? reinterpret_cast<const float4*>(xv)[j] : make_float4(0.f, 0.f, 0.f, 0.f);
       xx = make_float4(fmaf(a, pp.x, xx.x), fmaf(a, pp.y, xx.y), fmaf(a, pp.z, xx.z), fmaf(a, pp.w, xx.w));
@@ -1383,7 +1387,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
   }
   for (int64_t j = banded ? M : (M4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride) {
     const float rr = fmaf(-a, q[j], r[j]);
-    if (LAST) {
+    if (NORM) {
+    } else if (LAST) {
       xv[j] = fmaf(a, p[j], xread ? xv[j] : 0.f);
     } else {
       const float zz = rr * dinv[j];
@@ -1401,6 +1406,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
     if (bsum) {
       bsum[0] = rz;
       bsum[1] = rn;
+    } else if (NORM) {   // the loop ends here: the count and |r| (x comes from k_pcg_combine)
+      sc->iterations = iter + 1;
+      sc->rnorm2 = rn;
     } else if (LAST) {   // the loop ends here: record the count and |r|, x is complete
       sc->iterations = iter + 1;
       sc->rnorm2 = rn;
@@ -1704,6 +1712,41 @@ static BandSpan band_span(const Frame* band) {
   return bs;
 }
 
+// x = sum_i alpha_i p_i over the stored search directions of the finished
+// loop (n = the iterations it ran), in iteration order with fmaf -- the
+// same operations as the textbook loop's x += alpha_i p_i, so the same bits.
+// Replaces the per-iteration x read / write of the deferred x-update.
+__global__ void __launch_bounds__(kThreads) k_pcg_combine(int64_t M, DirList dl, float* __restrict__ xv, Scalars* sc) {
+  const int n = min(sc->iterations, dl.n);
+  if (n <= 0) return;
+  __shared__ float a[kMaxStoredDirs];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = (float)sc->alpha_hist[i];
+  __syncthreads();
+  const int64_t M4 = M >> 2, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M4; j += stride) {
+    float4 xx = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int i = 0; i < n; ++i) {
+      const float4 pp = __ldg(reinterpret_cast<const float4*>(dl.p[i]) + j);
+      xx = make_float4(fmaf(a[i], pp.x, xx.x), fmaf(a[i], pp.y, xx.y), fmaf(a[i], pp.z, xx.z), fmaf(a[i], pp.w, xx.w));
+    }
+    reinterpret_cast<float4*>(xv)[j] = xx;
+  }
+  for (int64_t j = (M4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride) {
+    float xx = 0.f;
+    for (int i = 0; i < n; ++i) xx = fmaf(a[i], dl.p[i][j], xx);
+    xv[j] = xx;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->xinit = 1;
+    sc->pending = 0;
+  }
+}
+
+void launch_pcg_combine(const Launch& L, int64_t M, const DirList& dl, float* xv, Scalars* sc) {
+  k_pcg_combine<<<L.grid, kThreads, 0, L.stream>>>(M, dl, xv, sc);
+}
+
 void launch_pcg_xfinal(const Launch& L, int64_t M, float* xv, const float* p0, const float* p1, Scalars* sc,
                        unsigned* ticket, const Frame* band) {
   launch_pdl(k_pcg_xfinal, L.grid, kThreads, 0, L.stream, M, xv, p0, p1, sc, ticket, band_span(band));
@@ -1711,10 +1754,13 @@ void launch_pcg_xfinal(const Launch& L, int64_t M, float* xv, const float* p0, c
 
 void launch_pcg_update(const Launch& L, int64_t M, float* r, const float* q, const float* dinv, float* z,
                        const float* p, float* xv, double* part, unsigned* ticket, Scalars* sc, int iter,
-                       const Frame* band, bool last) {
+                       const Frame* band, int last) {
   const BandSpan bs = band_span(band);
   double* bsum = band ? band->bsum : nullptr;
-  if (last && !band)
+  if (last == 2 && !band)
+    launch_pdl(k_pcg_update<true, true>, L.grid, kThreads, 0, L.stream, M, r, q, dinv, z, part, ticket, sc, iter, bs,
+               bsum, p, xv);
+  else if (last && !band)
     launch_pdl(k_pcg_update<true>, L.grid, kThreads, 0, L.stream, M, r, q, dinv, z, part, ticket, sc, iter, bs, bsum,
                p, xv);
   else
@@ -1740,7 +1786,7 @@ __global__ void k_band_finalize(int phase, const double* __restrict__ g, int nba
   switch (phase) {
     case BAND_EG: fin_energy_eg(tot, sc, true); break;
     case BAND_TRIAL: fin_energy_trial(tot, sc, alpha, dev_ls, last_trial); break;
-    case BAND_APPLY: if (!sc->stop) fin_pcg_apply(tot[0], sc); break;
+    case BAND_APPLY: if (!sc->stop) fin_pcg_apply(tot[0], sc, iter); break;
     case BAND_UPDATE: if (!sc->stop) fin_pcg_update(tot[0], tot[1], sc, iter); break;
     default: break;
   }

@@ -39,6 +39,8 @@ if __name__ == "__main__":
                 extra = ["-DLS_XDEFER=1"]
             elif n == 205:      # energy kernel at 2 CTAs/SM (more registers, no rematerialisation)
                 extra = ["-DLS_EG_MINB=2"]
+            elif n == 206:      # sampler: 4 pixels per thread (twice the threads) instead of 8
+                extra = ["-DLS_SAMPLE_PIX=4"]
             build_variant(n, extra)
     else:
         for n in [0] + variants:
@@ -50,6 +52,7 @@ if __name__ == "__main__":
             try:
                 d = json.loads(r.stdout.strip().splitlines()[-1])
                 pk = d["roofline"]["per_kernel"]
-                print(n, {k: round(v["avg_us"], 1) for k, v in pk.items()}, flush=True)
+                print(n, {k: round(v["avg_us"], 1) for k, v in pk.items()},
+                      {"fps": round(d["value"], 2), "ms_per_frame": round(d["ms_per_step"], 3)}, flush=True)
             except Exception as e:
                 print(n, "failed", r.stderr[-800:], flush=True)
