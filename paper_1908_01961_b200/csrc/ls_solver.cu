@@ -43,6 +43,10 @@
 #ifndef LS_XDEFER
 #define LS_XDEFER 0
 #endif
+// LS_KEEP_R=1: round 1's PCG update (r and z stored, 5U per iteration)
+#ifndef LS_KEEP_R
+#define LS_KEEP_R 0
+#endif
 
 namespace ls {
 
@@ -372,7 +376,11 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
         const float di = rcpf(d > 0.f ? d : 1.f);   // Jacobi preconditioner 1/diag (solver.py:87), MUFU
         const float zf = bf * di;
         const size_t o = (size_t)(3 + k) * N + i;
-        if (r_out) { r_out[o] = bf; d_out[o] = di; u_out[o] = zf; }
+        if (d_out) {
+          if (LS_KEEP_R) r_out[o] = bf;   // r = b is never read again (z-only recurrence)
+          d_out[o] = di;
+          u_out[o] = zf;
+        }
         if (b_raw) { b_raw[o] = bf; diag_raw[o] = d; }
         rz = fmaf(bf, zf, rz);
         bb = fmaf(bf, bf, bb);
@@ -471,7 +479,11 @@ __device__ __forceinline__ void energy_pixel(const Frame& f, const Coef<float>& 
     const float bf = -g;
     const float di = rcpf(d > 0.f ? d : 1.f);   // Jacobi preconditioner 1/diag (solver.py:87), MUFU
     const float zf = bf * di;
-    if (r_out) { r_out[ch * N + i] = bf; d_out[ch * N + i] = di; u_out[ch * N + i] = zf; }
+    if (d_out) {
+      if (LS_KEEP_R) r_out[ch * N + i] = bf;
+      d_out[ch * N + i] = di;
+      u_out[ch * N + i] = zf;
+    }
     if (b_raw) { b_raw[ch * N + i] = bf; diag_raw[ch * N + i] = d; }
     rz = fmaf(bf, zf, rz);
     bb = fmaf(bf, bf, bb);
@@ -1365,6 +1377,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
   const bool banded = band.planes > 0;
   const int64_t M4 = banded ? (int64_t)band.planes * band.len4 : (M >> 2);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+#if LS_KEEP_R
   for (int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < M4; jj += stride) {
     const int64_t j = banded ? span_index(band, jj) : jj;
     float4 rr = reinterpret_cast<const float4*>(r)[j];
@@ -1398,6 +1411,50 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
     }
     acc[1] += (double)rr * rr;
   }
+#else
+  // the preconditioned residual alone: z_{i+1} = z_i - alpha dinv q_i
+  // (r_{i+1} = z_{i+1} / dinv is never stored; rz and |r|^2 use 1/dinv on the
+  // fly) -- 4U words per iteration instead of 5U
+  auto one = [&](float zv, float qv, float dv, float& zn, double& rz, double& rn) {
+    zn = fmaf(-a, qv * dv, zv);
+    const float rr = zn * rcpf(dv);
+    rz += (double)(rr * zn);
+    rn += (double)(rr * rr);
+  };
+  for (int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < M4; jj += stride) {
+    const int64_t j = banded ? span_index(band, jj) : jj;
+    const float4 zz = reinterpret_cast<const float4*>(z)[j];
+    const float4 qq = __ldg(reinterpret_cast<const float4*>(q) + j);
+    const float4 di = __ldg(reinterpret_cast<const float4*>(dinv) + j);
+    float4 zn;
+    double rz = 0.0, rn = 0.0;
+    one(zz.x, qq.x, di.x, zn.x, rz, rn);
+    one(zz.y, qq.y, di.y, zn.y, rz, rn);
+    one(zz.z, qq.z, di.z, zn.z, rz, rn);
+    one(zz.w, qq.w, di.w, zn.w, rz, rn);
+    if (NORM) {
+    } else if (LAST) {
+      const float4 pp = __ldg(reinterpret_cast<const float4*>(p) + j);
+      float4 xx = xread ? reinterpret_cast<const float4*>(xv)[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+      xx = make_float4(fmaf(a, pp.x, xx.x), fmaf(a, pp.y, xx.y), fmaf(a, pp.z, xx.z), fmaf(a, pp.w, xx.w));
+      reinterpret_cast<float4*>(xv)[j] = xx;
+    } else {
+      reinterpret_cast<float4*>(z)[j] = zn;
+    }
+    acc[0] += rz;
+    acc[1] += rn;
+  }
+  for (int64_t j = banded ? M : (M4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride) {
+    float zn;
+    one(z[j], q[j], dinv[j], zn, acc[0], acc[1]);
+    if (NORM) {
+    } else if (LAST) {
+      xv[j] = fmaf(a, p[j], xread ? xv[j] : 0.f);
+    } else {
+      z[j] = zn;
+    }
+  }
+#endif
   block_reduce_store<2>(acc, part);
   if (!last_block(ticket)) return;
   const double rz = sum_partials<2>(part, gridDim.x, 0);
