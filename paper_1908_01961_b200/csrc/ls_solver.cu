@@ -941,17 +941,28 @@ __device__ __forceinline__ void tma_issue_pcg(float* stage, const PcgMaps& m, ui
                                               bool with_p) {
   constexpr uint32_t xb = sizeof(float) * (NT + 3) * kSP;
   constexpr uint32_t ob = sizeof(float) * (NT * kSP + 3 * kRP);
-  mbar_expect_tx(&bar[0], (with_p ? 2 : 1) * ob);
+  const bool p_here = with_p && !LS_PEARLY;   // LS_PEARLY: the p window has its own barrier
+  mbar_expect_tx(&bar[0], (p_here ? 2 : 1) * ob);
   mbar_expect_tx(&bar[1], xb);
   float* z = stage + pad32((NT + 3) * kSP);
   float* pp = z + op_floats(NT);
   tma_load_3d(z, &m.ZT, &bar[0], tx0 - kSX, ty0 - 1, 0);
   tma_load_3d(z + pad32(NT * kSP), &m.ZR, &bar[0], tx0 - kRX, ty0 - kHalf, 0);
-  if (with_p) {
+  if (p_here) {
     tma_load_3d(pp, &m.PT, &bar[0], tx0 - kSX, ty0 - 1, 0);
     tma_load_3d(pp + pad32(NT * kSP), &m.PR, &bar[0], tx0 - kRX, ty0 - kHalf, 0);
   }
   tma_load_3d(stage, &m.X, &bar[1], tx0 - kSX, ty0 - 1, 0);
+}
+
+// the p_{i-1} window alone (LS_PEARLY), on its own barrier
+template <int NT>
+__device__ __forceinline__ void tma_issue_pprev(float* stage, const PcgMaps& m, uint64_t* bar, int tx0, int ty0) {
+  constexpr uint32_t ob = sizeof(float) * (NT * kSP + 3 * kRP);
+  mbar_expect_tx(bar, ob);
+  float* pp = stage + pad32((NT + 3) * kSP) + op_floats(NT);
+  tma_load_3d(pp, &m.PT, bar, tx0 - kSX, ty0 - 1, 0);
+  tma_load_3d(pp + pad32(NT * kSP), &m.PR, bar, tx0 - kRX, ty0 - kHalf, 0);
 }
 
 
@@ -968,7 +979,7 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
                                                            float* __restrict__ xv) {
   constexpr int U = NT + 3;
   extern __shared__ __align__(128) float smem[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[3];
   pdl_wait();
   pdl_trigger();
   if (sc->stop) return;
@@ -993,10 +1004,13 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
     if (threadIdx.x == 0) {
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
+      mbar_init(&bars[2], 1);
       fence_barrier_init();
       if ((int)blockIdx.x < ntiles) {
         const int t = blockIdx.x;
         tma_issue_pcg<NT>(smem, maps, &bars[0], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH, with_p);
+        if (LS_PEARLY && with_p)
+          tma_issue_pprev<NT>(smem, maps, &bars[2], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH);
       }
     }
     __syncthreads();
@@ -1018,7 +1032,10 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
     const int x = tx0 + lx, y = ty0 + ly;
     const bool own = x < W && y < f.y_hi;
     const PixPre pre = pix_prefetch(f, x, y, own);
-    if (TMA) mbar_wait(&bars[0], phase);   // operand windows
+    if (TMA) {
+      mbar_wait(&bars[0], phase);   // operand windows
+      if (LS_PEARLY && with_p) mbar_wait(&bars[2], phase);
+    }
 #if LS_XDEFER
     if (pend) {
 #pragma unroll
@@ -1026,7 +1043,7 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
       pend = false;
     }
 #endif
-    else {
+    if (!TMA) {
       __syncthreads();
       load_halo1<U>(sX, X, N, W, H, tx0, ty0);
       load_halo1<NT>(sZT, z + 3 * (size_t)N, N, W, H, tx0, ty0);
@@ -1054,6 +1071,13 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
       form(sZT, sPT, NT * kSP / 4);
       form(sZR, sPR, 3 * kRP / 4);
       if (!TMA) __syncthreads();
+      if (TMA && LS_PEARLY && !xupd) {   // the p region is free: the next tile's p_{i-1} now
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const int t = blockIdx.x + (j + 1) * gridDim.x;
+          if (t < ntiles) tma_issue_pprev<NT>(smem, maps, &bars[2], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH);
+        }
+      }
     }
     if (TMA) {   // state window (arrived during the formation); the wait's
       mbar_wait(&bars[1], phase);   // acquire + the barrier below order the formed operand
@@ -1098,7 +1122,11 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
       __syncthreads();
       if (threadIdx.x == 0) {
         const int t = blockIdx.x + (j + 1) * gridDim.x;
-        if (t < ntiles) tma_issue_pcg<NT>(smem, maps, &bars[0], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH, with_p);
+        if (t < ntiles) {
+          tma_issue_pcg<NT>(smem, maps, &bars[0], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH, with_p);
+          if (LS_PEARLY && with_p && xupd)   // the deferred x-update still needed p_{i-1} here
+            tma_issue_pprev<NT>(smem, maps, &bars[2], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH);
+        }
       }
     }
     if (xupd && own) {   // x += alpha_{i-1} p_{i-1}, overlapping the next tile's loads
