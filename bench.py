@@ -359,8 +359,11 @@ def run_ours(args):
     # x = sum alpha_i p_i is formed once after the loop, k_pcg_combine.)
     x_deferred = os.environ.get("LS_X_DEFERRED") == "1"
     bytes_apply = N * (4 * ((7 if x_deferred else 5) * U + 2) + 2 * ent_per_px)
-    # k_pcg_update: reads r, q, dinv (3U); writes r, z (2U)
-    bytes_update = N * 4 * 5 * U
+    # k_pcg_update: reads z, q, dinv (3U); writes z (U) -- only the preconditioned
+    # residual is carried (r = z / dinv on the fly); the last of the 16 launches
+    # writes nothing (3U): the per-launch average
+    n_it = cfg.pcg_iterations
+    bytes_update = N * 4 * U * (4 * (n_it - 1) + 3) / n_it
     kern = {
         "apply": (prof["apply"], bytes_apply),
         "update": (prof["update"], bytes_update),

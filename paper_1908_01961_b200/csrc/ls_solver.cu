@@ -43,6 +43,17 @@
 #ifndef LS_XDEFER
 #define LS_XDEFER 0
 #endif
+// LS_PEARLY=1: the operator kernel prefetches the next tile's p_{i-1} window
+// into the p region as soon as the current tile's operand is formed
+#ifndef LS_PEARLY
+#define LS_PEARLY 0
+#endif
+// LS_PFORM_GLOBAL=1: the operator forms p = z + beta p_{i-1} with p_{i-1}
+// read from global memory (L2) instead of a staged window: half the operand
+// shared memory (46 KB per CTA)
+#ifndef LS_PFORM_GLOBAL
+#define LS_PFORM_GLOBAL 0
+#endif
 // LS_KEEP_R=1: round 1's PCG update (r and z stored, 5U per iteration)
 #ifndef LS_KEEP_R
 #define LS_KEEP_R 0
@@ -932,7 +943,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_apply(Frame f, Coef<float> c, c
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int op_floats(int NT) { return pad32(NT * kSP) + pad32(3 * kRP); }
 // X, z and p_{i-1} windows (p_i = z_i + beta p_{i-1} is formed in place over z)
-__host__ __device__ constexpr int pcg_stage(int NT, bool) { return pad32((NT + 3) * kSP) + 2 * op_floats(NT); }
+__host__ __device__ constexpr int pcg_stage(int NT, bool) {
+  return pad32((NT + 3) * kSP) + (LS_PFORM_GLOBAL ? 1 : 2) * op_floats(NT);
+}
 
 template <int NT>
 // two barriers: bar[0] the operand windows (z, p_{i-1}) the formation pass
@@ -941,7 +954,7 @@ __device__ __forceinline__ void tma_issue_pcg(float* stage, const PcgMaps& m, ui
                                               bool with_p) {
   constexpr uint32_t xb = sizeof(float) * (NT + 3) * kSP;
   constexpr uint32_t ob = sizeof(float) * (NT * kSP + 3 * kRP);
-  const bool p_here = with_p && !LS_PEARLY;   // LS_PEARLY: the p window has its own barrier
+  const bool p_here = with_p && !LS_PEARLY && !LS_PFORM_GLOBAL;   // LS_PEARLY: the p window has its own barrier
   mbar_expect_tx(&bar[0], (p_here ? 2 : 1) * ob);
   mbar_expect_tx(&bar[1], xb);
   float* z = stage + pad32((NT + 3) * kSP);
@@ -1068,8 +1081,37 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
           z4[e] = a;
         }
       };
+#if LS_PFORM_GLOBAL
+      {   // p_{i-1} from global (zero outside the image, like the TMA boxes)
+        const float4* pg = reinterpret_cast<const float4*>(pprev);
+        constexpr int c4t = kSW / 4, c4r = kRW / 4;
+        for (int e = threadIdx.x; e < NT * kSH * c4t; e += kThreads) {
+          const int k = e / (kSH * c4t), rem = e - k * (kSH * c4t), rr = rem / c4t, c4 = rem - rr * c4t;
+          const int gy = ty0 - 1 + rr, gx = tx0 - kSX + 4 * c4;
+          float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (gy >= 0 && gy < H && gx >= 0 && gx < W) b = __ldg(pg + (((size_t)(3 + k) * N + (size_t)gy * W + gx) >> 2));
+          float4* zp = reinterpret_cast<float4*>(sZT + k * kSP + rr * kSW + 4 * c4);
+          float4 a = *zp;
+          a.x = fmaf(beta, b.x, a.x); a.y = fmaf(beta, b.y, a.y);
+          a.z = fmaf(beta, b.z, a.z); a.w = fmaf(beta, b.w, a.w);
+          *zp = a;
+        }
+        for (int e = threadIdx.x; e < 3 * kHaloH * c4r; e += kThreads) {
+          const int ch = e / (kHaloH * c4r), rem = e - ch * (kHaloH * c4r), rr = rem / c4r, c4 = rem - rr * c4r;
+          const int gy = ty0 - kHalf + rr, gx = tx0 - kRX + 4 * c4;
+          float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (gy >= 0 && gy < H && gx >= 0 && gx < W) b = __ldg(pg + (((size_t)ch * N + (size_t)gy * W + gx) >> 2));
+          float4* zp = reinterpret_cast<float4*>(sZR + ch * kRP + rr * kRW + 4 * c4);
+          float4 a = *zp;
+          a.x = fmaf(beta, b.x, a.x); a.y = fmaf(beta, b.y, a.y);
+          a.z = fmaf(beta, b.z, a.z); a.w = fmaf(beta, b.w, a.w);
+          *zp = a;
+        }
+      }
+#else
       form(sZT, sPT, NT * kSP / 4);
       form(sZR, sPR, 3 * kRP / 4);
+#endif
       if (!TMA) __syncthreads();
       if (TMA && LS_PEARLY && !xupd) {   // the p region is free: the next tile's p_{i-1} now
         __syncthreads();
@@ -1113,9 +1155,10 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
       }
       if (xupd) {   // p_{i-1} of the own pixel into registers before the stage is released
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) pold[ch] = sPR[ch * kRP + rc0];
+        for (int ch = 0; ch < 3; ++ch) pold[ch] = LS_PFORM_GLOBAL ? __ldg(pprev + (size_t)ch * N + i) : sPR[ch * kRP + rc0];
 #pragma unroll
-        for (int k = 0; k < NT; ++k) pold[3 + k] = sPT[k * kSP + sc0];
+        for (int k = 0; k < NT; ++k)
+          pold[3 + k] = LS_PFORM_GLOBAL ? __ldg(pprev + (size_t)(3 + k) * N + i) : sPT[k * kSP + sc0];
       }
     }
     if (TMA) {
