@@ -43,10 +43,11 @@
 #ifndef LS_XDEFER
 #define LS_XDEFER 0
 #endif
-// LS_PEARLY=1: the operator kernel prefetches the next tile's p_{i-1} window
-// into the p region as soon as the current tile's operand is formed
+// LS_PEARLY (default 1): the operator kernel prefetches the next tile's
+// p_{i-1} window into the p region as soon as the current tile's operand is
+// formed, on its own mbarrier (142.4 -> 140.7 us at 1080p K=8)
 #ifndef LS_PEARLY
-#define LS_PEARLY 0
+#define LS_PEARLY 1
 #endif
 // LS_PFORM_GLOBAL=1: the operator forms p = z + beta p_{i-1} with p_{i-1}
 // read from global memory (L2) instead of a staged window: half the operand

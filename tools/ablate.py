@@ -41,8 +41,8 @@ if __name__ == "__main__":
                 extra = ["-DLS_EG_MINB=2"]
             elif n == 206:      # sampler: 4 pixels per thread (twice the threads) instead of 8
                 extra = ["-DLS_SAMPLE_PIX=4"]
-            elif n == 207:      # operator: next tile's p window prefetched after the formation
-                extra = ["-DLS_PEARLY=1"]
+            elif n == 207:      # operator: the p window loaded with the tile's other windows (round 1)
+                extra = ["-DLS_PEARLY=0"]
             elif n == 208:      # operator: p_{i-1} read from L2 in the formation, 4 CTAs/SM (64 registers)
                 extra = ["-DLS_PFORM_GLOBAL=1", "-DLS_PCG_MINB=4"]
             elif n == 209:      # operator: p_{i-1} read from L2 in the formation, 3 CTAs/SM
