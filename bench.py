@@ -391,6 +391,15 @@ def run_ours(args):
                                  "directions stored, x = sum alpha_i p_i in one pass after the loop "
                                  "(operator 5U per launch)"),
                 "per_kernel": per_kernel,
+                # one PCG iteration as a unit (operator + update; their bytes over
+                # their summed launch times)
+                "pcg_iteration": {
+                    "bytes": bytes_apply + bytes_update,
+                    "us": 1e3 * (kern["apply"][0]["ms"] / max(kern["apply"][0]["count"], 1) +
+                                 kern["update"][0]["ms"] / max(kern["update"][0]["count"], 1)),
+                    "frac": (bytes_apply + bytes_update) /
+                            ((kern["apply"][0]["ms"] / max(kern["apply"][0]["count"], 1) +
+                              kern["update"][0]["ms"] / max(kern["update"][0]["count"], 1)) / 1e3) / 1e9 / peak},
                 "timing": f"per-kernel CUDA events over a second timed pass of {steps} frames "
                           f"({prof_t_ms / steps:.2f} ms/frame with the events)",
                 # SURVEY.md 8(d) compulsory-traffic model of a whole streaming
