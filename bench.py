@@ -383,6 +383,11 @@ def run_ours(args):
     for k in ("energy_grad", "trial"):
         per_kernel[k] = {"launches": prof[k]["count"],
                          "avg_us": 1e3 * prof[k]["ms"] / max(prof[k]["count"], 1)}
+    it_us = per_kernel["apply"]["avg_us"] + per_kernel["update"]["avg_us"]
+    it_bytes = bytes_apply + bytes_update
+    pcg_iter = {"bytes": it_bytes, "us": it_us,
+                "achieved_gbs": it_bytes / (it_us / 1e6) / 1e9 if it_us else None,
+                "frac": it_bytes / (it_us / 1e6) / 1e9 / peak if it_us else None}
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic_from_profiles(kname[dom]),
                 "kernel": kname[dom], "peak_source": peak_src,
@@ -391,15 +396,9 @@ def run_ours(args):
                                  "directions stored, x = sum alpha_i p_i in one pass after the loop "
                                  "(operator 5U per launch)"),
                 "per_kernel": per_kernel,
-                # one PCG iteration as a unit (operator + update; their bytes over
-                # their summed launch times)
-                "pcg_iteration": {
-                    "bytes": bytes_apply + bytes_update,
-                    "us": 1e3 * (kern["apply"][0]["ms"] / max(kern["apply"][0]["count"], 1) +
-                                 kern["update"][0]["ms"] / max(kern["update"][0]["count"], 1)),
-                    "frac": (bytes_apply + bytes_update) /
-                            ((kern["apply"][0]["ms"] / max(kern["apply"][0]["count"], 1) +
-                              kern["update"][0]["ms"] / max(kern["update"][0]["count"], 1)) / 1e3) / 1e9 / peak},
+                # one PCG iteration as a unit: operator + update bytes over their
+                # summed average launch times
+                "pcg_iteration": pcg_iter,
                 "timing": f"per-kernel CUDA events over a second timed pass of {steps} frames "
                           f"({prof_t_ms / steps:.2f} ms/frame with the events)",
                 # SURVEY.md 8(d) compulsory-traffic model of a whole streaming
