@@ -212,6 +212,18 @@ LS_API int ls_flip_flop_stream(ls_ctx* ctx, const double* colors_host, float* X0
 LS_API int ls_flip_flop_graph(ls_ctx* ctx, const double* colors_host, const float* X_in, float* X_out, int outer,
                               int gn_steps, double tol_rel, ls_gn_record* out, int* n_records, int* status,
                               int* fault_step);
+/* n independent flip-flops (one per context, same palette and schedule) as
+ * one launch sequence: all are enqueued, each on its context's stream, before
+ * any is waited for -- the K candidate solves of correct_reflectance
+ * (correction.py:168-201, whose thread pool this replaces).  Per context i:
+ * state buffers X0[i] (input) / X1[i] / X2[i], records at out + i*outer*gn_steps,
+ * n_records[i], status[i], final_buffer[i], fault_step[i] as
+ * ls_flip_flop_stream's, and its own return code in rcs[i].  Returns LS_OK
+ * unless the arguments are invalid. */
+LS_API int ls_flip_flop_batch(ls_ctx* const* ctxs, int n, const double* colors_host, float* const* X0,
+                              float* const* X1, float* const* X2, int outer, int gn_steps, double tol_rel,
+                              ls_gn_record* out, int* n_records, int* status, int* final_buffer,
+                              int* fault_step, int* rcs);
 /* Dense 3K x 3K refinement normal system at delta_b = 0 (energy.py:563-610);
  * uses the cluster ids set by ls_set_anchor when use_ids != 0.  Host outputs. */
 LS_API int ls_dense_normal(ls_ctx* ctx, const double* colors_host, const float* X, int use_ids,

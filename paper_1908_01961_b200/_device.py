@@ -18,12 +18,12 @@ from . import _lib as L
 
 from collections import OrderedDict
 
-# (device, H, W, K, thread) -> DeviceSolver, least recently used first; the
+# (device, H, W, K, thread, slot) -> DeviceSolver, least recently used first; the
 # streaming loop reuses one entry, varying sizes (correction bounding boxes,
 # segmentation of other frame sizes) are evicted beyond MAX_CONTEXTS
 _cache: "OrderedDict" = OrderedDict()
 _cache_lock = threading.Lock()
-MAX_CONTEXTS = 16
+MAX_CONTEXTS = 32
 
 
 def _device_of(t) -> torch.device:
@@ -392,8 +392,30 @@ def edge_from_chroma(chroma_planes: torch.Tensor) -> torch.Tensor:
     return out
 
 
+_slot = threading.local()
+
+
+class solver_slot:
+    """Context manager: inside it, get_solver hands out the contexts of slot
+    `name` (distinct from the thread's default ones), so that several solves
+    of the same size can be prepared and then run side by side, each on its
+    own context and stream (correction.correct_reflectance)."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        self.prev = getattr(_slot, "name", None)
+        _slot.name = self.name
+        return self
+
+    def __exit__(self, *exc):
+        _slot.name = self.prev
+        return False
+
+
 def get_solver(device: torch.device, H: int, W: int, K: int) -> DeviceSolver:
-    key = (device.index or 0, H, W, K, threading.get_ident())
+    key = (device.index or 0, H, W, K, threading.get_ident(), getattr(_slot, "name", None))
     with _cache_lock:
         s = _cache.get(key)
         if s is None:
@@ -404,6 +426,38 @@ def get_solver(device: torch.device, H: int, W: int, K: int) -> DeviceSolver:
         else:
             _cache.move_to_end(key)
         return s
+
+
+def flip_flop_batch(solvers, streams, colors, X0s, outer: int, gn_steps: int, tol_rel: float):
+    """ls_flip_flop_batch: the device-resident flip-flop of every solver (one
+    context each, its state X0s[i]) enqueued on streams[i] before any is
+    waited for.  Returns per solver (rc, records, status, final state, fault
+    step) as DeviceSolver.flip_flop_stream does; rc is the solver's own code."""
+    n = len(solvers)
+    if n == 0:
+        return []
+    lib = solvers[0].lib
+    a, pa = L.dbl_array(colors)
+    X1s, X2s = [], []
+    for s, st, X0 in zip(solvers, streams, X0s):
+        with torch.cuda.stream(st):
+            X1s.append(torch.empty_like(X0))
+            X2s.append(torch.empty_like(X0))
+        lib.ls_set_stream(s.ctx, C.c_void_p(st.cuda_stream))
+    per = max(1, outer * gn_steps)
+    recs = (L.GNRecord * (n * per))()
+    ptrs = lambda ts: (C.c_void_p * n)(*[t.data_ptr() for t in ts])     # noqa: E731
+    ints = lambda: (C.c_int * n)()                                      # noqa: E731
+    nrec, status, final, fault, rcs = ints(), ints(), ints(), ints(), ints()
+    ctxs = (C.c_void_p * n)(*[s.ctx.value for s in solvers])
+    solvers[0]._chk(lib.ls_flip_flop_batch(ctxs, n, pa, ptrs(X0s), ptrs(X1s), ptrs(X2s), int(outer),
+                                           int(gn_steps), float(tol_rel), recs, nrec, status, final,
+                                           fault, rcs))
+    out = []
+    for i in range(n):
+        X = (X0s[i], X1s[i], X2s[i])[final[i]]
+        out.append((rcs[i], [recs[i * per + j] for j in range(nrec[i])], status[i], X, fault[i]))
+    return out
 
 
 def utility_solver(device=None) -> DeviceSolver:

@@ -98,6 +98,9 @@ SIGNATURES = {
                             C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "ls_flip_flop_graph": [P, DBL_P, P, P, C.c_int, C.c_int, C.c_double, C.POINTER(GNRecord),
                            C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    "ls_flip_flop_batch": [C.POINTER(P), C.c_int, DBL_P, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.c_int,
+                           C.c_int, C.c_double, C.POINTER(GNRecord), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                           C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "ls_dense_normal": [P, DBL_P, P, C.c_int, DBL_P, DBL_P],
     "ls_svd_solve": [P, C.c_int, DBL_P, DBL_P, C.c_double, DBL_P],
     "ls_dense_step": [P, DBL_P, P, DBL_P, C.POINTER(DenseRecord)],

@@ -1313,6 +1313,63 @@ extern "C" int ls_flip_flop_stream(ls_ctx* c, const double* colors, float* X0, f
   return finish_flip_flop(c, out, n_records, status, final_buffer, fault_step);
 }
 
+// Independent flip-flops over n contexts as one launch sequence
+// (correction.py:168-201's K candidate solves): every context's whole
+// flip-flop is enqueued on that context's own stream before any is waited
+// for, so small solves (the candidates' bounding boxes) run side by side on
+// the GPU; then one synchronisation per context.  Per-context results as
+// ls_flip_flop_stream's, records at out + i * outer * gn_steps; rcs[i] is the
+// context's own code (a failed candidate does not stop the others).
+extern "C" int ls_flip_flop_batch(ls_ctx* const* ctxs, int n, const double* colors, float* const* X0,
+                                  float* const* X1, float* const* X2, int outer, int gn_steps, double tol_rel,
+                                  ls_gn_record* out, int* n_records, int* status, int* final_buffer,
+                                  int* fault_step, int* rcs) {
+  LS_ARG(ctxs && n >= 0 && X0 && X1 && X2 && out && n_records && status && final_buffer && fault_step && rcs,
+         "bad arguments");
+  LS_ARG(outer >= 0 && gn_steps >= 0 && (int64_t)outer * gn_steps <= kMaxStepRecords, "too many GN steps");
+  const int per = outer * gn_steps;
+  std::vector<char> live(n, 0);
+  for (int i = 0; i < n; ++i) {
+    ls_ctx* c = ctxs[i];
+    n_records[i] = 0;
+    status[i] = 0;
+    final_buffer[i] = 0;
+    fault_step[i] = -1;
+    LS_ARG(c && X0[i] && X1[i] && X2[i], "bad arguments");
+    LS_ARG(c->dev == ctxs[0]->dev, "contexts on different devices");
+    for (int j = 0; j < i; ++j) LS_ARG(ctxs[j] != c, "a context appears twice in the batch");
+  }
+  LS_CK(cudaSetDevice(ctxs[0]->dev));
+  // allocations first (cudaMalloc may synchronise the device)
+  for (int i = 0; i < n; ++i) {
+    int rc = whole_frame_only(ctxs[i]);
+    if (!rc) rc = check_ready(ctxs[i]);
+    if (!rc) rc = ensure_pdirs(ctxs[i], ctxs[i]->cfg.pcg_iterations);
+    rcs[i] = rc;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (rcs[i]) continue;
+    float* const bufs[3] = {X0[i], X1[i], X2[i]};
+    int k = 0;
+    rcs[i] = enqueue_flip_flop(ctxs[i], colors, bufs, outer, gn_steps, tol_rel, &k);
+    live[i] = rcs[i] == LS_OK;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (!live[i]) continue;
+    ls_ctx* c = ctxs[i];
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+      g_err = std::string("CUDA: ") + cudaGetErrorString(e);
+      rcs[i] = LS_ERR_CUDA;
+      continue;
+    }
+    prof_harvest(c);
+    rcs[i] = finish_flip_flop(c, out + (size_t)i * per, n_records + i, status + i, final_buffer + i,
+                              fault_step + i);
+  }
+  return LS_OK;
+}
+
 // The same flip-flop as ONE CUDA graph launch.  The graph is captured once
 // over context-owned state buffers (so every pointer it bakes in -- kernel
 // arguments and TMA descriptors -- stays valid) and replayed while the

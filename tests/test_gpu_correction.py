@@ -52,6 +52,12 @@ def test_correct_reflectance_picks_the_reference_color():
     scores = [C._candidate_sparsity(frame, cmap, pal, region, k, EnergyWeights(), cfg, 0) for k in (1, 2, 3)]
     np.testing.assert_allclose(scores, d["c_scores"], rtol=0.05)
     assert C.correct_reflectance(region, frame, cmap, pal, config=cfg, max_workers=1) == int(d["c_pick"])
+    # batched (all candidates in flight, one context + stream each): the same
+    # kernels on the same inputs, so the same scores bit for bit
+    batch = C._candidate_batch(frame, cmap, pal, region, (1, 2, 3), EnergyWeights(), cfg, 0)
+    assert [batch[k] for k in (1, 2, 3)] == scores
+    assert C.correct_reflectance(region, frame, cmap, pal, config=cfg) == int(d["c_pick"])
+    assert C.correct_reflectance(region, frame, cmap, pal, config=cfg, max_workers=2) == int(d["c_pick"])
     # the corrected map carries the pick over the region
     region.corrected_id = int(d["c_pick"])
     fixed = C.apply_region_correction(cmap, region, pal)
