@@ -10,6 +10,8 @@
 // a comparison (chroma gate, nearest-palette argmin), so the integer outputs
 // (partners, cluster ids) are bit-identical to the reference.
 #include <climits>
+#include <cstdlib>
+#include <algorithm>
 
 #include "ls_kernels.h"
 
@@ -168,6 +170,7 @@ __global__ void k_edge(const double* __restrict__ ch, int H, int W, float* __res
 #define LS_SAMPLE_PIX 8
 #endif
 constexpr int kSamplePix = LS_SAMPLE_PIX;
+constexpr double kGateSq = 0x1.47ae147ae147ap-9;   // max{s : sqrt_rn(s) < 0.05}
 
 __global__ void k_sample(const __grid_constant__ SampleParams P, const SampleState* __restrict__ Sg, const double* __restrict__ ch,
                          const double* __restrict__ pch, int H, int W, int16_t* __restrict__ codes,
@@ -233,8 +236,12 @@ __global__ void k_sample(const __grid_constant__ SampleParams P, const SampleSta
         const bool inside = py >= 0 && py < H;
         const int q = inside ? py * W + px : p;
         const double* src = tk ? pch : ch;
-        const double dist = norm2d(__dsub_rn(c0, src[q]), __dsub_rn(c1, src[N + q]));
-        const bool keep = inside && (dist < 0.05) && (tk || q != p);
+        // |c - c_q| < 0.05 (energy.py:175) without the square root: sqrt_rn is
+        // monotone, so sqrt_rn(s) < 0.05 <=> s <= kGateSq, the largest double
+        // whose correctly rounded root is below 0.05 (tests/test_gate_constant.py)
+        const double a = __dsub_rn(c0, src[q]), b = __dsub_rn(c1, src[N + q]);
+        const double s2 = __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b));
+        const bool keep = inside && (s2 <= kGateSq) && (tk || q != p);
         int16_t code = -1;
         if (keep) {
           code = (int16_t)make_ent(py - y, px - x, tk, false);
@@ -444,6 +451,80 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_rows(int N, const int32_t
   }
 }
 
+// The same sort, warp-cooperative: a warp takes 32 consecutive rows (one
+// contiguous span of the entry arrays), loads the span into shared memory
+// with coalesced accesses, each lane sorts its own row there, and the warp
+// stores the span back coalesced.  Spans longer than kWarpSpan fall back to
+// the per-lane in-place sort.  Keys are unique within a row, so the result is
+// the one k_sort_rows produces.
+constexpr int kWarpSpan = 640, kWarpSortWarps = 4;
+
+__global__ void __launch_bounds__(32 * kWarpSortWarps) k_sort_rows_warp(int N, const int32_t* __restrict__ row_ptr,
+                                                                        uint16_t* ent, uint32_t* key, float* ent_w) {
+  __shared__ uint32_t sk[kWarpSortWarps][kWarpSpan];
+  __shared__ uint16_t se[kWarpSortWarps][kWarpSpan];
+  __shared__ float sw[kWarpSortWarps][kWarpSpan];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* K = sk[wid];
+  uint16_t* E = se[wid];
+  float* Wt = sw[wid];
+  const int nwarps = gridDim.x * kWarpSortWarps;
+  for (int p0 = (blockIdx.x * kWarpSortWarps + wid) * 32; p0 < N; p0 += nwarps * 32) {
+    const int p = p0 + lane;
+    const int pend = min(p0 + 32, N);
+    const int a0 = row_ptr[p0];
+    const int span = row_ptr[pend] - a0;
+    const int ra = p < N ? row_ptr[p] : 0, n = p < N ? row_ptr[p + 1] - ra : 0;
+    if (span <= kWarpSpan) {
+      for (int j = lane; j < span; j += 32) {
+        K[j] = key[a0 + j];
+        E[j] = ent[a0 + j];
+        if (ent_w) Wt[j] = ent_w[a0 + j];
+      }
+      __syncwarp();
+      const int o = ra - a0;
+      for (int i = o + 1; i < o + n; ++i) {
+        const uint32_t k = K[i];
+        const uint16_t e = E[i];
+        const float w = ent_w ? Wt[i] : 0.f;
+        int j = i - 1;
+        while (j >= o && K[j] > k) {
+          K[j + 1] = K[j];
+          E[j + 1] = E[j];
+          if (ent_w) Wt[j + 1] = Wt[j];
+          --j;
+        }
+        K[j + 1] = k;
+        E[j + 1] = e;
+        if (ent_w) Wt[j + 1] = w;
+      }
+      __syncwarp();
+      for (int j = lane; j < span; j += 32) {
+        key[a0 + j] = K[j];
+        ent[a0 + j] = E[j];
+        if (ent_w) ent_w[a0 + j] = Wt[j];
+      }
+      __syncwarp();
+    } else {
+      for (int i = ra + 1; i < ra + n; ++i) {
+        const uint32_t k = key[i];
+        const uint16_t e = ent[i];
+        const float w = ent_w ? ent_w[i] : 0.f;
+        int j = i - 1;
+        while (j >= ra && key[j] > k) {
+          key[j + 1] = key[j];
+          ent[j + 1] = ent[j];
+          if (ent_w) ent_w[j + 1] = ent_w[j];
+          --j;
+        }
+        key[j + 1] = k;
+        ent[j + 1] = e;
+        if (ent_w) ent_w[j + 1] = w;
+      }
+    }
+  }
+}
+
 __global__ void k_pairs_from_samples(const int16_t* __restrict__ codes, int H, int W, const int32_t* __restrict__ off,
                                      int64_t* src, int64_t* dst, uint8_t* temporal) {
   const int N = H * W;
@@ -585,7 +666,8 @@ void launch_sample(cudaStream_t s, const SampleParams& P_in, SampleState* S, con
   if (known) k_sample_init_known<<<1, 1, 0, s>>>(S, known, n_known_lists);
   else k_sample_init<<<1, 1, 0, s>>>(S);
   for (int pass = 0; pass < passes; ++pass) {
-    k_sample_zero<<<grid_for(N + 1), 256, 0, s>>>(S, N + 1, out_cnt, in_cnt);
+    // grid-stride over a bounded grid: the redo passes usually exit at once
+    k_sample_zero<<<std::min(grid_for(N + 1), 1184), 256, 0, s>>>(S, N + 1, out_cnt, in_cnt);
     k_sample<<<grid_for(nthreads, 128), 128, 0, s>>>(P, S, chroma, prev_chroma, H, W, codes, out_cnt, in_cnt, S);
     k_sample_fix<<<1, 1, 0, s>>>(S, pass == passes - 1);
   }
@@ -615,7 +697,11 @@ void launch_fill_from_pairs(cudaStream_t s, int64_t n, const int64_t* src, const
   if (n > 0) k_fill_pairs<<<grid_for(n), 256, 0, s>>>(n, src, dst, temporal, weight, W, row_ptr, fill, ent, key, ent_w);
 }
 void launch_sort_rows(cudaStream_t s, int N, const int32_t* row_ptr, uint16_t* ent, uint32_t* key, float* ent_w) {
-  k_sort_rows<<<grid_for(N, kSortThreads), kSortThreads, 0, s>>>(N, row_ptr, ent, key, ent_w);
+  if (std::getenv("LS_SORT_THREAD"))      // the per-thread form (A/B)
+    k_sort_rows<<<grid_for(N, kSortThreads), kSortThreads, 0, s>>>(N, row_ptr, ent, key, ent_w);
+  else
+    k_sort_rows_warp<<<grid_for(((int64_t)N + 31) / 32, kWarpSortWarps), 32 * kWarpSortWarps, 0, s>>>(
+        N, row_ptr, ent, key, ent_w);
 }
 void launch_pairs_from_samples(cudaStream_t s, const int16_t* codes, int H, int W, const int32_t* off, int64_t* src,
                                int64_t* dst, uint8_t* temporal) {

@@ -352,8 +352,14 @@ def install(solver, frame: Frame, aux: EnergyAux):
     else:
         raise ValueError("EnergyAux needs cluster_ids or r_cluster_log")
     if aux.prev_r is not None:
-        pr = as_cuda(aux.prev_r, device=img.device)
-        solver.set_prev_r(pr.permute(2, 0, 1).contiguous())
+        pr = aux.prev_r
+        planes = pr.permute(2, 0, 1) if isinstance(pr, torch.Tensor) else None
+        if not (planes is not None and planes.is_cuda and planes.dtype == torch.float32
+                and planes.device == img.device and planes.is_contiguous()):
+            # (the streaming case passes the previous state's r, a view of its
+            # planes: used as it is, no (H, W, 3) round trip)
+            planes = as_cuda(pr, device=img.device).permute(2, 0, 1).contiguous()
+        solver.set_prev_r(planes)
     else:
         solver.set_prev_r(None)
     solver.installed = (frame, aux)
