@@ -216,13 +216,18 @@ __global__ void k_sample(const __grid_constant__ SampleParams P, const SampleSta
         tp |= (uint32_t)(((unsigned long long)st.next() * 2ULL) >> 32) << d;
       }
     }
+    int x = p0 % W, y = p0 / W;
 #pragma unroll
-    for (int pp = 0; pp < kSamplePix; ++pp) {
+    for (int pp = 0; pp < kSamplePix; ++pp, ++x) {
       if (pp >= np) break;
       const int p = p0 + pp;
-      const int x = p % W, y = p / W;
+      if (x == W) {
+        x = 0;
+        ++y;
+      }
       const double c0 = ch[p], c1 = ch[N + p];
       int cnt = 0;
+      uint32_t packed[2] = {0u, 0u};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int d = 4 * pp + k;
@@ -248,8 +253,9 @@ __global__ void k_sample(const __grid_constant__ SampleParams P, const SampleSta
           ++cnt;
           if (!tk) atomicAdd(in_cnt + q, 1);
         }
-        codes[4 * p + k] = code;
+        packed[k >> 1] |= (uint32_t)(uint16_t)code << (16 * (k & 1));
       }
+      reinterpret_cast<uint2*>(codes)[p] = make_uint2(packed[0], packed[1]);   // the 4 codes, one store
       out_cnt[p] = cnt;
     }
   }
@@ -340,24 +346,47 @@ __global__ void k_degree(int N, const int32_t* a, const int32_t* b, int32_t* deg
 }
 
 // out entries in slot order (keys 0..3), incoming entries keyed by 4 + 4*src + slot
+// out entries first, in slot order (keys 0..3) at fixed positions (the rank
+// of the slot among the pixel's kept draws: no atomics); incoming entries
+// after them, keyed by 4 + 4*src + slot, placed by an atomic counter of the
+// destination row (k_sort_rows* restores their key order)
 __global__ void k_fill_samples(const int16_t* __restrict__ codes, int H, int W, const int32_t* __restrict__ row_ptr,
-                               int32_t* fill, uint16_t* ent, uint32_t* key) {
+                               const int32_t* __restrict__ out_cnt, int32_t* fill, uint16_t* ent, uint32_t* key) {
   const int N = H * W;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
     const int x = p % W, y = p / W;
+    const int a = row_ptr[p];
+    const uint2 packed = __ldg(reinterpret_cast<const uint2*>(codes) + p);   // the pixel's 4 codes
+    int16_t c[4];
+    c[0] = (int16_t)(packed.x & 0xffffu);
+    c[1] = (int16_t)(packed.x >> 16);
+    c[2] = (int16_t)(packed.y & 0xffffu);
+    c[3] = (int16_t)(packed.y >> 16);
+    // the incoming slots first: the four partner rows' bounds and atomic
+    // counters are requested together, their latencies overlap
+    int dst[4];
+#pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int16_t c = codes[4 * p + k];
-      if (c < 0) continue;
-      const int pos = atomicAdd(fill + p, 1);
-      ent[row_ptr[p] + pos] = (uint16_t)c;
-      key[row_ptr[p] + pos] = (uint32_t)k;
-      if (!(c & kEntTemporal)) {
+      dst[k] = -1;
+      if (c[k] >= 0 && !(c[k] & kEntTemporal)) {
         int dy, dx;
-        decode_offset((uint16_t)c, dy, dx);
+        decode_offset((uint16_t)c[k], dy, dx);
         const int q = (y + dy) * W + (x + dx);
-        const int pq = atomicAdd(fill + q, 1);
-        ent[row_ptr[q] + pq] = make_ent(-dy, -dx, false, true);
-        key[row_ptr[q] + pq] = 4u + 4u * (uint32_t)p + (uint32_t)k;
+        dst[k] = __ldg(row_ptr + q) + __ldg(out_cnt + q) + atomicAdd(fill + q, 1);
+      }
+    }
+    int own = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (c[k] < 0) continue;
+      ent[a + own] = (uint16_t)c[k];
+      key[a + own] = (uint32_t)k;
+      ++own;
+      if (dst[k] >= 0) {
+        int dy, dx;
+        decode_offset((uint16_t)c[k], dy, dx);
+        ent[dst[k]] = make_ent(-dy, -dx, false, true);
+        key[dst[k]] = 4u + 4u * (uint32_t)p + (uint32_t)k;
       }
     }
   }
@@ -688,8 +717,8 @@ void launch_degree(cudaStream_t s, int N, const int32_t* a, const int32_t* b, in
   k_degree<<<grid_for(N), 256, 0, s>>>(N, a, b, deg);
 }
 void launch_fill_from_samples(cudaStream_t s, const int16_t* codes, int H, int W, const int32_t* row_ptr,
-                              int32_t* fill, uint16_t* ent, uint32_t* key) {
-  k_fill_samples<<<grid_for((int64_t)H * W), 256, 0, s>>>(codes, H, W, row_ptr, fill, ent, key);
+                              const int32_t* out_cnt, int32_t* fill, uint16_t* ent, uint32_t* key) {
+  k_fill_samples<<<grid_for((int64_t)H * W), 256, 0, s>>>(codes, H, W, row_ptr, out_cnt, fill, ent, key);
 }
 void launch_fill_from_pairs(cudaStream_t s, int64_t n, const int64_t* src, const int64_t* dst,
                             const uint8_t* temporal, const double* weight, int W, const int32_t* row_ptr,

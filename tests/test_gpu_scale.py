@@ -55,6 +55,29 @@ def test_1080p_sampler_and_segment_bit_exact():
     assert np.array_equal(ids, O.segment(img1, clip.colors))
 
 
+def test_1080p_sampler_with_a_rejection_bit_exact():
+    """Seed 95's u32 stream has a zero word at 16,473,226 (< 8 N at 1080p:
+    a Lemire rejection in the dy draws; tools/find_rejection_seed.py).  The
+    device finds it, shifts the rest of the stream and redraws: the threads of
+    the warp holding the zero seek by the full jump, every other thread from
+    its warp's base state.  Pairs equal numpy's, with and without the temporal
+    section (which the shift moves as well)."""
+    clip = _clip(1080, 1920, 8, n=2, seed=4)
+    from paper_1908_01961_b200.imaging import Frame, chromaticity
+    from paper_1908_01961_b200.energy import sample_consistency
+    f0, f1 = (Frame(f.cuda()) for f in clip.frames)
+    c0, c1 = chromaticity(f0), chromaticity(f1)
+    img0 = clip.frames[0].double().numpy()
+    img1 = clip.frames[1].double().numpy()
+    oc0, oc1 = O.chromaticity(img0)[0], O.chromaticity(img1)[0]
+    for prev, oprev in ((None, None), (c0, oc0)):
+        s = sample_consistency(c1, prev, 95)
+        ref = O.sample_pairs(oc1, oprev, 95)
+        assert np.array_equal(s.src.cpu().numpy(), ref.src)
+        assert np.array_equal(s.dst.cpu().numpy(), ref.dst)
+        assert np.array_equal(s.temporal.cpu().numpy(), ref.temporal)
+
+
 def test_1080p_operator_symmetric_and_step_deterministic():
     from paper_1908_01961_b200.energy import assemble_blocks
     from paper_1908_01961_b200.solver import gn_step_sparse
