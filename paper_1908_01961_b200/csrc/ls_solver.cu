@@ -119,6 +119,31 @@ __device__ __forceinline__ float rsqrtf_fast(float v) {
   return r;
 }
 
+// Tile coordinates of a persistent CTA's walk (tile = blockIdx.x + j gridDim.x)
+// kept incrementally: the div / mod by the tile-row count cost ~35
+// instructions per thread and tile (~3% of the operator's) when recomputed.
+#ifndef LS_TILEWALK
+#define LS_TILEWALK 1   // 0: recompute tile / ntx, tile % ntx every tile (A/B)
+#endif
+struct TileWalk {
+  int tx, ty, sx, sy, ntx;
+  __device__ __forceinline__ TileWalk(int t0, int stride, int n) : ntx(n) {
+    tx = t0 % n;
+    ty = t0 / n;
+    sx = stride % n;
+    sy = stride / n;
+  }
+  __device__ __forceinline__ void next(int& nx, int& ny) const {
+    nx = tx + sx;
+    ny = ty + sy;
+    if (nx >= ntx) {
+      nx -= ntx;
+      ++ny;
+    }
+  }
+  __device__ __forceinline__ void advance() { next(tx, ty); }
+};
+
 // non-negativity weight (energy.py:115-118) with the MUFU reciprocal
 __device__ __forceinline__ float nonneg_wf(float t, float eps) { return t > 0.f ? 0.f : rcpf(fabsf(t) + eps); }
 
@@ -250,16 +275,17 @@ struct EPre {
   int id, e0, e1;
 };
 __device__ __forceinline__ EPre energy_prefetch(const Frame& f, int x, int y, bool own) {
-  EPre p{{0.f, 0.f, 0.f}, 0.f, 0, 0, 0};
-  if (own) {
-    const int i = y * f.W + x;
+  // branch-free (pixel 0 stands in for a pixel outside the image; its values
+  // are never used): inside an `if`, the compiler converted the image values
+  // to fp64 right after their loads, stalling on them before the TMA wait
+  EPre p;
+  const int i = own ? y * f.W + x : 0;
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) p.img[ch] = __ldg(f.img + ch * f.N + i);
-    p.edge = __ldg(f.edge + i);
-    p.id = f.ids ? __ldg(f.ids + i) : 0;
-    p.e0 = __ldg(f.row_ptr + i);
-    p.e1 = __ldg(f.row_ptr + i + 1);
-  }
+  for (int ch = 0; ch < 3; ++ch) p.img[ch] = __ldg(f.img + ch * f.N + i);
+  p.edge = __ldg(f.edge + i);
+  p.id = f.ids ? __ldg(f.ids + i) : 0;
+  p.e0 = __ldg(f.row_ptr + i);
+  p.e1 = __ldg(f.row_ptr + i + 1);
   return p;
 }
 
@@ -631,10 +657,12 @@ __global__ void __launch_bounds__(kThreads, LS_EG_MINB) k_energy(Frame f, Coef<f
     __syncthreads();
   }
   uint32_t phase = 0;
-  for (int j = 0;; ++j) {
+  TileWalk walk(blockIdx.x, gridDim.x, ntx);
+  for (int j = 0;; ++j, walk.advance()) {
     const int tile = blockIdx.x + j * gridDim.x;
     if (tile >= ntiles) break;
-    const int tx0 = (tile % ntx) * kTileW, ty0 = f.y_lo + (tile / ntx) * kTileH;
+    const int tx0 = (LS_TILEWALK ? walk.tx : tile % ntx) * kTileW,
+              ty0 = f.y_lo + (LS_TILEWALK ? walk.ty : tile / ntx) * kTileH;
     const int st = (NST == 2) ? (j & 1) : 0;
     float* sX = smem + st * STAGE;
     float* sXR = sX + e_off_XR(NT);
@@ -674,7 +702,12 @@ __global__ void __launch_bounds__(kThreads, LS_EG_MINB) k_energy(Frame f, Coef<f
       __syncthreads();
       if (threadIdx.x == 0) {
         const int t = blockIdx.x + (j + NST) * gridDim.x;
-        if (t < ntiles) tma_issue_energy<NT>(sX, maps, &bars[st], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH, with_d);
+        if (t < ntiles) {   // NST tiles ahead
+          TileWalk w2 = walk;
+#pragma unroll
+          for (int a = 0; a < NST; ++a) w2.advance();
+          tma_issue_energy<NT>(sX, maps, &bars[st], w2.tx * kTileW, f.y_lo + w2.ty * kTileH, with_d);
+        }
       }
     }
   }
@@ -1039,10 +1072,12 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
   bool pend = false;
   size_t pend_i = 0;
 #endif
-  for (int j = 0;; ++j) {
+  TileWalk walk(blockIdx.x, gridDim.x, ntx);
+  for (int j = 0;; ++j, walk.advance()) {
     const int tile = blockIdx.x + j * gridDim.x;
     if (tile >= ntiles) break;
-    const int tx0 = (tile % ntx) * kTileW, ty0 = f.y_lo + (tile / ntx) * kTileH;
+    const int tx0 = (LS_TILEWALK ? walk.tx : tile % ntx) * kTileW,
+              ty0 = f.y_lo + (LS_TILEWALK ? walk.ty : tile / ntx) * kTileH;
     const int x = tx0 + lx, y = ty0 + ly;
     const bool own = x < W && y < f.y_hi;
     const PixPre pre = pix_prefetch(f, x, y, own);
@@ -1118,7 +1153,9 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
         __syncthreads();
         if (threadIdx.x == 0) {
           const int t = blockIdx.x + (j + 1) * gridDim.x;
-          if (t < ntiles) tma_issue_pprev<NT>(smem, maps, &bars[2], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH);
+          int nx, ny;
+          walk.next(nx, ny);
+          if (t < ntiles) tma_issue_pprev<NT>(smem, maps, &bars[2], nx * kTileW, f.y_lo + ny * kTileH);
         }
       }
     }
@@ -1167,9 +1204,11 @@ __global__ void __launch_bounds__(kThreads, LS_PCG_MINB) k_pcg_apply(Frame f, Co
       if (threadIdx.x == 0) {
         const int t = blockIdx.x + (j + 1) * gridDim.x;
         if (t < ntiles) {
-          tma_issue_pcg<NT>(smem, maps, &bars[0], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH, with_p);
+          int nx, ny;
+          walk.next(nx, ny);
+          tma_issue_pcg<NT>(smem, maps, &bars[0], nx * kTileW, f.y_lo + ny * kTileH, with_p);
           if (LS_PEARLY && with_p && xupd)   // the deferred x-update still needed p_{i-1} here
-            tma_issue_pprev<NT>(smem, maps, &bars[2], (t % ntx) * kTileW, f.y_lo + (t / ntx) * kTileH);
+            tma_issue_pprev<NT>(smem, maps, &bars[2], nx * kTileW, f.y_lo + ny * kTileH);
         }
       }
     }

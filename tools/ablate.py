@@ -47,6 +47,8 @@ if __name__ == "__main__":
                 extra = ["-DLS_PFORM_GLOBAL=1", "-DLS_PCG_MINB=4"]
             elif n == 209:      # operator: p_{i-1} read from L2 in the formation, 3 CTAs/SM
                 extra = ["-DLS_PFORM_GLOBAL=1"]
+            elif n == 210:      # tile coordinates by div / mod every tile (before the incremental walk)
+                extra = ["-DLS_TILEWALK=0"]
             build_variant(n, extra)
     else:
         for n in [0] + variants:
