@@ -156,6 +156,8 @@ struct ls_ctx {
   bool band_dev = false;         // inside ls_band_frame_begin / _end: device-side decisions
   float* ring[3] = {nullptr, nullptr, nullptr};   // state buffers of the graph flip-flop
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t cond_stream = nullptr;      // captures the bodies of graph conditional nodes
+  bool use_cond = false;                   // LS_GRAPH_COND=1: halvings as graph conditional nodes
   cudaGraphExec_t graph_exec = nullptr;
   unsigned char graph_key[1024] = {0};
   long long graph_launches = 0;
@@ -311,6 +313,7 @@ int ls_ctx_create(int device, int H, int W, int K, const ls_weights* w, const ls
   set_geometry(c);
   c->use_tma = (W % 4 == 0) && tma_encode_fn() != nullptr && std::getenv("LS_NO_TMA") == nullptr;
   c->x_deferred = std::getenv("LS_X_DEFERRED") != nullptr && std::string(std::getenv("LS_X_DEFERRED")) == "1";
+  c->use_cond = std::getenv("LS_GRAPH_COND") != nullptr && std::string(std::getenv("LS_GRAPH_COND")) == "1";
   {   // opt-in single-reduction PCG (whole frames with TMA only)
     const char* pv = std::getenv("LS_PCG");
     c->pcg_cg1 = pv && std::string(pv) == "cg1" && c->use_tma;
@@ -453,6 +456,7 @@ int ls_ctx_destroy(ls_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->cond_stream) cudaStreamDestroy(c->cond_stream);
   for (void* p : c->allocs) cudaFree(p);
   for (auto& e : c->prof.pool) cudaEventDestroy(e);
   cudaFree(c->ent);
@@ -1220,6 +1224,51 @@ int ls_gn_step(ls_ctx* c, const double* colors, const float* X, float* X_out, ls
   return LS_OK;
 }
 
+// Graph conditional nodes for the line-search halvings (opt-in,
+// LS_GRAPH_COND=1 at context creation: measured slower -- 61.6 / 62.0 vs
+// 62.3 / 62.4 frames/s at 1080p K=8 in two A/B pairs; the conditional nodes
+// cost the graph more than the 16 early-exit launches per frame they
+// remove).  Under stream capture,
+// trial h >= 1 is the body of an IF node whose handle trial h-1's last CTA
+// sets (1 while the search is undecided); the handle defaults to 0 at every
+// graph launch, so a decided search -- or a skipped predecessor -- skips the
+// rest without launching them (the eager path launches them and they exit
+// at once).  cond_open adds the node after the capture's current
+// dependencies and redirects the context's launches into the body.
+static int cond_open(ls_ctx* c, cudaGraphConditionalHandle h, cudaStream_t* saved) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  LS_CK(cudaStreamGetCaptureInfo(c->stream, &st, &id, &g, &deps, &nd));
+  LS_ARG(st == cudaStreamCaptureStatusActive, "conditional node outside a capture");
+  alignas(cudaGraphNodeParams) unsigned char pbuf[sizeof(cudaGraphNodeParams)];
+  std::memset(pbuf, 0, sizeof(pbuf));      // (no default constructor: unions)
+  cudaGraphNodeParams& p = *reinterpret_cast<cudaGraphNodeParams*>(pbuf);
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeIf;
+  p.conditional.size = 1;
+  cudaGraphNode_t node = nullptr;
+  LS_CK(cudaGraphAddNode(&node, g, deps, nd, &p));
+  LS_CK(cudaStreamUpdateCaptureDependencies(c->stream, &node, 1, cudaStreamSetCaptureDependencies));
+  if (!c->cond_stream) LS_CK(cudaStreamCreateWithFlags(&c->cond_stream, cudaStreamNonBlocking));
+  LS_CK(cudaStreamBeginCaptureToGraph(c->cond_stream, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeThreadLocal));
+  *saved = c->stream;
+  c->stream = c->cond_stream;
+  return LS_OK;
+}
+
+static int cond_close(ls_ctx* c, cudaStream_t saved) {
+  cudaGraph_t body = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(c->stream, &body);
+  c->stream = saved;
+  LS_CK(e);
+  return LS_OK;
+}
+
 // Whole streaming flip-flop (solver.py:311-338 with refine = False) enqueued
 // without host round trips: per GN step the EG kernel, the PCG, up to
 // max_halvings+1 trial kernels deciding accept / halve on the device, and a
@@ -1242,13 +1291,36 @@ static int enqueue_flip_flop(ls_ctx* c, const double* colors, float* const bufs[
       if (rc) return rc;
       EnergyMaps em;
       const bool etma = energy_maps(c, bufs[in_id], c->x, &em);
+      // under capture: trials 1.. as conditional nodes (handles made first:
+      // each trial's kernel carries its successor's)
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      LS_CK(cudaStreamIsCapturing(c->stream, &cs));
+      const bool cond = cs == cudaStreamCaptureStatusActive && c->use_cond && c->cfg.max_halvings > 0;
+      std::vector<cudaGraphConditionalHandle> hs(c->cfg.max_halvings + 2, 0);
+      if (cond) {
+        cudaStreamCaptureStatus st;
+        unsigned long long id = 0;
+        cudaGraph_t g = nullptr;
+        LS_CK(cudaStreamGetCaptureInfo(c->stream, &st, &id, &g, nullptr, nullptr));
+        for (int h = 1; h <= c->cfg.max_halvings; ++h)
+          LS_CK(cudaGraphConditionalHandleCreate(&hs[h], g, 0, cudaGraphCondAssignDefault));
+      }
       double alpha = 1.0;
       for (int h = 0; h <= c->cfg.max_halvings; ++h, alpha *= 0.5) {
+        cudaStream_t saved = nullptr;
+        if (cond && h >= 1) {
+          const int rc = cond_open(c, hs[h], &saved);
+          if (rc) return rc;
+        }
         const size_t pi = prof_begin(c);
         launch_energy(1, L_energy(c), f, cd, bufs[in_id], c->x, (float)alpha, nullptr, bufs[out_id], nullptr, nullptr,
                       nullptr, nullptr, nullptr, c->part, c->tickets + 0, c->sc, etma ? &em : nullptr, c->ctl, 1,
-                      h == c->cfg.max_halvings);
+                      h == c->cfg.max_halvings, hs[h + 1]);
         prof_end(c, PC_TRIAL, pi);
+        if (cond && h >= 1) {
+          const int rc = cond_close(c, saved);
+          if (rc) return rc;
+        }
       }
       launch_step_end(c->stream, c->grid_update, c->ctl, c->sc, bufs[in_id], bufs[out_id], M, out_id, c->recs);
       c->launches += 2 + c->cfg.max_halvings;

@@ -44,7 +44,8 @@ struct Launch {
 void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
                    const float* dx, float alpha, const float* Y, float* Xout, float* r_out, float* d_out,
                    float* u_out, float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc,
-                   const EnergyMaps* maps, const FrameCtl* ctl = nullptr, int dev_ls = 0, int last_trial = 0);
+                   const EnergyMaps* maps, const FrameCtl* ctl = nullptr, int dev_ls = 0, int last_trial = 0,
+                   unsigned long long next_cond = 0);   // a trial's successor's graph conditional handle
 void launch_frame_init(cudaStream_t s, FrameCtl* ctl);
 void launch_step_end(cudaStream_t s, int grid, FrameCtl* ctl, const Scalars* sc, const float* Xin, float* Xout,
                      int64_t M, int out_id, StepRecord* recs);

@@ -616,7 +616,8 @@ __global__ void __launch_bounds__(kThreads, LS_EG_MINB) k_energy(Frame f, Coef<f
                                                      float* __restrict__ diag_raw, double* part,
                                                      unsigned* ticket, Scalars* sc, int ntiles,
                                                      const FrameCtl* ctl, int dev_ls, int last_trial,
-                                                     const __grid_constant__ EnergyMaps maps) {
+                                                     const __grid_constant__ EnergyMaps maps,
+                                                     unsigned long long next_cond) {
   constexpr int U = NT + 3;
   constexpr bool TRIAL = MODE == MODE_TRIAL;
   pdl_wait();
@@ -724,6 +725,9 @@ __global__ void __launch_bounds__(kThreads, LS_EG_MINB) k_energy(Frame f, Coef<f
       fin_energy_eg(tot, sc, r_out != nullptr);
     } else {
       fin_energy_trial(tot, sc, alpha, dev_ls, last_trial);
+      // CUDA-graph flip-flop: the next halving's trial is the body of a
+      // conditional node; it runs only while the line search is undecided
+      if (next_cond) cudaGraphSetConditional(next_cond, sc->ls_done ? 0u : 1u);
     }
     *ticket = 0u;
   }
@@ -1648,28 +1652,30 @@ template <int NT, int MODE>
 static void launch_energy_mt(const Launch& L, const Frame& f, const Coef<float>& c, const float* X, const float* dx,
                              float alpha, const float* Y, float* Xout, float* r_out, float* d_out, float* u_out,
                              float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc,
-                             const EnergyMaps* maps, const FrameCtl* ctl, int dev_ls, int last_trial) {
+                             const EnergyMaps* maps, const FrameCtl* ctl, int dev_ls, int last_trial,
+                             unsigned long long next_cond) {
   if (maps)
     launch_pdl(k_energy<NT, MODE, true>, L.grid, kThreads, energy_smem<NT>(MODE, true), L.stream,
                f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, ctl,
-               dev_ls, last_trial, *maps);
+               dev_ls, last_trial, *maps, next_cond);
   else
     k_energy<NT, MODE, false><<<L.grid, kThreads, energy_smem<NT>(MODE, false), L.stream>>>(
         f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, ctl, dev_ls,
-        last_trial, EnergyMaps{});
+        last_trial, EnergyMaps{}, next_cond);
 }
 
 template <int NT>
 static void launch_energy_nt(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
                              const float* dx, float alpha, const float* Y, float* Xout, float* r_out, float* d_out,
                              float* u_out, float* b_raw, float* diag_raw, double* part, unsigned* ticket,
-                             Scalars* sc, const EnergyMaps* maps, const FrameCtl* ctl, int dev_ls, int last_trial) {
+                             Scalars* sc, const EnergyMaps* maps, const FrameCtl* ctl, int dev_ls, int last_trial,
+                             unsigned long long next_cond) {
   if (mode == MODE_EG)
     launch_energy_mt<NT, MODE_EG>(L, f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket,
-                                  sc, maps, ctl, dev_ls, last_trial);
+                                  sc, maps, ctl, dev_ls, last_trial, 0ULL);
   else
     launch_energy_mt<NT, MODE_TRIAL>(L, f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part,
-                                     ticket, sc, maps, ctl, dev_ls, last_trial);
+                                     ticket, sc, maps, ctl, dev_ls, last_trial, next_cond);
 }
 
 template <int NT>
@@ -1686,9 +1692,11 @@ static void launch_apply_nt(const Launch& L, const Frame& f, const Coef<float>& 
 void launch_energy(int mode, const Launch& L, const Frame& f, const Coef<float>& c, const float* X,
                    const float* dx, float alpha, const float* Y, float* Xout, float* r_out, float* d_out,
                    float* u_out, float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc,
-                   const EnergyMaps* maps, const FrameCtl* ctl, int dev_ls, int last_trial) {
+                   const EnergyMaps* maps, const FrameCtl* ctl, int dev_ls, int last_trial,
+                   unsigned long long next_cond) {
   LS_DISPATCH_NT(f.NT, (launch_energy_nt<NT_>(mode, L, f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw,
-                                              diag_raw, part, ticket, sc, maps, ctl, dev_ls, last_trial)));
+                                              diag_raw, part, ticket, sc, maps, ctl, dev_ls, last_trial,
+                                              next_cond)));
 }
 
 // ---------------------------------------------------------------------------

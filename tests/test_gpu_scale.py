@@ -258,6 +258,38 @@ def test_graph_flip_flop_equals_eager_and_replays():
         assert torch.equal(Xa, Xb)
 
 
+def test_graph_conditional_halvings_equal_eager(monkeypatch):
+    """Opt-in LS_GRAPH_COND=1: the line-search halvings captured as graph
+    conditional nodes (a trial's last CTA enables its successor) give the
+    eager path's records and state bit for bit -- from rough starting states
+    that make the search halve and reject."""
+    import numpy as np
+    from paper_1908_01961_b200 import _device
+    from paper_1908_01961_b200.energy import install
+    monkeypatch.setenv("LS_GRAPH_COND", "1")
+    clip = _clip(64, 96, 3, n=2, seed=13)
+    st = _state(clip, idx=1)
+    H, W, K = st.frame.height, st.frame.width, st.palette.K
+    from dataclasses import replace
+    from paper_1908_01961_b200.energy import EnergyWeights
+    s = _device.DeviceSolver(st.layers.X.device, H, W, K)      # created with the variable set
+    g = torch.Generator(device="cpu").manual_seed(5)
+    halved = 0
+    for w, iters in ((st.weights, 16), (EnergyWeights(p=0.5, eps_irls=1e-3), 2), (EnergyWeights(p=0.3), 1)):
+        s.configure(w, replace(st.config, pcg_iterations=iters))
+        install(s, st.frame, st.aux)
+        for scale in (0.0, 1.0, 4.0):
+            X0 = st.layers.X.clone()
+            X0 += scale * torch.randn(X0.shape, generator=g).to(X0.device)
+            rg = s.flip_flop_stream(st.palette.colors, X0, 2, 2, 0.0, graph=True)
+            re = s.flip_flop_stream(st.palette.colors, X0, 2, 2, 0.0, graph=False)
+            assert torch.equal(rg[3], re[3])
+            assert [(r.energy_after, r.alpha, r.accepted) for r in rg[1]] == \
+                [(r.energy_after, r.alpha, r.accepted) for r in re[1]]
+            halved += sum(1 for r in re[1] if r.alpha != 1.0)
+    assert halved > 0, "no halving exercised"
+
+
 def test_graph_recaptures_when_the_palette_changes():
     """The captured flip-flop bakes the palette into its kernels: a new
     palette must re-capture (results equal the eager path for A, B, A)."""
