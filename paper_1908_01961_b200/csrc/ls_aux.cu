@@ -167,7 +167,7 @@ __global__ void k_edge(const double* __restrict__ ch, int H, int W, float* __res
 // reported through S.new_zero and the pass is repeated on the device
 // (k_sample_fix / redo) -- no host round trip.
 #ifndef LS_SAMPLE_PIX
-#define LS_SAMPLE_PIX 8
+#define LS_SAMPLE_PIX 4   // 4: 176 -> 116 us per streaming frame vs 8 (2: 141 us; tools/ablate.py 206, 212)
 #endif
 constexpr int kSamplePix = LS_SAMPLE_PIX;
 constexpr double kGateSq = 0x1.47ae147ae147ap-9;   // max{s : sqrt_rn(s) < 0.05}

@@ -122,6 +122,9 @@ __device__ __forceinline__ float rsqrtf_fast(float v) {
 // Tile coordinates of a persistent CTA's walk (tile = blockIdx.x + j gridDim.x)
 // kept incrementally: the div / mod by the tile-row count cost ~35
 // instructions per thread and tile (~3% of the operator's) when recomputed.
+#ifndef LS_UPD_F32P
+#define LS_UPD_F32P 0
+#endif
 #ifndef LS_TILEWALK
 #define LS_TILEWALK 1   // 0: recompute tile / ntx, tile % ntx every tile (A/B)
 #endif
@@ -1543,10 +1546,28 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(int64_t M, float* __res
     const float4 di = __ldg(reinterpret_cast<const float4*>(dinv) + j);
     float4 zn;
     double rz = 0.0, rn = 0.0;
+#if LS_UPD_F32P
+    {   // the float4's four products summed in fp32, one fp64 add each (A/B)
+      float rz4 = 0.f, rn4 = 0.f;
+      auto one4 = [&](float zv, float qv, float dv, float& znv) {
+        znv = fmaf(-a, qv * dv, zv);
+        const float rr = znv * rcpf(dv);
+        rz4 = fmaf(rr, znv, rz4);
+        rn4 = fmaf(rr, rr, rn4);
+      };
+      one4(zz.x, qq.x, di.x, zn.x);
+      one4(zz.y, qq.y, di.y, zn.y);
+      one4(zz.z, qq.z, di.z, zn.z);
+      one4(zz.w, qq.w, di.w, zn.w);
+      rz = (double)rz4;
+      rn = (double)rn4;
+    }
+#else
     one(zz.x, qq.x, di.x, zn.x, rz, rn);
     one(zz.y, qq.y, di.y, zn.y, rz, rn);
     one(zz.z, qq.z, di.z, zn.z, rz, rn);
     one(zz.w, qq.w, di.w, zn.w, rz, rn);
+#endif
     if (NORM) {
     } else if (LAST) {
       const float4 pp = __ldg(reinterpret_cast<const float4*>(p) + j);

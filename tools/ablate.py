@@ -39,7 +39,7 @@ if __name__ == "__main__":
                 extra = ["-DLS_XDEFER=1"]
             elif n == 205:      # energy kernel at 2 CTAs/SM (more registers, no rematerialisation)
                 extra = ["-DLS_EG_MINB=2"]
-            elif n == 206:      # sampler: 4 pixels per thread (twice the threads) instead of 8
+            elif n == 206:      # sampler: 4 pixels per thread (now the default)
                 extra = ["-DLS_SAMPLE_PIX=4"]
             elif n == 207:      # operator: the p window loaded with the tile's other windows (round 1)
                 extra = ["-DLS_PEARLY=0"]
@@ -49,6 +49,12 @@ if __name__ == "__main__":
                 extra = ["-DLS_PFORM_GLOBAL=1"]
             elif n == 210:      # tile coordinates by div / mod every tile (before the incremental walk)
                 extra = ["-DLS_TILEWALK=0"]
+            elif n == 212:      # sampler: 2 pixels per thread
+                extra = ["-DLS_SAMPLE_PIX=2"]
+            elif n == 213:      # sampler: 8 pixels per thread (the round-2 default before 4)
+                extra = ["-DLS_SAMPLE_PIX=8"]
+            elif n == 211:      # update: a float4's products summed in fp32 before the fp64 accumulators
+                extra = ["-DLS_UPD_F32P=1"]
             build_variant(n, extra)
     else:
         for n in [0] + variants:
