@@ -346,12 +346,16 @@ __global__ void k_degree(int N, const int32_t* a, const int32_t* b, int32_t* deg
 }
 
 // out entries in slot order (keys 0..3), incoming entries keyed by 4 + 4*src + slot
-// out entries first, in slot order (keys 0..3) at fixed positions (the rank
-// of the slot among the pixel's kept draws: no atomics); incoming entries
-// after them, keyed by 4 + 4*src + slot, placed by an atomic counter of the
-// destination row (k_sort_rows* restores their key order)
+// Sampled adjacency rows: the pixel's own draws first, in slot order, at
+// fixed positions (their rank among its kept draws: no atomics), then the
+// incoming entries, placed by an atomic counter of the destination row.
+// The reference order of the incoming entries is by source pixel (then slot),
+// and a source p = q + dy W + dx (|dx| <= 7 < W) ascends with the (dy, dx) the
+// entry code stores row-major -- so sorting the incoming segment by the code
+// itself restores it (equal codes are the same source: interchangeable).  No
+// sort keys are written.
 __global__ void k_fill_samples(const int16_t* __restrict__ codes, int H, int W, const int32_t* __restrict__ row_ptr,
-                               const int32_t* __restrict__ out_cnt, int32_t* fill, uint16_t* ent, uint32_t* key) {
+                               const int32_t* __restrict__ out_cnt, int32_t* fill, uint16_t* ent) {
   const int N = H * W;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
     const int x = p % W, y = p / W;
@@ -380,13 +384,11 @@ __global__ void k_fill_samples(const int16_t* __restrict__ codes, int H, int W, 
     for (int k = 0; k < 4; ++k) {
       if (c[k] < 0) continue;
       ent[a + own] = (uint16_t)c[k];
-      key[a + own] = (uint32_t)k;
       ++own;
       if (dst[k] >= 0) {
         int dy, dx;
         decode_offset((uint16_t)c[k], dy, dx);
         ent[dst[k]] = make_ent(-dy, -dx, false, true);
-        key[dst[k]] = 4u + 4u * (uint32_t)p + (uint32_t)k;
       }
     }
   }
@@ -554,6 +556,47 @@ __global__ void __launch_bounds__(32 * kWarpSortWarps) k_sort_rows_warp(int N, c
   }
 }
 
+// The sampled rows' incoming segments sorted by entry code (k_fill_samples),
+// warp-cooperative like k_sort_rows_warp: a warp's 32 rows are one contiguous
+// span, loaded into shared memory coalesced, sorted per lane, stored back.
+constexpr int kEntSpan = 1024;
+__global__ void __launch_bounds__(32 * kWarpSortWarps) k_sort_incoming_warp(int N, const int32_t* __restrict__ row_ptr,
+                                                                            const int32_t* __restrict__ out_cnt,
+                                                                            uint16_t* ent) {
+  __shared__ uint16_t se[kWarpSortWarps][kEntSpan];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint16_t* E = se[wid];
+  const int nwarps = gridDim.x * kWarpSortWarps;
+  for (int p0 = (blockIdx.x * kWarpSortWarps + wid) * 32; p0 < N; p0 += nwarps * 32) {
+    const int p = p0 + lane;
+    const int pend = min(p0 + 32, N);
+    const int a0 = row_ptr[p0];
+    const int span = row_ptr[pend] - a0;
+    const int ra = p < N ? row_ptr[p] + out_cnt[p] : 0, rb = p < N ? row_ptr[p + 1] : 0;
+    auto isort = [](uint16_t* v, int lo, int hi) {
+      for (int i = lo + 1; i < hi; ++i) {
+        const uint16_t e = v[i];
+        int j = i - 1;
+        while (j >= lo && v[j] > e) {
+          v[j + 1] = v[j];
+          --j;
+        }
+        v[j + 1] = e;
+      }
+    };
+    if (span <= kEntSpan) {
+      for (int j = lane; j < span; j += 32) E[j] = ent[a0 + j];
+      __syncwarp();
+      isort(E, ra - a0, rb - a0);
+      __syncwarp();
+      for (int j = lane; j < span; j += 32) ent[a0 + j] = E[j];
+      __syncwarp();
+    } else {
+      isort(ent, ra, rb);
+    }
+  }
+}
+
 __global__ void k_pairs_from_samples(const int16_t* __restrict__ codes, int H, int W, const int32_t* __restrict__ off,
                                      int64_t* src, int64_t* dst, uint8_t* temporal) {
   const int N = H * W;
@@ -717,8 +760,11 @@ void launch_degree(cudaStream_t s, int N, const int32_t* a, const int32_t* b, in
   k_degree<<<grid_for(N), 256, 0, s>>>(N, a, b, deg);
 }
 void launch_fill_from_samples(cudaStream_t s, const int16_t* codes, int H, int W, const int32_t* row_ptr,
-                              const int32_t* out_cnt, int32_t* fill, uint16_t* ent, uint32_t* key) {
-  k_fill_samples<<<grid_for((int64_t)H * W), 256, 0, s>>>(codes, H, W, row_ptr, out_cnt, fill, ent, key);
+                              const int32_t* out_cnt, int32_t* fill, uint16_t* ent) {
+  k_fill_samples<<<grid_for((int64_t)H * W), 256, 0, s>>>(codes, H, W, row_ptr, out_cnt, fill, ent);
+  const int N = H * W;
+  k_sort_incoming_warp<<<grid_for(((int64_t)N + 31) / 32, kWarpSortWarps), 32 * kWarpSortWarps, 0, s>>>(
+      N, row_ptr, out_cnt, ent);
 }
 void launch_fill_from_pairs(cudaStream_t s, int64_t n, const int64_t* src, const int64_t* dst,
                             const uint8_t* temporal, const double* weight, int W, const int32_t* row_ptr,

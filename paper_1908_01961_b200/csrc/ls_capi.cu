@@ -658,8 +658,7 @@ int ls_sample_consistency(ls_ctx* c, const double* chroma, const double* prev_ch
   LS_CK(cudaMemsetAsync(c->deg + N, 0, sizeof(int32_t), c->stream));
   LS_CK(launch_scan(c->stream, c->deg, c->row_ptr, (int64_t)N + 1, 0, c->cub_tmp));
   LS_CK(cudaMemsetAsync(c->fill, 0, sizeof(int32_t) * N, c->stream));
-  launch_fill_from_samples(c->stream, c->codes, c->H, c->W, c->row_ptr, c->out_cnt, c->fill, c->ent, c->key);
-  launch_sort_rows(c->stream, N, c->row_ptr, c->ent, c->key, nullptr);
+  launch_fill_from_samples(c->stream, c->codes, c->H, c->W, c->row_ptr, c->out_cnt, c->fill, c->ent);
   // pair offsets (src-major, slot order) for ls_get_pairs / ls_pair_count
   LS_CK(launch_scan(c->stream, c->out_cnt, c->pair_off, (int64_t)N + 1, 0, c->cub_tmp));
   LS_CK(cudaGetLastError());

@@ -170,8 +170,9 @@ void launch_zero_scan(cudaStream_t s, const SampleParams& P, unsigned long long 
 void launch_pairs_count(cudaStream_t s, int64_t n, const int64_t* src, const int64_t* dst,
                         const uint8_t* temporal, int H, int W, int32_t* out_cnt, int32_t* in_cnt, int* bad);
 void launch_degree(cudaStream_t s, int N, const int32_t* out_cnt, const int32_t* in_cnt, int32_t* deg);
+// the sampled adjacency's rows in reference order (fill + incoming-segment sort)
 void launch_fill_from_samples(cudaStream_t s, const int16_t* codes, int H, int W, const int32_t* row_ptr,
-                              const int32_t* out_cnt, int32_t* fill, uint16_t* ent, uint32_t* key);
+                              const int32_t* out_cnt, int32_t* fill, uint16_t* ent);
 void launch_fill_from_pairs(cudaStream_t s, int64_t n, const int64_t* src, const int64_t* dst,
                             const uint8_t* temporal, const double* weight, int W, const int32_t* row_ptr,
                             int32_t* fill, uint16_t* ent, uint32_t* key, float* ent_w);

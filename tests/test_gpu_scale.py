@@ -78,6 +78,29 @@ def test_1080p_sampler_with_a_rejection_bit_exact():
         assert np.array_equal(s.temporal.cpu().numpy(), ref.temporal)
 
 
+def test_sampled_adjacency_rows_in_reference_order():
+    """The sampled adjacency (k_fill_samples + incoming segments sorted by
+    entry code) orders every row exactly as the explicit-pairs path
+    (ls_set_pairs: own pairs, then incoming ones by pair index = source
+    pixel, slot), so the operator's fixed-order consistency sums agree bit
+    for bit -- at 1080p, with temporal partners."""
+    from paper_1908_01961_b200.solver import _solver_for
+    clip = _clip(1080, 1920, 8, n=2, seed=4)
+    st0 = _state(clip)
+    st = _state(clip, idx=1, prev=(st0.frame, st0.layers), seed=7)
+    s = _solver_for(st)
+    g = torch.Generator(device="cpu").manual_seed(3)
+    p = torch.randn(st.layers.X.shape, generator=g).to(st.layers.X.device)
+    w_sampled = s.apply(st.palette.colors, st.layers.X, p)
+    from paper_1908_01961_b200.energy import _guard_csr
+    src, dst, tmp = s.get_pairs()
+    _guard_csr(s)
+    s.set_pairs(src, dst, tmp)
+    w_pairs = s.apply(st.palette.colors, st.layers.X, p)
+    s.installed = None            # the context's adjacency is no longer the aux's
+    assert torch.equal(w_sampled, w_pairs)
+
+
 def test_1080p_operator_symmetric_and_step_deterministic():
     from paper_1908_01961_b200.energy import assemble_blocks
     from paper_1908_01961_b200.solver import gn_step_sparse
