@@ -147,11 +147,15 @@ __global__ void k_edge(const double* __restrict__ ch, int H, int W, float* __res
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     const int x = i % W, y = i / W;
     const double c0 = ch[i], c1 = ch[N + i];
-    double d = 0.0;
-    if (x < W - 1) d = fmax(d, norm2d(__dsub_rn(ch[i + 1], c0), __dsub_rn(ch[N + i + 1], c1)));
-    if (x > 0) d = fmax(d, norm2d(__dsub_rn(c0, ch[i - 1]), __dsub_rn(c1, ch[N + i - 1])));
-    if (y < H - 1) d = fmax(d, norm2d(__dsub_rn(ch[i + W], c0), __dsub_rn(ch[N + i + W], c1)));
-    if (y > 0) d = fmax(d, norm2d(__dsub_rn(c0, ch[i - W]), __dsub_rn(c1, ch[N + i - W])));
+    // max of the four correctly rounded norms = the root of the largest
+    // squared norm (sqrt_rn is monotone): one square root instead of four
+    auto sq = [](double a, double b) { return __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)); };
+    double s2 = 0.0;
+    if (x < W - 1) s2 = fmax(s2, sq(__dsub_rn(ch[i + 1], c0), __dsub_rn(ch[N + i + 1], c1)));
+    if (x > 0) s2 = fmax(s2, sq(__dsub_rn(c0, ch[i - 1]), __dsub_rn(c1, ch[N + i - 1])));
+    if (y < H - 1) s2 = fmax(s2, sq(__dsub_rn(ch[i + W], c0), __dsub_rn(ch[N + i + W], c1)));
+    if (y > 0) s2 = fmax(s2, sq(__dsub_rn(c0, ch[i - W]), __dsub_rn(c1, ch[N + i - W])));
+    const double d = __dsqrt_rn(s2);
     edge[i] = (float)(1.0 - exp(-50.0 * d));
   }
 }
@@ -827,16 +831,28 @@ void launch_copy(cudaStream_t s, void* dst, const void* src, int64_t bytes) {
 }
 
 // flag = 0 if any value is NaN / inf (flag preset to 1 by the caller)
+// (float4 over a bounded grid when x is 16-byte aligned; a frame is read once)
 __global__ void k_all_finite(const float* __restrict__ x, int64_t n, int* flag) {
   bool ok = true;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t head = 0;
+  if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
+    const int64_t n4 = n >> 2;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+      const float4 v = __ldg(x4 + i);
+      ok = ok && isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
+    }
+    head = n4 << 2;
+  }
+  for (int64_t i = head + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
     ok = ok && isfinite(x[i]);
   if (!__syncthreads_and(ok) && threadIdx.x == 0) *flag = 0;
 }
 __global__ void k_set_flag(int* flag) { *flag = 1; }
 void launch_all_finite(cudaStream_t s, const float* x, int64_t n, int* flag) {
   k_set_flag<<<1, 1, 0, s>>>(flag);
-  if (n > 0) k_all_finite<<<grid_for(n), 256, 0, s>>>(x, n, flag);
+  if (n > 0) k_all_finite<<<std::min(grid_for((n + 3) / 4), 148 * 8), 256, 0, s>>>(x, n, flag);
 }
 
 void launch_set_i32(cudaStream_t s, int32_t* p, int n, int32_t v) {
@@ -864,6 +880,7 @@ template <int OP>
 __global__ void __launch_bounds__(kScanThreads) k_scan(const int* __restrict__ in, int* __restrict__ out, int64_t n,
                                                       unsigned long long* status, unsigned* counter) {
   constexpr int ident = OP == 0 ? 0 : INT_MIN;
+  static_assert(kScanItems == 8, "two int4 per thread");
   __shared__ int s_tile, s_prefix;
   __shared__ int s_warp[kScanThreads / 32];
   if (threadIdx.x == 0) s_tile = (int)atomicAdd(counter, 1u);
@@ -871,9 +888,17 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const int* __restrict__ i
   const int tile = s_tile;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t base = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  const bool vec = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) == 0;
   int v[kScanItems];
+  if (vec && base + kScanItems <= n) {   // 2 x int4 per thread (a 32-byte run)
+    const int4 a = __ldg(reinterpret_cast<const int4*>(in + base));
+    const int4 b = __ldg(reinterpret_cast<const int4*>(in + base) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
 #pragma unroll
-  for (int j = 0; j < kScanItems; ++j) v[j] = base + j < n ? in[base + j] : ident;
+    for (int j = 0; j < kScanItems; ++j) v[j] = base + j < n ? in[base + j] : ident;
+  }
 #pragma unroll
   for (int j = 1; j < kScanItems; ++j) v[j] = scan_op<OP>(v[j - 1], v[j]);   // thread-inclusive
   int t = v[kScanItems - 1];
@@ -897,32 +922,54 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const int* __restrict__ i
   const int up = __shfl_up_sync(0xffffffffu, t, 1);
   int excl = lane > 0 ? up : ident;                         // exclusive within the warp
   if (wid > 0) excl = scan_op<OP>(s_warp[wid - 1], excl);   // ... within the tile
-  if (threadIdx.x == 0) {
+  if (wid == 0) {
+    // decoupled look-back by the whole first warp: lane l reads predecessor
+    // tile - 1 - l of the current 32-tile window; the values from the nearest
+    // inclusive prefix (flag Pre) onwards are combined by a warp reduction,
+    // the window slides back until a prefix is found
     const int agg = s_warp[kScanThreads / 32 - 1];
     int prefix = ident;
     if (tile == 0) {
-      atomicExch(status, kFlagPre | (unsigned)agg);
+      if (lane == 0) atomicExch(status, kFlagPre | (unsigned)agg);
     } else {
-      atomicExch(status + tile, kFlagAgg | (unsigned)agg);
-      for (int j = tile - 1;; --j) {
-        unsigned long long st;
-        do {
-          st = *reinterpret_cast<volatile unsigned long long*>(status + j);
-        } while ((st >> 32) == 0ull);
-        prefix = scan_op<OP>((int)(unsigned)(st & 0xffffffffull), prefix);
-        if ((st & ~0xffffffffull) == kFlagPre) break;
+      if (lane == 0) atomicExch(status + tile, kFlagAgg | (unsigned)agg);
+      for (int top = tile - 1;; top -= 32) {
+        const int j = top - lane;
+        unsigned long long st = kFlagPre | (unsigned)ident;   // beyond tile 0: a neutral prefix
+        if (j >= 0) {
+          do {
+            st = *reinterpret_cast<volatile unsigned long long*>(status + j);
+          } while ((st >> 32) == 0ull);
+        }
+        const unsigned pre_mask = __ballot_sync(0xffffffffu, (st & ~0xffffffffull) == kFlagPre);
+        const int stop = pre_mask ? __ffs(pre_mask) - 1 : 32;   // nearest lane holding a prefix
+        int val = lane <= stop ? (int)(unsigned)(st & 0xffffffffull) : ident;
+        // combine lanes 0..stop (order-free for + and max)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val = scan_op<OP>(val, __shfl_xor_sync(0xffffffffu, val, o));
+        prefix = scan_op<OP>(val, prefix);
+        if (pre_mask) break;
       }
-      atomicExch(status + tile, kFlagPre | (unsigned)scan_op<OP>(prefix, agg));
+      if (lane == 0) atomicExch(status + tile, kFlagPre | (unsigned)scan_op<OP>(prefix, agg));
     }
-    s_prefix = prefix;
+    if (lane == 0) s_prefix = prefix;
   }
   __syncthreads();
   const int pre = scan_op<OP>(s_prefix, excl);
+  int o8[kScanItems];
 #pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    if (base + j >= n) break;
-    if (OP == 0) out[base + j] = pre + (j > 0 ? v[j - 1] : 0);   // exclusive sum
-    else out[base + j] = scan_op<OP>(pre, v[j]);                 // inclusive max
+  for (int j = 0; j < kScanItems; ++j)
+    o8[j] = OP == 0 ? pre + (j > 0 ? v[j - 1] : 0)     // exclusive sum
+                    : scan_op<OP>(pre, v[j]);          // inclusive max
+  if (vec && base + kScanItems <= n) {
+    reinterpret_cast<int4*>(out + base)[0] = make_int4(o8[0], o8[1], o8[2], o8[3]);
+    reinterpret_cast<int4*>(out + base)[1] = make_int4(o8[4], o8[5], o8[6], o8[7]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      if (base + j >= n) break;
+      out[base + j] = o8[j];
+    }
   }
 }
 

@@ -117,6 +117,7 @@ struct ls_ctx {
   int* small_i = nullptr;                     // [0] bad flag, [1] temporal count, [2] first_valid
   SampleState* sstate = nullptr;          // device-side sampler rejection bookkeeping
   bool sampled_counts_known = true;
+  bool pair_off_ready = false;             // pair_off scanned from out_cnt (lazily, on demand)
   void* cub_tmp = nullptr;      // scan scratch (launch_scan)
   size_t cub_bytes = 0;
   int32_t *seg_raw = nullptr, *seg_key = nullptr, *seg_last = nullptr;
@@ -659,10 +660,11 @@ int ls_sample_consistency(ls_ctx* c, const double* chroma, const double* prev_ch
   LS_CK(launch_scan(c->stream, c->deg, c->row_ptr, (int64_t)N + 1, 0, c->cub_tmp));
   LS_CK(cudaMemsetAsync(c->fill, 0, sizeof(int32_t) * N, c->stream));
   launch_fill_from_samples(c->stream, c->codes, c->H, c->W, c->row_ptr, c->out_cnt, c->fill, c->ent);
-  // pair offsets (src-major, slot order) for ls_get_pairs / ls_pair_count
-  LS_CK(launch_scan(c->stream, c->out_cnt, c->pair_off, (int64_t)N + 1, 0, c->cub_tmp));
+  // (pair offsets for ls_get_pairs / ls_pair_count: scanned when asked for,
+  // ensure_pair_off -- the streaming solve never reads them)
+  c->pair_off_ready = false;
   LS_CK(cudaGetLastError());
-  c->launches += 1 + 3 * kSamplePasses + 6;
+  c->launches += 1 + 3 * kSamplePasses + 5;
   c->n_pairs = -1;                       // resolved lazily by ls_pair_count
   c->n_entries = -1;
   c->n_temporal = P.has_prev ? -1 : 0;
@@ -674,10 +676,22 @@ int ls_sample_consistency(ls_ctx* c, const double* chroma, const double* prev_ch
   return LS_OK;
 }
 
+// pair offsets (src-major, slot order) of the sampled pairs
+static int ensure_pair_off(ls_ctx* c) {
+  if (c->pair_off_ready) return LS_OK;
+  LS_CK(launch_scan(c->stream, c->out_cnt, c->pair_off, (int64_t)c->N + 1, 0, c->cub_tmp));
+  LS_CK(cudaGetLastError());
+  c->launches += 1;
+  c->pair_off_ready = true;
+  return LS_OK;
+}
+
 // pair / entry / temporal counts of the sampled adjacency (synchronises)
 int ls_pair_count(ls_ctx* c, int64_t* n_pairs, int64_t* n_temporal, int64_t* n_entries) {
   LS_ARG(c && c->has_pairs, "no consistency partners");
   if (!c->sampled_counts_known) {
+    const int rc = ensure_pair_off(c);
+    if (rc) return rc;
     int32_t v[2] = {0, 0};
     int err = 0;
     LS_CK(cudaMemcpyAsync(&v[0], c->pair_off + c->N, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
@@ -701,6 +715,8 @@ int ls_pair_count(ls_ctx* c, int64_t* n_pairs, int64_t* n_temporal, int64_t* n_e
 
 int ls_get_pairs(ls_ctx* c, int64_t* src, int64_t* dst, uint8_t* temporal) {
   LS_ARG(c && c->has_pairs && c->pairs_from_sampler, "no sampled pairs");
+  const int rc = ensure_pair_off(c);
+  if (rc) return rc;
   launch_pairs_from_samples(c->stream, c->codes, c->H, c->W, c->pair_off, src, dst, temporal);
   LS_CK(cudaGetLastError());
   return LS_OK;
