@@ -137,9 +137,6 @@ __global__ void k_image(const float* __restrict__ hwc, int N, float* __restrict_
   }
 }
 
-__device__ __forceinline__ double norm2d(double a, double b) {
-  return __dsqrt_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)));
-}
 
 // ---- chroma-edge gate (energy.py:121-136) ----------------------------------
 __global__ void k_edge(const double* __restrict__ ch, int H, int W, float* __restrict__ edge) {
@@ -627,20 +624,49 @@ __global__ void k_pairs_from_samples(const int16_t* __restrict__ codes, int H, i
 __global__ void k_segment_raw(const float* __restrict__ img, const double* __restrict__ ch, int N, int K,
                               const PalChroma pal, int32_t* ids_raw, int32_t* key, int* first_valid, int own_lo,
                               int own_hi) {
+  int fv = INT_MAX;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     const double c0 = ch[i], c1 = ch[N + i];
+    // argmin over the rounded norms sqrt_rn(s_k), first minimum wins
+    // (palette.py:203-207), with one square root: the winner is the first k
+    // whose root equals the root of the smallest square s_min -- a root can
+    // only tie with it when s_k is within rounding of s_min, so only such k
+    // (besides s_k == s_min) are checked explicitly
+    auto sq = [&](int k) {
+      const double a = __dsub_rn(c0, pal.c[2 * k]), b = __dsub_rn(c1, pal.c[2 * k + 1]);
+      return __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b));
+    };
+    double smin = sq(0);
+    for (int k = 1; k < K; ++k) smin = fmin(smin, sq(k));
+    const double rmin = __dsqrt_rn(smin);
+    const double near = smin * (1.0 + 1e-12);
     int best = 0;
-    double bd = 0.0;
     for (int k = 0; k < K; ++k) {
-      const double d = norm2d(__dsub_rn(c0, pal.c[2 * k]), __dsub_rn(c1, pal.c[2 * k + 1]));
-      if (k == 0 || d < bd) { bd = d; best = k; }    // argmin: first minimum wins
+      const double sk = sq(k);
+      if (sk == smin || (sk <= near && __dsqrt_rn(sk) == rmin)) {
+        best = k;
+        break;
+      }
     }
     ids_raw[i] = best + 1;
     const double s = __dadd_rn(__dadd_rn((double)img[i], (double)img[N + i]), (double)img[2 * N + i]);
     const bool dark = s < 0.02;
     const bool own = i >= own_lo && i < own_hi;
     key[i] = (dark || i < own_lo) ? -1 : i;
-    if (!dark && own) atomicMin(first_valid, i);
+    if (!dark && own) fv = min(fv, i);
+  }
+  // first non-dark own pixel: a block minimum, one atomic per block
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fv = min(fv, __shfl_xor_sync(0xffffffffu, fv, o));
+  __shared__ int s_fv[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) s_fv[wid] = fv;
+  __syncthreads();
+  if (wid == 0) {
+    fv = lane < (int)(blockDim.x >> 5) ? s_fv[lane] : INT_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) fv = min(fv, __shfl_xor_sync(0xffffffffu, fv, o));
+    if (lane == 0 && fv != INT_MAX) atomicMin(first_valid, fv);
   }
 }
 

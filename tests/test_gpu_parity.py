@@ -172,6 +172,23 @@ def test_segment_bit_exact():
     assert np.array_equal(cm.ids.cpu().numpy(), d["ids"])
 
 
+def test_segment_ties_bit_exact():
+    """Argmin ties (palette.py:203-207, first minimum wins): duplicated palette
+    colors, colors mirrored about pixel chromas, and pixels quantised onto a
+    coarse grid so that many squared distances coincide -- the device's
+    one-root argmin against the oracle's per-color norms."""
+    from paper_1908_01961_b200.palette import segment, BaseColorPalette
+    from paper_1908_01961_b200.imaging import Frame
+    rng = np.random.default_rng(11)
+    img = np.round(rng.uniform(0.05, 1.0, size=(96, 128, 3)) * 8) / 8      # few distinct chromas
+    img[:4, :4] = 0.001                                                    # dark pixels
+    colors = np.array([[0.5, 0.25, 0.25], [0.25, 0.5, 0.25], [0.25, 0.5, 0.25],   # a duplicate
+                       [0.25, 0.25, 0.5], [0.375, 0.375, 0.25], [0.25, 0.375, 0.375]])
+    cm = segment(Frame(torch.as_tensor(img, dtype=torch.float32, device="cuda")), BaseColorPalette(colors=colors))
+    ref = O.segment(img.astype(np.float32).astype(np.float64), colors)
+    assert np.array_equal(cm.ids.cpu().numpy(), ref)
+
+
 def test_dense_system_svd_and_step():
     from paper_1908_01961_b200.energy import refine_normal_system, EnergyWeights
     from paper_1908_01961_b200.solver import svd_solve, solve_dense_block, SolverState, SolveConfig
