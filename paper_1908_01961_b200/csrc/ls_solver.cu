@@ -607,7 +607,7 @@ __device__ void fin_pcg_update(double rz, double rn, Scalars* sc, int iter) {
   if (rz <= 0.0) sc->stop = 1;          // solver.py:101-103
 }
 
-template <int NT, int MODE, bool TMA>
+template <int NT, int MODE, bool TMA, bool COND = false>
 #ifndef LS_EG_MINB
 #define LS_EG_MINB kStencilMinBlocks
 #endif
@@ -730,7 +730,9 @@ __global__ void __launch_bounds__(kThreads, LS_EG_MINB) k_energy(Frame f, Coef<f
       fin_energy_trial(tot, sc, alpha, dev_ls, last_trial);
       // CUDA-graph flip-flop: the next halving's trial is the body of a
       // conditional node; it runs only while the line search is undecided
-      if (next_cond) cudaGraphSetConditional(next_cond, sc->ls_done ? 0u : 1u);
+      // (a separate instantiation: a kernel calling the device graph API is
+      // not listed by ncu inside graphs, and the default path never needs it)
+      if (COND && next_cond) cudaGraphSetConditional(next_cond, sc->ls_done ? 0u : 1u);
     }
     *ticket = 0u;
   }
@@ -1661,6 +1663,8 @@ static void prepare_nt() {
                        (int)energy_smem<NT>(MODE_EG, false));
   cudaFuncSetAttribute(k_energy<NT, MODE_TRIAL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)energy_smem<NT>(MODE_TRIAL, true));
+  cudaFuncSetAttribute(k_energy<NT, MODE_TRIAL, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)energy_smem<NT>(MODE_TRIAL, true));
   cudaFuncSetAttribute(k_energy<NT, MODE_TRIAL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)energy_smem<NT>(MODE_TRIAL, false));
   cudaFuncSetAttribute(k_apply<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem<NT>(true));
@@ -1675,10 +1679,18 @@ static void launch_energy_mt(const Launch& L, const Frame& f, const Coef<float>&
                              float* b_raw, float* diag_raw, double* part, unsigned* ticket, Scalars* sc,
                              const EnergyMaps* maps, const FrameCtl* ctl, int dev_ls, int last_trial,
                              unsigned long long next_cond) {
+  if constexpr (MODE == MODE_TRIAL) {
+    if (maps && next_cond) {
+      launch_pdl(k_energy<NT, MODE, true, true>, L.grid, kThreads, energy_smem<NT>(MODE, true), L.stream,
+                 f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, ctl,
+                 dev_ls, last_trial, *maps, next_cond);
+      return;
+    }
+  }
   if (maps)
     launch_pdl(k_energy<NT, MODE, true>, L.grid, kThreads, energy_smem<NT>(MODE, true), L.stream,
                f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, ctl,
-               dev_ls, last_trial, *maps, next_cond);
+               dev_ls, last_trial, *maps, 0ULL);
   else
     k_energy<NT, MODE, false><<<L.grid, kThreads, energy_smem<NT>(MODE, false), L.stream>>>(
         f, c, X, dx, alpha, Y, Xout, r_out, d_out, u_out, b_raw, diag_raw, part, ticket, sc, L.ntiles, ctl, dev_ls,
