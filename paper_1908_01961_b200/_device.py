@@ -125,8 +125,13 @@ class DeviceSolver:
         step installs its frame twice (segmentation, then the solve).  The
         key holds a reference to the tensor (so its memory cannot be reused
         under the same address) and torch's in-place version counter."""
-        key = (image_hwc.data_ptr(), tuple(image_hwc.shape), image_hwc._version)
-        if self._image_key is not None and self._image_key[0] == key and self._image_key[1] is image_hwc:
+        try:
+            version = image_hwc._version
+        except RuntimeError:        # inference tensors keep no version counter: never skip
+            version = None
+        key = (image_hwc.data_ptr(), tuple(image_hwc.shape), version)
+        if (version is not None and self._image_key is not None and self._image_key[0] == key
+                and self._image_key[1] is image_hwc):
             return
         self._enter()
         self._chk(self.lib.ls_set_image(self.ctx, L.dptr(image_hwc)))

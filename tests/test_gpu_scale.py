@@ -313,6 +313,28 @@ def test_graph_conditional_halvings_equal_eager(monkeypatch):
     assert halved > 0, "no halving exercised"
 
 
+def test_context_image_reinstalled_after_in_place_edit_and_in_inference_mode():
+    """A context skips ls_set_image for the tensor it already holds,
+    unmodified: an in-place edit (torch's version counter moves) must be seen,
+    and inference tensors (no version counter) are never skipped."""
+    from paper_1908_01961_b200.imaging import Frame
+    from paper_1908_01961_b200.palette import BaseColorPalette, segment
+    clip = _clip(48, 64, 3, n=2, seed=17)
+    pal = BaseColorPalette(colors=clip.colors)
+    f = Frame(clip.frames[0].cuda())
+    segment(f, pal)
+    f.data.copy_(clip.frames[1].cuda())               # same tensor, new contents
+    ids_edit = segment(f, pal).ids
+    ids_fresh = segment(Frame(clip.frames[1].cuda()), pal).ids
+    assert torch.equal(ids_edit, ids_fresh)
+    with torch.inference_mode():
+        g = Frame(clip.frames[0].cuda())
+        a = segment(g, pal).ids.clone()
+        g.data.copy_(clip.frames[1].cuda())
+        b = segment(g, pal).ids
+    assert torch.equal(b, ids_fresh) and not torch.equal(a, b)
+
+
 def test_graph_recaptures_when_the_palette_changes():
     """The captured flip-flop bakes the palette into its kernels: a new
     palette must re-capture (results equal the eager path for A, B, A)."""
