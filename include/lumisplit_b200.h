@@ -323,6 +323,12 @@ LS_API int ls_band_clear(ls_ctx* ctx);
 /* out[6] = {partials (512 doubles), z, p_even, p_odd, x, r}: the PCG vectors
  * (U planes of H*W floats each) whose halo rows the caller refreshes. */
 LS_API int ls_band_buffers(ls_ctx* ctx, void** out);
+/* Keep the band's PCG search directions: allocates n (<= 64) buffers of U x H_local
+ * x W floats (once; not during a graph capture) and returns them in out[0..n-1].
+ * From then on ls_band_pcg_apply(iter) writes p_iter to out[iter] (the caller
+ * exchanges its halo rows there) and leaves x alone, and ls_band_pcg_finish forms
+ * x = sum alpha_i p_i in one pass -- the whole-frame loop's layout. */
+LS_API int ls_band_dirs(ls_ctx* ctx, int n, void** out);
 /* Raw PCG64 u32 zeros (the Lemire rejections of energy.py:162-171) at stream
  * positions [begin, end): list (device, 17 int64) = {count, positions...}.
  * The bands split [0, 12*GH*W + 64) and gather their lists; the gathered

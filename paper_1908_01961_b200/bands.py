@@ -263,10 +263,32 @@ class _Band:
         self.x = _view(ptrs[4], (U, Hl, W), torch.float32, device)
         self.zlist = torch.zeros(L.ZERO_LIST, dtype=torch.int64, device=device)
         self.ring = None        # state buffers of the device-resident flip-flop
+        self.dirs = None        # the kept PCG search directions (ls_band_dirs), U x Hl x W each
+        self._shape = (U, Hl, W)
         self.summary = torch.zeros(3, dtype=torch.int32, device=device)
 
     def chk(self, rc):
         self.solver._chk(rc)
+
+    def ensure_dirs(self, n: int):
+        """Keep this band's PCG search directions (the whole-frame loop's
+        layout: no x-update in the operator, x = sum alpha_i p_i once per GN
+        step).  Left off (p ping-pong, deferred x) where the context keeps
+        none (LS_X_DEFERRED=1, LS_PCG=cg1) or n is out of range."""
+        if self.dirs is not None and len(self.dirs) >= n:
+            return
+        if not 1 <= n <= 64:
+            return
+        ptrs = (C.c_void_p * n)()
+        if self.lib.ls_band_dirs(self.ctx, int(n), ptrs) != L.LS_OK:
+            self.dirs = None
+            return
+        dev = self.solver.device
+        self.dirs = [_view(ptrs[i], self._shape, torch.float32, dev) for i in range(n)]
+
+    def pdir(self, it: int):
+        """The buffer p_it lands in (its halo rows are exchanged)."""
+        return self.dirs[it] if self.dirs is not None and it < len(self.dirs) else self.p[it & 1]
 
 
 def _rec(**kw):
@@ -420,7 +442,7 @@ class BandedSolver:
             for b, Xb in zip(bands, Xs):
                 b.chk(b.lib.ls_band_pcg_apply(b.ctx, pa, L.dptr(Xb), it))
             self._gather_finalize(L.BAND_APPLY, 1, it)
-            ex.halo([b.p[it & 1] for b in bands])
+            ex.halo([b.pdir(it) for b in bands])
             for b in bands:
                 b.chk(b.lib.ls_band_pcg_update(b.ctx, it))
             self._gather_finalize(L.BAND_UPDATE, 2, it)
@@ -463,9 +485,14 @@ class BandedSolver:
             ex.halo(Xouts)
         return L.LS_OK, rec
 
+    def _ensure_dirs(self):
+        for b in self.bands:
+            b.ensure_dirs(int(self.cfg.pcg_iterations))
+
     def gn_step(self, colors, X, X_out):
         a, pa = L.dbl_array(colors)
         self._enter()
+        self._ensure_dirs()
         Xs = self._local(X)
         Xouts = [torch.empty_like(x) for x in Xs]
         rc, rec = self._gn_step_local(pa, Xs, Xouts, self.cfg.pcg_iterations, self.cfg.max_halvings)
@@ -539,6 +566,7 @@ class BandedSolver:
         trial); the device-resident flip_flop_stream must match it."""
         a, pa = L.dbl_array(colors)
         self._enter()
+        self._ensure_dirs()
         Xs = self._local(X0)
         recs, e_prev, stalled = [], None, False
         status = 0
@@ -613,7 +641,7 @@ class BandedSolver:
                     for b, Xb in zip(bands, Xs):
                         b.chk(b.lib.ls_band_pcg_apply(b.ctx, pa, L.dptr(Xb), it))
                     self._gfd(L.BAND_APPLY, 1, it)
-                    ex.halo([b.p[it & 1] for b in bands])
+                    ex.halo([b.pdir(it) for b in bands])
                     for b in bands:
                         b.chk(b.lib.ls_band_pcg_update(b.ctx, it))
                     self._gfd(L.BAND_UPDATE, 2, it)
@@ -644,6 +672,8 @@ class BandedSolver:
         a, pa = L.dbl_array(colors)
         if outer * gn_steps > 256:
             raise ValueError("too many GN steps")
+        self._enter()
+        self._ensure_dirs()          # (allocations: before any capture)
         for b in self.bands:
             if b.ring is None:
                 b.ring = [torch.empty((self.U, b.spec.height, self.W), dtype=torch.float32, device=self.device)

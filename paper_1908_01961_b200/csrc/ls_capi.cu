@@ -159,6 +159,7 @@ struct ls_ctx {
   cudaStream_t cap_stream = nullptr;
   cudaStream_t cond_stream = nullptr;      // captures the bodies of graph conditional nodes
   bool use_cond = false;                   // LS_GRAPH_COND=1: halvings as graph conditional nodes
+  bool band_stored = false;                // row band: PCG directions kept (ls_band_dirs)
   cudaGraphExec_t graph_exec = nullptr;
   unsigned char graph_key[1024] = {0};
   long long graph_launches = 0;
@@ -1057,7 +1058,7 @@ static int run_pcg_cg1(ls_ctx* c, const double* colors, const float* X, int iter
 // Buffers: r, d = 1/diag, u = z = r/diag, wv = q = A p, p / s = ping-pong p.
 // the stored-direction buffers for a loop of `iters` iterations (outside captures)
 static int ensure_pdirs(ls_ctx* c, int iters) {
-  if (c->x_deferred || c->band_partial || c->pcg_cg1 || iters < 1 || iters > kMaxStoredDirs) return LS_OK;
+  if (c->x_deferred || c->pcg_cg1 || iters < 1 || iters > kMaxStoredDirs) return LS_OK;
   const size_t M = (size_t)c->U * c->N;
   while ((int)c->pdirs.size() < iters) {
     float* b = nullptr;
@@ -1724,6 +1725,21 @@ int ls_band_buffers(ls_ctx* c, void** out) {
   return LS_OK;
 }
 
+int ls_band_dirs(ls_ctx* c, int n, void** out) {
+  LS_ARG(c && c->band_partial && out && n >= 1 && n <= kMaxStoredDirs, "bad arguments");
+  LS_ARG(!c->x_deferred && !c->pcg_cg1, "stored PCG directions are off in this context");
+  LS_CK(cudaSetDevice(c->dev));
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  LS_CK(cudaStreamIsCapturing(c->stream, &cs));
+  LS_ARG(cs == cudaStreamCaptureStatusNone || (int)c->pdirs.size() >= n,
+         "PCG direction buffers must exist before a graph capture");
+  const int rc = ensure_pdirs(c, n);
+  if (rc) return rc;
+  for (int i = 0; i < n; ++i) out[i] = c->pdirs[i];
+  c->band_stored = true;
+  return LS_OK;
+}
+
 int ls_band_zero_scan(ls_ctx* c, uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t begin,
                       uint64_t end, int64_t* list) {
   LS_ARG(c && list && end >= begin, "bad arguments");
@@ -1771,12 +1787,17 @@ int ls_band_pcg_apply(ls_ctx* c, const double* colors, const float* X, int iter)
   const Frame f = frame_of(c);
   const Coef<float> cd = make_coef<float>(c->w, colors, c->K);
   float* pbuf[2] = {c->p, c->s};
+  // stored directions (ls_band_dirs): p_iter into its own buffer, no
+  // deferred x-update in the operator -- x = sum alpha_i p_i in ls_band_pcg_finish
+  const bool stored = c->band_stored && iter < (int)c->pdirs.size();
+  float* pprev = stored ? c->pdirs[iter > 0 ? iter - 1 : 0] : pbuf[(iter + 1) & 1];
+  float* pnew = stored ? c->pdirs[iter] : pbuf[iter & 1];
   PcgMaps maps;
-  const bool tma = pcg_maps(c, X, pbuf[(iter + 1) & 1], &maps);
+  const bool tma = pcg_maps(c, X, pprev, &maps);
   const Launch La{c->grid_pcg, c->ntiles, c->stream};
   const size_t pi = prof_begin(c);
-  launch_pcg_apply(La, f, cd, X, c->u, pbuf[(iter + 1) & 1], pbuf[iter & 1], c->wv, c->part, c->tickets + 1, c->sc,
-                   iter, tma ? &maps : nullptr, c->x);
+  launch_pcg_apply(La, f, cd, X, c->u, pprev, pnew, c->wv, c->part, c->tickets + 1, c->sc, iter,
+                   tma ? &maps : nullptr, stored ? nullptr : c->x);
   prof_end(c, PC_APPLY, pi);
   c->launches += 1;
   LS_CK(cudaGetLastError());
@@ -1791,8 +1812,9 @@ int ls_band_pcg_update(ls_ctx* c, int iter) {
   float* pbuf[2] = {c->p, c->s};
   const int64_t M = (int64_t)c->U * c->N;
   const size_t pi = prof_begin(c);
-  launch_pcg_update(L_update(c), M, c->r, c->wv, c->d, c->u, pbuf[iter & 1], c->x, c->part, c->tickets + 2, c->sc,
-                    iter, &f);
+  const bool stored = c->band_stored && iter < (int)c->pdirs.size();
+  launch_pcg_update(L_update(c), M, c->r, c->wv, c->d, c->u, stored ? c->pdirs[iter] : pbuf[iter & 1],
+                    stored ? nullptr : c->x, c->part, c->tickets + 2, c->sc, iter, &f);
   prof_end(c, PC_UPDATE, pi);
   c->launches += 1;
   LS_CK(cudaGetLastError());
@@ -1803,7 +1825,15 @@ int ls_band_pcg_finish(ls_ctx* c) {
   int rc = band_ready(c);
   if (rc) return rc;
   const Frame f = frame_of(c);
-  launch_pcg_xfinal(L_update(c), (int64_t)c->U * c->N, c->x, c->p, c->s, c->sc, c->tickets + 4, &f);
+  if (c->band_stored && !c->pdirs.empty()) {   // x = sum alpha_i p_i over the whole local rows
+    DirList dl;
+    std::memset(&dl, 0, sizeof(dl));
+    dl.n = std::min<int>((int)c->pdirs.size(), kMaxStoredDirs);
+    for (int i = 0; i < dl.n; ++i) dl.p[i] = c->pdirs[i];
+    launch_pcg_combine(L_update(c), (int64_t)c->U * c->N, dl, c->x, c->sc);
+  } else {
+    launch_pcg_xfinal(L_update(c), (int64_t)c->U * c->N, c->x, c->p, c->s, c->sc, c->tickets + 4, &f);
+  }
   c->launches += 1;
   LS_CK(cudaGetLastError());
   return LS_OK;
