@@ -329,6 +329,16 @@ LS_API int ls_band_buffers(ls_ctx* ctx, void** out);
  * exchanges its halo rows there) and leaves x alone, and ls_band_pcg_finish forms
  * x = sum alpha_i p_i in one pass -- the whole-frame loop's layout. */
 LS_API int ls_band_dirs(ls_ctx* ctx, int n, void** out);
+/* In-process row bands (one device, one stream): ls_band_finalize_dev of all
+ * n bands at once, reading every band's partial sums directly (no gather
+ * copies); the same band-ordered sums and decisions.  Launched on ctxs[0]'s
+ * stream. */
+LS_API int ls_band_finalize_group(ls_ctx* const* ctxs, int n, int phase, int iter, double alpha, int last);
+/* n <= 32 strided slab copies in one launch: slab i copies planes[i] x count[i]
+ * floats from src[i] + p * src_stride[i] to dst[i] + p * dst_stride[i]
+ * (host arrays of device pointers; the halo moves between in-process bands). */
+LS_API int ls_copy_slabs(int n, const float* const* src, float* const* dst, const int64_t* src_stride,
+                         const int64_t* dst_stride, const int64_t* count, const int* planes, void* stream);
 /* Raw PCG64 u32 zeros (the Lemire rejections of energy.py:162-171) at stream
  * positions [begin, end): list (device, 17 int64) = {count, positions...}.
  * The bands split [0, 12*GH*W + 64) and gather their lists; the gathered

@@ -119,6 +119,9 @@ SIGNATURES = {
     "ls_band_clear": [P],
     "ls_band_buffers": [P, C.POINTER(C.c_void_p)],
     "ls_band_dirs": [P, C.c_int, C.POINTER(P)],
+    "ls_band_finalize_group": [C.POINTER(P), C.c_int, C.c_int, C.c_int, C.c_double, C.c_int],
+    "ls_copy_slabs": [C.c_int, C.POINTER(P), C.POINTER(P), C.POINTER(I64), C.POINTER(I64), C.POINTER(I64),
+                      C.POINTER(C.c_int), P],
     "ls_band_zero_scan": [P, U64, U64, U64, U64, U64, U64, P],
     "ls_band_set_zeros": [P, P, C.c_int],
     "ls_band_eg": [P, DBL_P, P],

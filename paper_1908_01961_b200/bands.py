@@ -161,16 +161,37 @@ class LocalExchange:
         than its bytes, so each move is ONE copy of the R_HALO rows next to
         the boundary in every plane (covering halo_pieces); full=True copies
         the whole HALO rows."""
+        moves = []
         for mv in halo_moves(self.bands):
             src, dst = self.bands[mv[0]], self.bands[mv[1]]
-            if full:
-                pieces = [(0, None, mv[2], mv[3])]
-            else:
-                rows = halo_pieces(mv)[0]
-                pieces = [(0, None, rows[2], rows[3])]
-            for p0, p1, g0, g1 in pieces:
-                piece = tensors[mv[0]][p0:p1, g0 - src.ya:g1 - src.ya]
-                tensors[mv[1]][p0:p1, g0 - dst.ya:g1 - dst.ya].copy_(piece, non_blocking=True)
+            g0, g1 = (mv[2], mv[3]) if full else halo_pieces(mv)[0][2:4]
+            moves.append((mv[0], mv[1], g0 - src.ya, g0 - dst.ya, g1 - g0))
+        t0 = tensors[0]
+        fused = (len(moves) <= 32 and t0.is_cuda and
+                 all(t.dtype == torch.float32 and t.is_contiguous() and t.dim() == 3 and t.device == t0.device
+                     for t in tensors))
+        if not fused:
+            for s_i, d_i, ys, yd, n in moves:
+                tensors[d_i][:, yd:yd + n].copy_(tensors[s_i][:, ys:ys + n], non_blocking=True)
+            return
+        # one launch for every move (ls_copy_slabs): on one device each copy
+        # costs a launch more than its bytes
+        k = len(moves)
+        srcs, dsts = (C.c_void_p * k)(), (C.c_void_p * k)()
+        sst, dst_, cnt = (C.c_int64 * k)(), (C.c_int64 * k)(), (C.c_int64 * k)()
+        pls = (C.c_int * k)()
+        for i, (s_i, d_i, ys, yd, n) in enumerate(moves):
+            ts, td = tensors[s_i], tensors[d_i]
+            W = ts.shape[2]
+            srcs[i] = ts.data_ptr() + 4 * ys * W
+            dsts[i] = td.data_ptr() + 4 * yd * W
+            sst[i], dst_[i] = ts.shape[1] * W, td.shape[1] * W
+            cnt[i], pls[i] = n * W, ts.shape[0]
+        lib = L.load()
+        st = torch.cuda.current_stream(t0.device).cuda_stream
+        rc = lib.ls_copy_slabs(k, srcs, dsts, sst, dst_, cnt, pls, C.c_void_p(st))
+        if rc != L.LS_OK:
+            raise L.NativeError(L.last_error())
 
 
 class DistExchange:
@@ -614,7 +635,15 @@ class BandedSolver:
         return int(n.value)
 
     def _gfd(self, phase: int, nv: int, it: int = 0, alpha: float = 0.0, last: int = 0):
-        """gather + device-side finalisation (ls_band_finalize_dev)."""
+        """gather + device-side finalisation (ls_band_finalize_dev); every band
+        in this process on one device: one ls_band_finalize_group launch
+        reading all bands' partials in place."""
+        if isinstance(self.exchange, LocalExchange) and len({b.solver.device for b in self.bands}) == 1:
+            if getattr(self, "_group", None) is None or len(self._group) != len(self.bands):
+                self._group = (C.c_void_p * len(self.bands))(*[b.ctx.value for b in self.bands])
+            b0 = self.bands[0]
+            b0.chk(b0.lib.ls_band_finalize_group(self._group, len(self.bands), phase, it, float(alpha), last))
+            return
         gs = self.exchange.gather([b.bsum[:nv].clone() for b in self.bands])
         for b, g in zip(self.bands, gs):
             b.chk(b.lib.ls_band_finalize_dev(b.ctx, phase, L.dptr(g), len(self.specs), it, float(alpha), last))

@@ -1909,6 +1909,48 @@ int ls_band_finalize_dev(ls_ctx* c, int phase, const double* gathered, int nband
   return LS_OK;
 }
 
+// all bands of this process at once (in-process row bands: the gather is a
+// read of the other bands' partial sums, no copies)
+extern "C" int ls_band_finalize_group(ls_ctx* const* ctxs, int n, int phase, int iter, double alpha, int last) {
+  LS_ARG(ctxs && n >= 1 && n <= kMaxGroupBands, "bad arguments");
+  LS_ARG(phase >= BAND_EG && phase <= BAND_TRIAL, "bad band phase");
+  BandGroup g;
+  std::memset(&g, 0, sizeof(g));
+  g.n = n;
+  for (int i = 0; i < n; ++i) {
+    ls_ctx* c = ctxs[i];
+    LS_ARG(c && c->band_partial && c->band_dev && c->dev == ctxs[0]->dev, "bad band context");
+    g.bsum[i] = c->bsum;
+    g.sc[i] = c->sc;
+    g.ctl[i] = c->ctl;
+  }
+  const int nv = phase == BAND_EG ? kTerms + 2 : phase == BAND_APPLY ? 1 : phase == BAND_UPDATE ? 2 : kTerms;
+  launch_band_finalize_group(ctxs[0]->stream, phase, g, nv, iter, (float)alpha, last);
+  ctxs[0]->launches += 1;
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
+// strided slab copies in one launch (halo moves between in-process bands)
+extern "C" int ls_copy_slabs(int n, const float* const* src, float* const* dst, const int64_t* src_stride,
+                             const int64_t* dst_stride, const int64_t* count, const int* planes, void* stream) {
+  LS_ARG(n >= 0 && n <= kMaxSlabs, "too many slabs");
+  LS_ARG(n == 0 || (src && dst && src_stride && dst_stride && count && planes), "bad arguments");
+  SlabList L;
+  std::memset(&L, 0, sizeof(L));
+  L.n = n;
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) {
+    LS_ARG(src[i] && dst[i] && count[i] >= 0 && planes[i] >= 0, "bad slab");
+    L.s[i] = Slab{src[i], dst[i], src_stride[i], dst_stride[i], count[i], planes[i]};
+    total = std::max<int64_t>(total, count[i] * planes[i]);
+  }
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
+  launch_copy_slabs((cudaStream_t)stream, L, grid);
+  LS_CK(cudaGetLastError());
+  return LS_OK;
+}
+
 int ls_band_step_end(ls_ctx* c, const float* X_in, float* X_out, int out_id) {
   LS_ARG(c && c->band_dev && X_in && X_out, "bad arguments");
   launch_step_end(c->stream, c->grid_update, c->ctl, c->sc, X_in, X_out, (int64_t)c->U * c->N, out_id, c->recs);

@@ -82,6 +82,29 @@ enum BandPhase { BAND_EG = 0, BAND_APPLY = 1, BAND_UPDATE = 2, BAND_TRIAL = 3, B
 void launch_band_sum(cudaStream_t s, const double* gathered, int nbands, int nv, double* out);
 void launch_band_finalize(cudaStream_t s, int phase, const double* gathered, int nbands, int nv, Scalars* sc,
                           int iter, float alpha, int dev_ls, int last_trial, const FrameCtl* ctl = nullptr);
+// the bands of one process finalised together (k_band_finalize_group)
+constexpr int kMaxGroupBands = 16;
+struct BandGroup {
+  const double* bsum[kMaxGroupBands];
+  Scalars* sc[kMaxGroupBands];
+  const FrameCtl* ctl[kMaxGroupBands];
+  int n;
+};
+void launch_band_finalize_group(cudaStream_t s, int phase, const BandGroup& g, int nv, int iter, float alpha,
+                                int last_trial);
+// strided slab copies (halo moves) in one launch
+constexpr int kMaxSlabs = 32;
+struct Slab {
+  const float* src;
+  float* dst;
+  int64_t src_stride, dst_stride, count;
+  int planes;
+};
+struct SlabList {
+  Slab s[kMaxSlabs];
+  int n;
+};
+void launch_copy_slabs(cudaStream_t s, const SlabList& L, int grid);
 int pcg_apply_grid_limit(int NT);
 int energy_grid_limit(int NT);
 void prepare_kernels(int NT);

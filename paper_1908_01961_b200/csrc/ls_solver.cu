@@ -2006,6 +2006,54 @@ void launch_band_finalize(cudaStream_t s, int phase, const double* gathered, int
   k_band_finalize<<<1, 32, 0, s>>>(phase, gathered, nbands, nv, sc, iter, alpha, dev_ls, last_trial, ctl);
 }
 
+// every band of one process at once: block b sums all bands' partials in band
+// order (the same sums as k_band_finalize over the gathered copy) and
+// finalises band b's scalars -- one launch instead of copies + a gather + one
+// finalisation per band
+__global__ void k_band_finalize_group(int phase, BandGroup g, int nv, int iter, float alpha, int last_trial) {
+  if (threadIdx.x != 0 || blockIdx.x >= (unsigned)g.n) return;
+  const int b = blockIdx.x;
+  Scalars* sc = g.sc[b];
+  const FrameCtl* ctl = g.ctl[b];
+  if (ctl && ctl->done) return;
+  if (phase == BAND_TRIAL && sc->ls_done) return;
+  double tot[kTerms + 2];
+  for (int j = 0; j < nv && j < kTerms + 2; ++j) {
+    double s = 0.0;
+    for (int bb = 0; bb < g.n; ++bb) s += ((volatile const double*)g.bsum[bb])[j];
+    tot[j] = s;
+  }
+  switch (phase) {
+    case BAND_EG: fin_energy_eg(tot, sc, true); break;
+    case BAND_TRIAL: fin_energy_trial(tot, sc, alpha, 1, last_trial); break;
+    case BAND_APPLY: if (!sc->stop) fin_pcg_apply(tot[0], sc, iter); break;
+    case BAND_UPDATE: if (!sc->stop) fin_pcg_update(tot[0], tot[1], sc, iter); break;
+    default: break;
+  }
+}
+
+void launch_band_finalize_group(cudaStream_t s, int phase, const BandGroup& g, int nv, int iter, float alpha,
+                                int last_trial) {
+  k_band_finalize_group<<<g.n, 32, 0, s>>>(phase, g, nv, iter, alpha, last_trial);
+}
+
+// strided slab copies in one launch (the halo moves between the bands of one
+// process): slab i copies planes x count floats, plane strides given
+__global__ void k_copy_slabs(SlabList L) {
+  for (int i = 0; i < L.n; ++i) {
+    const Slab& sl = L.s[i];
+    const int64_t total = (int64_t)sl.planes * sl.count;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t pl = e / sl.count, k = e - pl * sl.count;
+      sl.dst[pl * sl.dst_stride + k] = sl.src[pl * sl.src_stride + k];
+    }
+  }
+}
+
+void launch_copy_slabs(cudaStream_t s, const SlabList& L, int grid) {
+  if (L.n > 0) k_copy_slabs<<<grid, 256, 0, s>>>(L);
+}
+
 int pcg_apply_grid_limit(int NT) {
   int nb = 0;
   LS_DISPATCH_NT(NT, (prepare_nt<NT_>(), cudaOccupancyMaxActiveBlocksPerMultiprocessor(
