@@ -172,6 +172,29 @@ def test_segment_bit_exact():
     assert np.array_equal(cm.ids.cpu().numpy(), d["ids"])
 
 
+def test_frame_rejects_non_finite_values():
+    """imaging.py:36-57: a frame with NaN / inf anywhere raises FrameError
+    (k_all_finite: float4 body, scalar tail, unaligned views)."""
+    from paper_1908_01961_b200.imaging import Frame, FrameError
+    rng = np.random.default_rng(2)
+    base = torch.as_tensor(rng.uniform(0, 1, size=(37, 41, 3)), dtype=torch.float32, device="cuda")
+    Frame(base)                                            # finite: accepted
+    n = base.numel()
+    for pos in (0, 1, 2, 3, n // 2, n - 5, n - 2, n - 1):  # body and the scalar tail (n % 4 = 3)
+        for bad in (float("nan"), float("inf"), -float("inf")):
+            x = base.clone()
+            x.view(-1)[pos] = bad
+            with pytest.raises(FrameError):
+                Frame(x)
+    big = torch.zeros(1, 38, 41, 3, dtype=torch.float32, device="cuda").view(-1)
+    view = big[1:1 + n].view(37, 41, 3)                    # 4-byte aligned, not 16: scalar path
+    view.copy_(base)
+    Frame(view)
+    view[36, 40, 2] = float("nan")
+    with pytest.raises(FrameError):
+        Frame(view)
+
+
 def test_segment_ties_bit_exact():
     """Argmin ties (palette.py:203-207, first minimum wins): duplicated palette
     colors, colors mirrored about pixel chromas, and pixels quantised onto a
