@@ -2,7 +2,7 @@
 compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 sampler + CSR, segment, first frame with refinement (EG, PCG, trials,
 dense), streaming frames through the CUDA-graph flip-flop, row bands,
-flood fill and the edit recomposition."""
+flood fill, the batched correction candidates and the edit recomposition."""
 import sys
 sys.path.insert(0, '.')
 import torch
@@ -20,6 +20,10 @@ for bands in (0, 2):
     for f in clip.frames[1:]:
         st = dec.step(f)
 reg = correction.identify_region((40, 30), st.cluster_map)
+# the K candidate solves as one batched launch sequence (ls_flip_flop_batch)
+from paper_1908_01961_b200.imaging import Frame
+pick = correction.correct_reflectance(reg, Frame(clip.frames[-1]), st.cluster_map, dec.palette,
+                                      config=SolveConfig(outer_iterations=1, refine=False))
 out = editing.recolor(st.layers, dec.palette, 1, [0.3, 0.5, 0.2], st.cluster_map)
 torch.cuda.synchronize()
-print("workload ok", float(out.mean()), reg.size)
+print("workload ok", float(out.mean()), reg.size, pick)
