@@ -122,6 +122,12 @@ LS_API int ls_sample_consistency(ls_ctx* ctx, const double* chroma_planes, const
 /* Device-to-device copy on the SMs (stream-ordered; unlike a D2D
  * cudaMemcpyAsync it never waits for a copy engine busy with host I/O). */
 LS_API int ls_device_copy(void* dst, const void* src, int64_t bytes, void* stream);
+/* The device int32 scan behind the adjacency rows and the segmentation
+ * (single pass, decoupled look-back): op 0 = exclusive sum, 1 = inclusive
+ * max, over n values; scratch = ls_scan_scratch_bytes(n) bytes of device
+ * memory, reset by the call.  Stream-ordered. */
+LS_API int64_t ls_scan_scratch_bytes(int64_t n);
+LS_API int ls_scan_i32(const int32_t* in, int32_t* out, int64_t n, int op, void* scratch, void* stream);
 /* Frame validity (imaging.py:36-57): *all_finite = no NaN / inf in x[0..n).
  * Synchronises `stream`; the flag comes back through mapped host memory. */
 LS_API int ls_all_finite(const float* x, int64_t n, void* stream, int* all_finite);

@@ -82,6 +82,7 @@ SIGNATURES = {
     "ls_get_edge": [P, P],
     "ls_get_chroma": [P, P],
     "ls_device_copy": [P, P, I64, P],
+    "ls_scan_i32": [P, P, I64, C.c_int, P, P],
     "ls_flood_fill": [P, C.c_int, P, C.c_int, C.c_int, P, P, P],
     "ls_recompose": [P, C.c_int, C.c_int, C.c_int, DBL_P, C.c_int, DBL_P, P, P, P, P, P],
     "ls_all_finite": [P, I64, P, C.POINTER(C.c_int)],
@@ -147,6 +148,8 @@ SIGNATURES = {
 BAND_EG, BAND_APPLY, BAND_UPDATE, BAND_TRIAL = 0, 1, 2, 3
 ZERO_LIST = 17          # 1 + kMaxRejections
 STRING_FUNCS = ("ls_version", "ls_last_error")
+# name -> argtypes of the functions returning int64_t
+INT64_FUNCS = {"ls_scan_scratch_bytes": [I64]}
 
 _lib = None
 _lock = threading.Lock()
@@ -176,12 +179,16 @@ def load(path: Path | str | None = None):
             fn = getattr(lib, name)
             fn.argtypes = []
             fn.restype = C.c_char_p
+        for name, argt in INT64_FUNCS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argt
+            fn.restype = I64
         _lib = lib
         return lib
 
 
 def symbols():
-    return list(SIGNATURES) + list(STRING_FUNCS)
+    return list(SIGNATURES) + list(STRING_FUNCS) + list(INT64_FUNCS)
 
 
 def last_error() -> str:

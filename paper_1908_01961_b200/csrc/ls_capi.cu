@@ -554,6 +554,18 @@ static int build_rows(ls_ctx* c, int64_t* total) {
   return LS_OK;
 }
 
+// the device scan the adjacency and segmentation use (decoupled look-back),
+// exposed for its own tests: op 0 exclusive sum, 1 inclusive max; scratch of
+// ls_scan_scratch_bytes(n) bytes (zeroed by the call)
+int64_t ls_scan_scratch_bytes(int64_t n) { return (int64_t)scan_scratch_bytes(n); }
+
+int ls_scan_i32(const int32_t* in, int32_t* out, int64_t n, int op, void* scratch, void* stream) {
+  LS_ARG(n >= 0 && (op == 0 || op == 1), "bad arguments");
+  LS_ARG(n == 0 || (in && out && scratch), "null arrays");
+  LS_CK(launch_scan((cudaStream_t)stream, in, out, n, op, scratch));
+  return LS_OK;
+}
+
 int ls_device_copy(void* dst, const void* src, int64_t bytes, void* stream) {
   LS_ARG((dst && src) || bytes == 0, "bad arguments");
   LS_ARG(bytes >= 0, "bad size");
