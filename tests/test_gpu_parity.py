@@ -88,6 +88,40 @@ def test_gradient_diag_apply(name):
     assert rel(to_reference_vector(Ap), d["Ap"]) < 2e-5
 
 
+@pytest.mark.parametrize("weighted", [False, True])
+def test_apply_with_a_hub_pixel_vs_oracle(weighted):
+    """Explicit partner rows where four hub pixels of one 32-pixel run each
+    pair with their whole 15x15 window: that run's adjacency span (~900
+    entries) overflows the warp sort's shared memory, so the in-place fallback
+    orders it -- the operator still matches the oracle's (unit and explicit
+    pair weights)."""
+    from paper_1908_01961_b200.energy import assemble_blocks, from_reference_vector, to_reference_vector
+    d = dict(load("ops_d"))
+    H, W = d["image"].shape[:2]
+    K = d["colors"].shape[0]
+    srcs, dsts = [], []
+    for hy, hx in ((16, 4), (16, 12), (16, 20), (16, 28)):     # flat 644 .. 668: one 32-row group
+        hub = hy * W + hx
+        for y in range(max(0, hy - 7), min(H, hy + 8)):
+            for x in range(max(0, hx - 7), min(W, hx + 8)):
+                if y * W + x != hub:
+                    srcs.append(y * W + x)
+                    dsts.append(hub)
+    rng = np.random.default_rng(4)
+    extra = len(srcs)
+    d["pair_src"] = np.concatenate([d["pair_src"], np.array(srcs, dtype=np.int64)])
+    d["pair_dst"] = np.concatenate([d["pair_dst"], np.array(dsts, dtype=np.int64)])
+    d["pair_temporal"] = np.concatenate([d["pair_temporal"], np.zeros(extra, dtype=bool)])
+    w = rng.uniform(0.5, 2.0, size=d["pair_src"].size) if weighted else np.ones(d["pair_src"].size)
+    d["pair_weight"] = w
+    frame, pal, layers, aux, wts = device_problem(d)
+    blocks = assemble_blocks(frame, pal, layers, aux, wts)
+    p = from_reference_vector(d["p"], H, W, K)
+    Ap = to_reference_vector(blocks.apply_normal(p))
+    osys = oracle_system(d)
+    assert rel(Ap, osys.apply(d["p"])) < 2e-5
+
+
 @pytest.mark.parametrize("name", OPS)
 def test_pcg16(name):
     from paper_1908_01961_b200.energy import assemble_blocks, to_reference_vector
