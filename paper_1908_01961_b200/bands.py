@@ -9,9 +9,12 @@ stencils 1).  Each GN step is the same sequence of kernels as the
 whole-frame path, issued per band:
 
     EG  -> gather partials -> finalise -> halo(z)
-    16 x [ apply  -> gather -> finalise -> halo(p)
+    16 x [ apply  -> gather -> finalise -> halo(p_i)
            update -> gather -> finalise -> halo(z) ]
-    halo(x); trials (gather, finalise, host accept / halve); halo(X_out)
+    x = sum alpha_i p_i; halo(x); trials (gather, finalise, accept / halve); halo(X_out)
+
+(every search direction p_i kept in its own buffer, ls_band_dirs, as in the
+whole-frame loop).
 
 Every reduction is a band partial (fp64, fixed order inside the band) and the
 finalisation sums the gathered partials in band order on every band, so all
@@ -21,7 +24,9 @@ whole-frame solve the only difference is the grouping of the fp64 sums.
 
 Exchanges are pluggable:
   * LocalExchange -- every band in this process (one GPU, or several GPUs
-    driven from one process): gathers are a stack, halos device copies.
+    driven from one process): on one device a phase's gather + finalisation
+    is one launch reading every band's partials in place
+    (ls_band_finalize_group) and a halo exchange one launch (ls_copy_slabs).
   * DistExchange  -- one band per rank of a torch.distributed group (NCCL
     over NVLink on B200s; gloo in the CPU tests): all_gather_into_tensor of
     the partials, batched P2P send / recv of the halo rows.
