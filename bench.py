@@ -434,10 +434,11 @@ def run_ours(args):
         # (energy.py:74-94), interleaved on the device by the unpack kernel, then D2H
         from paper_1908_01961_b200.energy import export_reference_layout
         Hl, Wl = int(st.layers.X.shape[1]), int(st.layers.X.shape[2])
-        dev_r = [torch.empty((Hl, Wl, 3), dtype=torch.float32, device=dev) for _ in range(2)]
-        dev_T = [torch.empty((Hl, Wl, K + 1), dtype=torch.float32, device=dev) for _ in range(2)]
+        NB = 3      # read-back buffers in flight (absorbs host-link jitter)
+        dev_r = [torch.empty((Hl, Wl, 3), dtype=torch.float32, device=dev) for _ in range(NB)]
+        dev_T = [torch.empty((Hl, Wl, K + 1), dtype=torch.float32, device=dev) for _ in range(NB)]
         out_host = [(torch.empty((Hl, Wl, 3), dtype=torch.float32).pin_memory(),
-                     torch.empty((Hl, Wl, K + 1), dtype=torch.float32).pin_memory()) for _ in range(2)]
+                     torch.empty((Hl, Wl, K + 1), dtype=torch.float32).pin_memory()) for _ in range(NB)]
         side = torch.cuda.Stream(device=dev)
         main = torch.cuda.current_stream()
         up = torch.cuda.Stream(device=dev)
@@ -458,7 +459,7 @@ def run_ours(args):
                 return t, ev
 
             n = len(hf)
-            copied = [None, None]
+            copied = [None] * NB
             e0.record()
             up.wait_stream(main)
             nxt = upload(0)
@@ -472,17 +473,17 @@ def run_ours(args):
                     nxt = (hf[i + 1].to(dev, non_blocking=True), torch.cuda.Event())
                     nxt[1].record(main)
                 s2 = dec.step(fdev)
-                if copied[i % 2] is not None:       # frame i-2's read-back of this buffer pair
-                    main.wait_event(copied[i % 2])
-                export_reference_layout(s2.layers, dev_r[i % 2], dev_T[i % 2])
+                if copied[i % NB] is not None:      # frame i-NB's read-back of this buffer pair
+                    main.wait_event(copied[i % NB])
+                export_reference_layout(s2.layers, dev_r[i % NB], dev_T[i % NB])
                 done = torch.cuda.Event()
                 done.record()
                 side.wait_event(done)
                 with torch.cuda.stream(side):
-                    out_host[i % 2][0].copy_(dev_r[i % 2], non_blocking=True)
-                    out_host[i % 2][1].copy_(dev_T[i % 2], non_blocking=True)
-                    copied[i % 2] = torch.cuda.Event()
-                    copied[i % 2].record(side)
+                    out_host[i % NB][0].copy_(dev_r[i % NB], non_blocking=True)
+                    out_host[i % NB][1].copy_(dev_T[i % NB], non_blocking=True)
+                    copied[i % NB] = torch.cuda.Event()
+                    copied[i % NB].record(side)
             main.wait_stream(side)
             e1.record()
             torch.cuda.synchronize()
