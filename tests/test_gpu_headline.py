@@ -94,13 +94,14 @@ def _frame1_state(clip, s0, seed):
     return st, img1, oaux
 
 
-@pytest.mark.parametrize("K", [8, 4, 12])
-def test_headline_1080p_operators_vs_oracle(K):
+@pytest.mark.parametrize("H,W,K", [(1080, 1920, 8), (1080, 1920, 4), (1080, 1920, 12), (2160, 3840, 8)])
+def test_headline_operators_vs_oracle(H, W, K):
     """Energies, -J^T F, diag(J^T J), J^T J p and PCG(16) of the NT=K+1
-    kernels at 1920x1080 with temporal partners (K=8: the bench's NT=9
-    instantiations; K=4 and K=12: the size sweep's)."""
+    kernels with temporal partners: 1920x1080 K=8 (the bench's NT=9
+    instantiations), K=4 and K=12 (the size sweep's), and 3840x2160 K=8
+    (configs[3]'s frame on one GPU)."""
     from paper_1908_01961_b200.energy import assemble_blocks, to_reference_vector
-    clip, dec, s0 = _streaming_setup(1080, 1920, K, seed=0)
+    clip, dec, s0 = _streaming_setup(H, W, K, seed=0)
     st, img1, oaux = _frame1_state(clip, s0, seed=1)
     r0, T0 = _host(st.layers.r), _host(st.layers.T)
     sysm = CO.System(img1, clip.colors, oaux, O.Weights())
