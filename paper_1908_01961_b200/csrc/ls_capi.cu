@@ -243,7 +243,10 @@ static void set_geometry(ls_ctx* c) {
   c->grid_pcg = std::max(1, std::min({c->ntiles, c->nsm * std::max(1, pcg_apply_grid_limit(c->NT)), kMaxBlocks}));
   const int64_t M = (int64_t)c->U * rows * c->W;
   const int64_t upd_blocks = (M / 4 + kThreads - 1) / kThreads;
-  c->grid_update = (int)std::max<int64_t>(1, std::min<int64_t>({upd_blocks, (int64_t)c->nsm * std::max(1, update_grid_limit()), (int64_t)kMaxBlocks}));
+  // LS_UPD_GRID: resident CTAs per SM of the streaming PCG update (A/B; default: its occupancy)
+  const char* ug = std::getenv("LS_UPD_GRID");
+  const int upd_per_sm = ug ? std::max(1, std::atoi(ug)) : std::max(1, update_grid_limit());
+  c->grid_update = (int)std::max<int64_t>(1, std::min<int64_t>({upd_blocks, (int64_t)c->nsm * upd_per_sm, (int64_t)kMaxBlocks}));
   c->grid_dense = std::max(1, std::min(c->nsm * 8, (rows * c->W + 63) / 64));
 }
 
